@@ -1,0 +1,252 @@
+// api.cpp -- the C ABI of libcapsconv (include/capsconv.h): validation,
+// shape law, workspace query, path dispatch, error mapping.
+//
+// Every argument is validated before anything is enqueued, so a non-OK
+// status other than CAPSCONV_ERR_CUDA leaves all buffers untouched.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace capsconv {
+
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_path_override{CAPSCONV_PATH_AUTO};
+static thread_local std::string t_last_error;
+
+void note_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+static capsconv_status_t fail(capsconv_status_t st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static capsconv_status_t fail(capsconv_status_t st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_last_error = buf;
+    return st;
+}
+
+const DeviceInfo &device_info() {
+    // Cached per current device (the common case is one device per process).
+    static thread_local DeviceInfo info;
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        info = DeviceInfo{};
+        return info;
+    }
+    if (info.device != dev) {
+        DeviceInfo d;
+        d.device = dev;
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) d.num_sms = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess) d.cc_major = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess) d.cc_minor = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess)
+            d.smem_optin = (size_t)v;
+        cudaGetLastError();
+        info = d;
+    }
+    return info;
+}
+
+// Product of extents with overflow detection.
+static bool mul_ok(int64_t a, int64_t b, int64_t *out) {
+    if (a > 0 && b > std::numeric_limits<int64_t>::max() / a) return false;
+    *out = a * b;
+    return true;
+}
+
+static capsconv_status_t make_problem(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                      int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                                      int64_t s, Problem *p) {
+    if (dt != CAPSCONV_F32 && dt != CAPSCONV_BF16) return fail(CAPSCONV_ERR_DTYPE, "unknown dtype %d", (int)dt);
+    if (s < 1) return fail(CAPSCONV_ERR_STRIDE, "stride %lld < 1", (long long)s);
+    const int64_t ext[] = {B, H, W, C, Cout, KH, KW, D1, D2, D3};
+    const char *names[] = {"B", "H", "W", "C", "Cout", "KH", "KW", "D1", "D2", "D3"};
+    for (int i = 0; i < 10; ++i)
+        if (ext[i] < 1) return fail(CAPSCONV_ERR_SHAPE, "extent %s = %lld < 1", names[i], (long long)ext[i]);
+    if (KH > H || KW > W)
+        return fail(CAPSCONV_ERR_SHAPE, "kernel %lldx%lld larger than input %lldx%lld", (long long)KH,
+                    (long long)KW, (long long)H, (long long)W);
+    p->dt = dt;
+    p->B = B; p->H = H; p->W = W; p->C = C; p->Cout = Cout;
+    p->KH = KH; p->KW = KW; p->D1 = D1; p->D2 = D2; p->D3 = D3; p->s = s;
+    p->Ho = (H - KH) / s + 1;
+    p->Wo = (W - KW) / s + 1;
+    // Element counts (and their byte sizes) must fit comfortably in int64.
+    int64_t n = 1;
+    const int64_t in_f[] = {B, H, W, C, D1, D2, 8};
+    for (int64_t f : in_f)
+        if (!mul_ok(n, f, &n)) return fail(CAPSCONV_ERR_OVERFLOW, "input element count overflows int64");
+    n = 1;
+    const int64_t out_f[] = {B, p->Ho, p->Wo, Cout, D1, D3, 8};
+    for (int64_t f : out_f)
+        if (!mul_ok(n, f, &n)) return fail(CAPSCONV_ERR_OVERFLOW, "output element count overflows int64");
+    n = 1;
+    const int64_t k_f[] = {KH, KW, C, Cout, D2, D3, 8};
+    for (int64_t f : k_f)
+        if (!mul_ok(n, f, &n)) return fail(CAPSCONV_ERR_OVERFLOW, "kernel element count overflows int64");
+    // Grid limits of the SIMT path: one thread per output element at most.
+    if (p->n_in() > (int64_t)1 << 40 || p->n_out() > (int64_t)1 << 40)
+        return fail(CAPSCONV_ERR_OVERFLOW, "problem exceeds 2^40 elements per tensor");
+    return CAPSCONV_OK;
+}
+
+static capsconv_path_t choose_path(capsconv_op_t op, const Problem &p) {
+    const int ov = g_path_override.load();
+    if (ov == CAPSCONV_PATH_SIMT) return CAPSCONV_PATH_SIMT;
+    if (mma_supported(op, p)) return CAPSCONV_PATH_MMA;
+    return CAPSCONV_PATH_SIMT;
+}
+
+static size_t workspace_for(capsconv_op_t op, const Problem &p) {
+    if (choose_path(op, p) == CAPSCONV_PATH_MMA) {
+        // The MMA path falls back to SIMT for misaligned pointers, so the
+        // workspace covers both.
+        size_t a = mma_workspace_bytes(op, p), b = simt_workspace_bytes(op, p);
+        return a > b ? a : b;
+    }
+    return simt_workspace_bytes(op, p);
+}
+
+static capsconv_status_t check_device() {
+    const DeviceInfo &d = device_info();
+    if (d.device < 0) return fail(CAPSCONV_ERR_DEVICE, "no CUDA device available");
+    if (d.cc_major != 10 || d.cc_minor != 0)
+        return fail(CAPSCONV_ERR_DEVICE, "device %d is sm_%d%d; libcapsconv is built for sm_100a only", d.device,
+                    d.cc_major, d.cc_minor);
+    return CAPSCONV_OK;
+}
+
+static bool aligned16(const void *a) { return ((uintptr_t)a & 15u) == 0; }
+
+static capsconv_status_t finish(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return fail(CAPSCONV_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    t_last_error.clear();
+    return CAPSCONV_OK;
+}
+
+}  // namespace capsconv
+
+using namespace capsconv;
+
+extern "C" {
+
+capsconv_status_t capsconv_output_dims(int64_t H, int64_t W, int64_t KH, int64_t KW, int64_t stride, int64_t *Ho,
+                                       int64_t *Wo) {
+    if (!Ho || !Wo) return fail(CAPSCONV_ERR_NULL, "Ho/Wo output pointer is NULL");
+    if (stride < 1) return fail(CAPSCONV_ERR_STRIDE, "stride %lld < 1", (long long)stride);
+    if (H < 1 || W < 1 || KH < 1 || KW < 1 || KH > H || KW > W)
+        return fail(CAPSCONV_ERR_SHAPE, "invalid spatial extents H=%lld W=%lld KH=%lld KW=%lld", (long long)H,
+                    (long long)W, (long long)KH, (long long)KW);
+    *Ho = (H - KH) / stride + 1;
+    *Wo = (W - KW) / stride + 1;
+    return CAPSCONV_OK;
+}
+
+capsconv_status_t capsconv_workspace_bytes(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W,
+                                           int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2,
+                                           int64_t D3, int64_t stride, size_t *bytes) {
+    if (!bytes) return fail(CAPSCONV_ERR_NULL, "bytes pointer is NULL");
+    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
+    Problem p;
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, &p);
+    if (st) return st;
+    *bytes = workspace_for(op, p);
+    return CAPSCONV_OK;
+}
+
+capsconv_status_t capsconv_select_path(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W,
+                                       int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2,
+                                       int64_t D3, int64_t stride, capsconv_path_t *path) {
+    if (!path) return fail(CAPSCONV_ERR_NULL, "path pointer is NULL");
+    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
+    Problem p;
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, &p);
+    if (st) return st;
+    *path = choose_path(op, p);
+    return CAPSCONV_OK;
+}
+
+capsconv_status_t capsconv_set_path_override(capsconv_path_t path) {
+    if (path != CAPSCONV_PATH_AUTO && path != CAPSCONV_PATH_SIMT && path != CAPSCONV_PATH_MMA)
+        return fail(CAPSCONV_ERR_DTYPE, "unknown path %d", (int)path);
+    g_path_override.store((int)path);
+    return CAPSCONV_OK;
+}
+
+#define CAPSCONV_PROLOGUE(OP, A, B_, OUT)                                                                     \
+    Problem p;                                                                                                \
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, &p);                \
+    if (st) return st;                                                                                        \
+    if (!(A) || !(B_) || !(OUT)) return fail(CAPSCONV_ERR_NULL, "a tensor pointer is NULL");                  \
+    const size_t need = workspace_for(OP, p);                                                                 \
+    if (workspace_bytes < need)                                                                               \
+        return fail(CAPSCONV_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);     \
+    if (need && !workspace) return fail(CAPSCONV_ERR_NULL, "workspace is NULL but %zu bytes are required", need); \
+    st = check_device();                                                                                      \
+    if (st) return st;                                                                                        \
+    cudaStream_t cs = (cudaStream_t)stream;                                                                   \
+    const bool mma = choose_path(OP, p) == CAPSCONV_PATH_MMA && aligned16(A) && aligned16(B_) &&             \
+                     aligned16(OUT) && (need == 0 || aligned16(workspace));
+
+capsconv_status_t capsconv_fwd(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                               int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                               const void *I, const void *K, void *O, void *workspace, size_t workspace_bytes,
+                               capsconv_stream_t stream) {
+    CAPSCONV_PROLOGUE(CAPSCONV_OP_FWD, I, K, O)
+    cudaError_t e = mma ? mma_fwd(p, I, K, O, workspace, workspace_bytes, cs) : simt_fwd(p, I, K, O, cs);
+    return finish(e, "capsconv_fwd");
+}
+
+capsconv_status_t capsconv_bwd_data(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                                    int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                                    const void *dO, const void *K, void *dI, void *workspace,
+                                    size_t workspace_bytes, capsconv_stream_t stream) {
+    CAPSCONV_PROLOGUE(CAPSCONV_OP_BWD_DATA, dO, K, dI)
+    cudaError_t e =
+        mma ? mma_bwd_data(p, dO, K, dI, workspace, workspace_bytes, cs) : simt_bwd_data(p, dO, K, dI, cs);
+    return finish(e, "capsconv_bwd_data");
+}
+
+capsconv_status_t capsconv_bwd_kernel(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                      int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                                      int64_t stride, const void *I, const void *dO, float *dK, void *workspace,
+                                      size_t workspace_bytes, capsconv_stream_t stream) {
+    CAPSCONV_PROLOGUE(CAPSCONV_OP_BWD_KERNEL, I, dO, dK)
+    cudaError_t e = mma ? mma_bwd_kernel(p, I, dO, dK, workspace, workspace_bytes, cs)
+                        : simt_bwd_kernel(p, I, dO, dK, workspace, workspace_bytes, cs);
+    return finish(e, "capsconv_bwd_kernel");
+}
+
+const char *capsconv_status_string(capsconv_status_t s) {
+    switch (s) {
+        case CAPSCONV_OK: return "CAPSCONV_OK";
+        case CAPSCONV_ERR_NULL: return "CAPSCONV_ERR_NULL: a required pointer is NULL";
+        case CAPSCONV_ERR_SHAPE: return "CAPSCONV_ERR_SHAPE: extent < 1 or kernel larger than input";
+        case CAPSCONV_ERR_STRIDE: return "CAPSCONV_ERR_STRIDE: stride < 1";
+        case CAPSCONV_ERR_DTYPE: return "CAPSCONV_ERR_DTYPE: unknown dtype, op or path";
+        case CAPSCONV_ERR_WORKSPACE: return "CAPSCONV_ERR_WORKSPACE: workspace too small";
+        case CAPSCONV_ERR_OVERFLOW: return "CAPSCONV_ERR_OVERFLOW: element count or index range too large";
+        case CAPSCONV_ERR_DEVICE: return "CAPSCONV_ERR_DEVICE: no sm_100 CUDA device";
+        case CAPSCONV_ERR_CUDA: return "CAPSCONV_ERR_CUDA: CUDA launch/runtime error";
+    }
+    return "CAPSCONV_ERR_UNKNOWN";
+}
+
+const char *capsconv_last_error(void) { return t_last_error.c_str(); }
+
+uint64_t capsconv_launch_count(void) { return g_launches.load(); }
+
+const char *capsconv_version(void) { return "0.1.0"; }
+
+}  // extern "C"

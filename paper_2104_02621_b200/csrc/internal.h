@@ -1,0 +1,56 @@
+// internal.h -- shared declarations of libcapsconv's CUDA path (product code;
+// nothing here is shared with oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "capsconv.h"
+
+namespace capsconv {
+
+// One validated problem: the extents of capsconv.h plus the derived output size.
+struct Problem {
+    capsconv_dtype_t dt;
+    int64_t B, H, W, C, Cout, KH, KW, D1, D2, D3, s;
+    int64_t Ho, Wo;
+
+    size_t elem() const { return dt == CAPSCONV_BF16 ? 2 : 4; }
+    int64_t n_in() const { return B * H * W * C * D1 * D2; }
+    int64_t n_out() const { return B * Ho * Wo * Cout * D1 * D3; }
+    int64_t n_k() const { return KH * KW * C * Cout * D2 * D3; }
+    int64_t n_pix_out() const { return B * Ho * Wo; }
+};
+
+// Device facts, cached once per device.
+struct DeviceInfo {
+    int device = -1;
+    int num_sms = 148;
+    int cc_major = 0, cc_minor = 0;
+    size_t smem_optin = 0;
+};
+const DeviceInfo &device_info();
+
+// Counts kernels enqueued by the library (capsconv_launch_count()).
+void note_launches(int n);
+
+// ---------------------------------------------------------------- SIMT path
+size_t simt_workspace_bytes(capsconv_op_t op, const Problem &p);
+cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, cudaStream_t st);
+cudaError_t simt_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, cudaStream_t st);
+cudaError_t simt_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK,
+                            void *ws, size_t ws_bytes, cudaStream_t st);
+
+// ---------------------------------------------------------------- tcgen05 (MMA) path
+// Returns true when the MMA path can take the problem (alignment excluded).
+bool mma_supported(capsconv_op_t op, const Problem &p);
+size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p);
+cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O,
+                    void *ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *dI,
+                         void *ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t mma_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK,
+                           void *ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace capsconv

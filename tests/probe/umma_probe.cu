@@ -1,0 +1,107 @@
+// umma_probe.cu -- test-only probe of the tcgen05 descriptor conventions in
+// csrc/umma.cuh: one CTA computes D = A(MxK) * B(NxK)^T with A and B staged in
+// shared memory in the canonical no-swizzle K-major or MN-major layouts,
+// including a start-address shift (the tap shift the capsule kernels use).
+#include <cuda_bf16.h>
+#include "umma.cuh"
+
+using namespace capsconv::umma;
+
+// A: global [RA][K] row-major (RA >= 128 + shift rows for K-major shifts,
+//    or K + kshift columns for MN-major k-shifts), B: global [N][K].
+// a_mn: 0 K-major, 1 MN-major.  Elements are 16-bit (bf16) or 32-bit (tf32).
+template <typename T>
+__global__ void probe_kernel(const T *A, const T *B, float *D, int RA, int KA, int N, int K, int a_mn, int b_mn,
+                             int shift) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    constexpr int E = sizeof(T);          // bytes per element
+    constexpr int PER16 = 16 / E;         // elements per 16-byte row
+    const int tid = threadIdx.x;
+    uint8_t *sA = smem;
+    const int RApad = (RA + 7) / 8 * 8;
+    const int KApad = (KA + 7) / 8 * 8;
+    // A layout
+    uint32_t a_lbo, a_sbo;
+    if (!a_mn) {  // K-major: rows at 16 B, row groups SBO=128, k-chunks LBO = RApad*16
+        a_lbo = RApad * 16; a_sbo = 128;
+        for (int i = tid; i < RA * KA; i += blockDim.x) {
+            int r = i / KA, k = i % KA;
+            *(T *)(sA + (k / PER16) * a_lbo + r * 16 + (k % PER16) * E) = A[i];
+        }
+    } else {      // MN-major: k rows at 16 B (k-groups LBO=128), m-groups at SBO = KApad*16
+        a_lbo = 128; a_sbo = KApad * 16;
+        for (int i = tid; i < RA * KA; i += blockDim.x) {
+            int m = i / KA, k = i % KA;
+            *(T *)(sA + (m / PER16) * a_sbo + (m % PER16) * E + k * 16) = A[i];
+        }
+    }
+    uint8_t *sB = smem + 65536;
+    uint32_t b_lbo, b_sbo;
+    const int Npad = (N + 7) / 8 * 8;
+    if (!b_mn) {
+        b_lbo = Npad * 16; b_sbo = 128;
+        for (int i = tid; i < N * K; i += blockDim.x) {
+            int n = i / K, k = i % K;
+            *(T *)(sB + (k / PER16) * b_lbo + n * 16 + (k % PER16) * E) = B[i];
+        }
+    } else {
+        b_lbo = 128; b_sbo = ((K + 7) / 8 * 8) * 16;
+        for (int i = tid; i < N * K; i += blockDim.x) {
+            int n = i / K, k = i % K;
+            *(T *)(sB + (n / PER16) * b_sbo + (n % PER16) * E + k * 16) = B[i];
+        }
+    }
+    if (tid < 32) tmem_alloc<256>(&tmem_base);
+    if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+    fence_proxy_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tm = tmem_base;
+    if (tid == 0) {
+        const uint32_t idesc = (E == 2) ? idesc_bf16(128, N, a_mn, b_mn) : idesc_tf32(128, N, a_mn, b_mn);
+        const int ksteps = K / (32 / E);   // 16 bf16 or 8 tf32 per MMA = 2 chunks
+        for (int ks = 0; ks < ksteps; ++ks) {
+            uint32_t a_addr, b_addr;
+            // K-major: a K-step is (32/E)/PER16 = 2 chunks of 16 B; MN-major: (32/E)/8 k-groups.
+            const int a_adv = a_mn ? (32 / E) / 8 : 2, b_adv = b_mn ? (32 / E) / 8 : 2;
+            a_addr = smem_u32(sA) + shift * 16 + ks * a_adv * a_lbo;   // shift: rows (K-major) / k-rows (MN)
+            b_addr = smem_u32(sB) + ks * b_adv * b_lbo;
+            uint64_t ad = smem_desc(a_addr, a_lbo, a_sbo);
+            uint64_t bd = smem_desc(b_addr, b_lbo, b_sbo);
+            if (E == 2) mma_bf16_ss(tm, ad, bd, idesc, ks > 0);
+            else mma_tf32_ss(tm, ad, bd, idesc, ks > 0);
+        }
+        mma_commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    fence_after_sync();
+    const int warp = tid / 32, lane = tid % 32;
+    const int row = warp * 32 + lane;
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        float v[8];
+        tmem_ld8(tm + ((uint32_t)(warp * 32) << 16) + c0, v);
+        tmem_wait_ld();
+        for (int j = 0; j < 8 && c0 + j < N; ++j) D[row * N + c0 + j] = v[j];
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc<256>(tm);
+}
+
+extern "C" int umma_probe(int tf32, const void *A, const void *B, float *D, int RA, int KA, int N, int K, int a_mn,
+                          int b_mn, int shift) {
+    const size_t smem = 65536 * 2;
+    if (tf32) {
+        cudaFuncSetAttribute(probe_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        probe_kernel<float><<<1, 128, smem>>>((const float *)A, (const float *)B, D, RA, KA, N, K, a_mn, b_mn, shift);
+    } else {
+        cudaFuncSetAttribute(probe_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        probe_kernel<__nv_bfloat16><<<1, 128, smem>>>((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, D, RA, KA,
+                                                       N, K, a_mn, b_mn, shift);
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    return (int)e;
+}

@@ -1,0 +1,72 @@
+"""Probe of the tcgen05 descriptor conventions (csrc/umma.cuh) on the GPU:
+D = A * B^T through shared-memory operands in canonical no-swizzle layouts,
+compared with a float64 matmul of the same bf16 / fp32 values."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PROBE = os.path.join(HERE, "probe")
+LIB = os.path.join(PROBE, "libumma_probe.so")
+SRC = os.path.join(PROBE, "umma_probe.cu")
+CSRC = os.path.join(os.path.dirname(HERE), "paper_2104_02621_b200", "csrc")
+
+
+@pytest.fixture(scope="module")
+def probe():
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC) or \
+            os.path.getmtime(LIB) < os.path.getmtime(os.path.join(CSRC, "umma.cuh")):
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17", "-Xcompiler",
+                        "-fPIC", "-shared", "-I", CSRC, "-I", os.path.join(os.path.dirname(HERE), "include"),
+                        "-o", LIB, SRC], check=True)
+    lib = ctypes.CDLL(LIB)
+    lib.umma_probe.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 7
+    lib.umma_probe.restype = ctypes.c_int
+    return lib
+
+
+CASES = [
+    # tf32, a_mn, b_mn, N, K, shift
+    (0, 0, 0, 32, 32, 0),
+    (0, 0, 0, 32, 32, 4),
+    (0, 0, 0, 32, 32, 1),
+    (0, 0, 0, 32, 64, 12),
+    (0, 0, 0, 48, 32, 0),
+    (0, 0, 0, 128, 48, 8),
+    (0, 0, 0, 256, 16, 0),
+    (0, 1, 0, 32, 32, 0),
+    (0, 1, 0, 64, 32, 4),
+    (0, 0, 1, 32, 32, 0),
+    (0, 1, 1, 32, 64, 0),
+    (1, 0, 0, 32, 32, 0),
+    (1, 0, 0, 64, 32, 4),
+    (1, 1, 0, 32, 16, 0),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "tf32%d_amn%d_bmn%d_N%d_K%d_sh%d" % c)
+def test_umma_layouts(probe, case):
+    tf32, a_mn, b_mn, N, K, shift = case
+    dt = torch.float32 if tf32 else torch.bfloat16
+    g = torch.Generator().manual_seed(1)
+    if a_mn:
+        RA, KA = 128, K + shift       # shift along K (k rows)
+    else:
+        RA, KA = 128 + shift, K       # shift along M (rows)
+    A = (torch.randint(-4, 5, (RA, KA), generator=g).float() / 4).to(dt)
+    B = (torch.randint(-4, 5, (N, K), generator=g).float() / 4).to(dt)
+    Ad, Bd = A.cuda(), B.cuda()
+    D = torch.zeros(128, N, dtype=torch.float32, device="cuda")
+    rc = probe.umma_probe(tf32, Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), RA, KA, N, K, a_mn, b_mn, shift)
+    assert rc == 0, "CUDA error %d" % rc
+    if a_mn:
+        Aeff = A[:, shift:shift + K]
+    else:
+        Aeff = A[shift:shift + 128, :]
+    ref = Aeff.double() @ B.double().T
+    torch.testing.assert_close(D.cpu().double(), ref, rtol=0, atol=0)
