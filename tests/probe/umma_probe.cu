@@ -12,19 +12,25 @@ using namespace capsconv::umma;
 // a_mn: 0 K-major, 1 MN-major.  Elements are 16-bit (bf16) or 32-bit (tf32).
 template <typename T>
 __global__ void probe_kernel(const T *A, const T *B, float *D, int RA, int KA, int N, int K, int a_mn, int b_mn,
-                             int shift) {
+                             int shift, int swz) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tmem_base;
     constexpr int E = sizeof(T);          // bytes per element
     constexpr int PER16 = 16 / E;         // elements per 16-byte row
     const int tid = threadIdx.x;
-    uint8_t *sA = smem;
+    uint8_t *sA = smem + ((1024 - (smem_u32(smem) & 1023)) & 1023);
     const int RApad = (RA + 7) / 8 * 8;
     const int KApad = (KA + 7) / 8 * 8;
     // A layout
     uint32_t a_lbo, a_sbo;
-    if (!a_mn) {  // K-major: rows at 16 B, row groups SBO=128, k-chunks LBO = RApad*16
+    if (swz) {    // SWIZZLE_128B K-major: 128-byte rows, chunk ^ (row % 8); K == 64
+        a_lbo = 16; a_sbo = 1024;
+        for (int i = tid; i < RA * KA; i += blockDim.x) {
+            int r = i / KA, k = i % KA;
+            *(T *)(sA + (r / 8) * 1024 + (r % 8) * 128 + (((k * E / 16) ^ (r % 8)) * 16) + (k * E % 16)) = A[i];
+        }
+    } else if (!a_mn) {  // K-major: rows at 16 B, row groups SBO=128, k-chunks LBO = RApad*16
         a_lbo = RApad * 16; a_sbo = 128;
         for (int i = tid; i < RA * KA; i += blockDim.x) {
             int r = i / KA, k = i % KA;
@@ -37,10 +43,16 @@ __global__ void probe_kernel(const T *A, const T *B, float *D, int RA, int KA, i
             *(T *)(sA + (m / PER16) * a_sbo + (m % PER16) * E + k * 16) = A[i];
         }
     }
-    uint8_t *sB = smem + 65536;
+    uint8_t *sB = sA + 65536;
     uint32_t b_lbo, b_sbo;
     const int Npad = (N + 7) / 8 * 8;
-    if (!b_mn) {
+    if (swz) {
+        b_lbo = 16; b_sbo = 1024;
+        for (int i = tid; i < N * K; i += blockDim.x) {
+            int n = i / K, k = i % K;
+            *(T *)(sB + (n / 8) * 1024 + (n % 8) * 128 + (((k * E / 16) ^ (n % 8)) * 16) + (k * E % 16)) = B[i];
+        }
+    } else if (!b_mn) {
         b_lbo = Npad * 16; b_sbo = 128;
         for (int i = tid; i < N * K; i += blockDim.x) {
             int n = i / K, k = i % K;
@@ -71,6 +83,13 @@ __global__ void probe_kernel(const T *A, const T *B, float *D, int RA, int KA, i
             b_addr = smem_u32(sB) + ks * b_adv * b_lbo;
             uint64_t ad = smem_desc(a_addr, a_lbo, a_sbo);
             uint64_t bd = smem_desc(b_addr, b_lbo, b_sbo);
+            if (swz) {
+                a_addr = smem_u32(sA) + shift * 128 + ks * 32;
+                b_addr = smem_u32(sB) + ks * 32;
+                ad = smem_desc(a_addr, 16, 1024) | (2ull << 61);
+                bd = smem_desc(b_addr, 16, 1024) | (2ull << 61);
+                if (swz == 2) ad |= (uint64_t)((a_addr >> 7) & 7) << 49;   // base offset
+            }
             if (E == 2) mma_bf16_ss(tm, ad, bd, idesc, ks > 0);
             else mma_tf32_ss(tm, ad, bd, idesc, ks > 0);
         }
@@ -92,16 +111,85 @@ __global__ void probe_kernel(const T *A, const T *B, float *D, int RA, int KA, i
 }
 
 extern "C" int umma_probe(int tf32, const void *A, const void *B, float *D, int RA, int KA, int N, int K, int a_mn,
-                          int b_mn, int shift) {
-    const size_t smem = 65536 * 2;
+                          int b_mn, int shift, int swz) {
+    const size_t smem = 65536 * 2 + 1024;
     if (tf32) {
         cudaFuncSetAttribute(probe_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        probe_kernel<float><<<1, 128, smem>>>((const float *)A, (const float *)B, D, RA, KA, N, K, a_mn, b_mn, shift);
+        probe_kernel<float><<<1, 128, smem>>>((const float *)A, (const float *)B, D, RA, KA, N, K, a_mn, b_mn, shift, swz);
     } else {
         cudaFuncSetAttribute(probe_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         probe_kernel<__nv_bfloat16><<<1, 128, smem>>>((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, D, RA, KA,
-                                                       N, K, a_mn, b_mn, shift);
+                                                       N, K, a_mn, b_mn, shift, swz);
     }
     cudaError_t e = cudaDeviceSynchronize();
     return (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// Throughput microbenchmark: `iters` back-to-back 128xNx16 bf16 MMAs into one
+// accumulator, operands from shared memory (SS) or A from TMEM (TS).  All
+// CTAs run the same loop; returns cycles per MMA measured by CTA 0.
+__global__ void bench_kernel(int N, int iters, int a_tmem, int nacc, int lay, unsigned long long *cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 65536 / 4; i += blockDim.x) ((uint32_t *)smem)[i] = 0x3c003c00u;
+    if (tid < 32) tmem_alloc<512>(&tmem_base);
+    if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+    fence_proxy_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tm = tmem_base;
+    if (tid < 32) {
+        const uint32_t idesc = idesc_bf16(128, N, 0, 0);
+        const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
+        uint64_t ad = smem_desc(sa, lay == 1 ? 128 * 16 + 64 : 128 * 16, 128);
+        uint64_t bd = smem_desc(sb, lay == 1 ? 256 * 16 + 64 : 256 * 16, 128);
+        if (lay == 2) {
+            ad = smem_desc((sa + 1023) & ~1023u, 16, 1024) | (2ull << 61);
+            bd = smem_desc((sb + 1023) & ~1023u, 16, 1024) | (2ull << 61);
+        }
+        const uint32_t step = nacc > 1 ? (uint32_t)N : 0u;
+        unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; it += 8) {
+            if (elect_one()) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t dcol = tm + (uint32_t)(u & 1) * step;
+                    if (a_tmem) {
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dcol),
+                            "r"(tm + 384), "l"(bd), "r"(idesc), "r"(1));
+                    } else {
+                        mma_bf16_ss(dcol, ad, bd, idesc, 1);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(&bar);
+        __syncwarp();
+        mbar_wait(&bar, 0);
+        unsigned long long t1 = clock64();
+        if (blockIdx.x == 0 && tid == 0) *cycles = (t1 - t0);
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc<512>(tm);
+}
+
+extern "C" double umma_bench(int N, int iters, int a_tmem, int nblocks, int nacc, int lay) {
+    unsigned long long *d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 32768);
+    bench_kernel<<<nblocks, 128, 65536 + 32768>>>(N, iters, a_tmem, nacc, lay, d);
+    unsigned long long h = 0;
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return -1.0;
+    return (double)h / iters;
 }

@@ -25,33 +25,38 @@ def probe():
                         "-fPIC", "-shared", "-I", CSRC, "-I", os.path.join(os.path.dirname(HERE), "include"),
                         "-o", LIB, SRC], check=True)
     lib = ctypes.CDLL(LIB)
-    lib.umma_probe.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 7
+    lib.umma_probe.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 8
     lib.umma_probe.restype = ctypes.c_int
     return lib
 
 
 CASES = [
-    # tf32, a_mn, b_mn, N, K, shift
-    (0, 0, 0, 32, 32, 0),
-    (0, 0, 0, 32, 32, 4),
-    (0, 0, 0, 32, 32, 1),
-    (0, 0, 0, 32, 64, 12),
-    (0, 0, 0, 48, 32, 0),
-    (0, 0, 0, 128, 48, 8),
-    (0, 0, 0, 256, 16, 0),
-    (0, 1, 0, 32, 32, 0),
-    (0, 1, 0, 64, 32, 4),
-    (0, 0, 1, 32, 32, 0),
-    (0, 1, 1, 32, 64, 0),
-    (1, 0, 0, 32, 32, 0),
-    (1, 0, 0, 64, 32, 4),
-    (1, 1, 0, 32, 16, 0),
+    # tf32, a_mn, b_mn, N, K, shift, swz
+    (0, 0, 0, 32, 64, 0, 1),
+    (0, 0, 0, 32, 64, 4, 1),
+    (0, 0, 0, 32, 64, 4, 2),
+    (0, 0, 0, 64, 64, 3, 1),
+    (0, 0, 0, 64, 64, 3, 2),
+    (0, 0, 0, 32, 64, 8, 1),
+    (0, 0, 0, 32, 32, 0, 0),
+    (0, 0, 0, 32, 32, 4, 0),
+    (0, 0, 0, 32, 32, 1, 0),
+    (0, 0, 0, 32, 64, 12, 0),
+    (0, 0, 0, 48, 32, 0, 0),
+    (0, 0, 0, 128, 48, 8, 0),
+    (0, 0, 0, 256, 16, 0, 0),
+    (0, 1, 0, 32, 32, 0, 0),
+    (0, 1, 0, 64, 32, 4, 0),
+    (0, 0, 1, 32, 32, 0, 0),
+    (0, 1, 1, 32, 64, 0, 0),
+    (1, 0, 0, 32, 32, 0, 0),
+    (1, 0, 0, 64, 32, 4, 0),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: "tf32%d_amn%d_bmn%d_N%d_K%d_sh%d" % c)
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "tf32%d_amn%d_bmn%d_N%d_K%d_sh%d_swz%d" % c)
 def test_umma_layouts(probe, case):
-    tf32, a_mn, b_mn, N, K, shift = case
+    tf32, a_mn, b_mn, N, K, shift, swz = case
     dt = torch.float32 if tf32 else torch.bfloat16
     g = torch.Generator().manual_seed(1)
     if a_mn:
@@ -62,7 +67,7 @@ def test_umma_layouts(probe, case):
     B = (torch.randint(-4, 5, (N, K), generator=g).float() / 4).to(dt)
     Ad, Bd = A.cuda(), B.cuda()
     D = torch.zeros(128, N, dtype=torch.float32, device="cuda")
-    rc = probe.umma_probe(tf32, Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), RA, KA, N, K, a_mn, b_mn, shift)
+    rc = probe.umma_probe(tf32, Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), RA, KA, N, K, a_mn, b_mn, shift, swz)
     assert rc == 0, "CUDA error %d" % rc
     if a_mn:
         Aeff = A[:, shift:shift + K]
