@@ -1,16 +1,620 @@
-// mma.cu -- tcgen05 / TMEM implicit-GEMM path (placeholder until the kernels land).
+// mma.cu -- tcgen05 / TMEM path of libcapsconv: forward and data gradient as
+// one shifted-window implicit GEMM (conv_mma.cuh), plus host planning.
+//
+// Roles in a CTA (288 threads, persistent over work items):
+//   warps 0-3  producers: stage the source window of the current channel chunk
+//              into shared memory (16-byte coalesced loads; each 16 B holds
+//              two D1 rows of one capsule, stored as two 8-byte pieces into the
+//              K-major rows (pixel, d1) -- the D1 repack of SURVEY H1); one
+//              thread also streams the prepacked weights with bulk copies.
+//   warps 4-7  epilogue: TMEM -> registers -> bf16 -> capsule layout in HBM.
+//   warp 8     MMA issuer: for every tap, the same window at a different row
+//              offset; accumulators stay in TMEM across taps and chunks
+//              (the paper's output_reduce, becomes free).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "conv_mma.cuh"
 #include "internal.h"
+#include "umma.cuh"
 
 namespace capsconv {
+using namespace umma;
 
-bool mma_supported(capsconv_op_t, const Problem &) { return false; }
-size_t mma_workspace_bytes(capsconv_op_t, const Problem &) { return 0; }
-cudaError_t mma_fwd(const Problem &, const void *, const void *, void *, void *, size_t, cudaStream_t) {
-    return cudaErrorNotSupported;
+namespace {
+
+constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ void tmem_alloc_dyn(uint32_t *dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
 }
-cudaError_t mma_bwd_data(const Problem &, const void *, const void *, void *, void *, size_t, cudaStream_t) {
-    return cudaErrorNotSupported;
+__device__ __forceinline__ void tmem_dealloc_dyn(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
 }
+
+struct Item {
+    int g, ig, nt, ks;
+    int tile0, ntl;      // first M tile, tiles in this item
+    int c_begin, c_end;  // channel chunks
+};
+
+__device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
+    Item it;
+    int r = item;
+    it.ks = r % P.ksplit; r /= P.ksplit;
+    it.nt = r % P.n_ntiles; r /= P.n_ntiles;
+    it.ig = r % P.n_igroups;
+    it.g = r / P.n_igroups;
+    it.tile0 = it.ig * P.G;
+    it.ntl = min(P.G, P.n_mtiles - it.tile0);
+    it.c_begin = it.ks * P.nchunks / P.ksplit;
+    it.c_end = (it.ks + 1) * P.nchunks / P.ksplit;
+    return it;
+}
+
+__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+
+// ------------------------------------------------------------------ producers
+__device__ __forceinline__ void load_window(const ConvMma &P, const Item &it, int ch, uint32_t a_stage, int tid) {
+    const int cc = P.CC;
+    const int upp = 2 * cc;                       // 16-byte units per pixel in this chunk
+    const int total = P.npl * P.win_px * upp;
+    const int vbase = it.tile0 * kTilePix + P.og_offmin[it.g];
+    const int vtotal = P.Bn * P.Hg * P.Wg;
+    const int c_src0 = ch * cc;
+    const uint4 *src = reinterpret_cast<const uint4 *>(P.src);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    constexpr int kBatch = 8;
+    for (int L0 = tid; L0 < total; L0 += kProducerThreads * kBatch) {
+        uint4 v[kBatch];
+        uint32_t dst[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const int L = L0 + j * kProducerThreads;
+            v[j] = make_uint4(0, 0, 0, 0);
+            dst[j] = 0xFFFFFFFFu;
+            if (L < total) {
+                const int pix = (int)P.fd_units.div((uint32_t)L);
+                const int u2 = L - pix * upp;
+                const int c = u2 >> 1, i = u2 & 1;
+                int k = 0, vl = pix;
+                while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+                const int vv = vbase + vl;
+                dst[j] = a_stage + k * P.plane_bytes + (c >> 1) * P.a_lbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
+                         (c & 1) * 8u;
+                if (vv >= 0 && vv < vtotal && c_src0 + c < P.CS) {
+                    const uint32_t b = P.fd_HgWg.div((uint32_t)vv);
+                    const uint32_t rr = (uint32_t)vv - b * HgWg;
+                    const uint32_t Y = P.fd_Wg.div(rr);
+                    const uint32_t X = rr - Y * (uint32_t)P.Wg;
+                    const int sy = P.pl_s * (int)Y + P.pl_oy[k];
+                    const int sx = P.pl_s * (int)X + P.pl_ox[k];
+                    if (sy < P.src_vH && sx < P.src_vW) {
+                        const size_t pixel = ((size_t)b * P.src_H + sy) * P.src_W + sx;
+                        // 16-byte unit index: pixel * (CS*16*2/16) + channel*2 + i
+                        v[j] = __ldg(src + pixel * (size_t)(P.CS * 2) + (size_t)(c_src0 + c) * 2 + i);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (dst[j] != 0xFFFFFFFFu) {
+                st_shared_v2(dst[j], v[j].x, v[j].y);          // row d1 = 2i
+                st_shared_v2(dst[j] + 16u, v[j].z, v[j].w);    // row d1 = 2i + 1
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_constant__ ConvMma P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    uint64_t *a_full = bars;
+    uint64_t *a_empty = bars + kMaxStages;
+    uint64_t *b_full = bars + 2 * kMaxStages;
+    uint64_t *acc_full = bars + 3 * kMaxStages;
+    uint64_t *acc_empty = acc_full + 2;
+    uint64_t *b_res = acc_empty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + 512);
+    const uint32_t stage0 = smem_u32(smem_raw) + 1024;
+    const uint32_t stage_stride = P.a_stage_bytes + (P.b_resident ? 0u : P.b_stage_bytes);
+    const uint32_t bres_addr = stage0 + P.nstages * stage_stride;
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P.nstages; ++s) {
+            mbar_init(a_full + s, kProducerThreads);
+            mbar_init(a_empty + s, 1);
+            mbar_init(b_full + s, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(acc_full + i, 1);
+            mbar_init(acc_empty + i, kEpilogueThreads / 32);
+        }
+        mbar_init(b_res, 1);
+        mbar_fence_init();
+    }
+    if (warp == 8) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) {
+        // ================================================= producers
+        const int tid = threadIdx.x;
+        if (P.b_resident && tid == 0) {
+            const uint32_t bytes = (uint32_t)(P.og_t1[0] - P.og_t0[0]) * (P.CC / 2) * P.N_tile * 16;
+            mbar_arrive_expect_tx(b_res, bytes);
+            bulk_g2s_u32(bres_addr, P.wpack, bytes, b_res);
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            const Item it = decode_item(P, item);
+            for (int ch = it.c_begin; ch < it.c_end; ++ch) {
+                mbar_wait(a_empty + stage, phase ^ 1);
+                const uint32_t a_stage = stage0 + stage * stage_stride;
+                if (!P.b_resident && tid == 0) {
+                    const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
+                    const size_t blk = (size_t)(P.CC / 2) * P.N_tile * 16;
+                    const size_t off = (((size_t)it.nt * P.nchunks + ch) * P.ntaps + t0) * blk;
+                    const uint32_t bytes = (uint32_t)((t1 - t0) * blk);
+                    mbar_arrive_expect_tx(b_full + stage, bytes);
+                    bulk_g2s_u32(a_stage + P.a_stage_bytes, P.wpack + off, bytes, b_full + stage);
+                }
+                load_window(P, it, ch, a_stage, tid);
+                fence_proxy_async_smem();
+                mbar_arrive(a_full + stage);
+                if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp < 8) {
+        // ================================================= epilogue
+        const int wq = warp - 4;
+        const int row = wq * 32 + lane;
+        const int vtotal = P.Bn * P.Hg * P.Wg;
+        const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+        int abuf = 0;
+        uint32_t aphase = 0;
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            const Item it = decode_item(P, item);
+            mbar_wait(acc_full + abuf, aphase);
+            fence_after_sync();
+            for (int gi = 0; gi < it.ntl; ++gi) {
+                const int u = (it.tile0 + gi) * kTilePix + (row >> 2);
+                const int d1 = row & 3;
+                bool valid = u < vtotal;
+                size_t opix = 0;
+                if (valid) {
+                    const uint32_t b = P.fd_HgWg.div((uint32_t)u);
+                    const uint32_t rr = (uint32_t)u - b * HgWg;
+                    const uint32_t Y = P.fd_Wg.div(rr);
+                    const uint32_t X = rr - Y * (uint32_t)P.Wg;
+                    const int oy = P.og_s * (int)Y + P.og_oy[it.g];
+                    const int ox = P.og_s * (int)X + P.og_ox[it.g];
+                    valid = oy < P.out_H && ox < P.out_W;
+                    opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
+                }
+                const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)((abuf * P.G + gi) * P.N_tile);
+                for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
+                    float v[16];
+                    tmem_ld16(tcol + n0, v);
+                    tmem_wait_ld();
+                    if (P.ksplit == 1) {
+                        if (valid) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int ch = it.nt * (P.N_tile / 4) + n0 / 4 + j;
+                                if (ch < P.NCH) {
+                                    __nv_bfloat162 lo = __floats2bfloat162_rn(v[4 * j], v[4 * j + 1]);
+                                    __nv_bfloat162 hi = __floats2bfloat162_rn(v[4 * j + 2], v[4 * j + 3]);
+                                    uint2 w;
+                                    w.x = *reinterpret_cast<uint32_t *>(&lo);
+                                    w.y = *reinterpret_cast<uint32_t *>(&hi);
+                                    *reinterpret_cast<uint2 *>(P.out + (opix * P.NCH + ch) * 16 + d1 * 4) = w;
+                                }
+                            }
+                        }
+                    } else if (u < vtotal) {
+                        const size_t rows_total = (size_t)P.n_mtiles * 128;
+                        const size_t ntot = (size_t)P.n_ntiles * P.N_tile;
+                        float *dst = P.part + ((size_t)it.ks * rows_total + (size_t)u * 4 + d1) * ntot +
+                                     (size_t)it.nt * P.N_tile + n0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            reinterpret_cast<float4 *>(dst)[j] =
+                                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    }
+                }
+            }
+            fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + abuf);
+            if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+        }
+    } else {
+        // ================================================= MMA issuer (warp 8)
+        const uint32_t idesc = idesc_bf16(128, P.N_tile, 0, 0);
+        const uint32_t b_lbo = (uint32_t)P.N_tile * 16;
+        int stage = 0;
+        uint32_t phase = 0;
+        int abuf = 0;
+        uint32_t aphase = 0;
+        if (P.b_resident) mbar_wait(b_res, 0);
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            const Item it = decode_item(P, item);
+            mbar_wait(acc_empty + abuf, aphase ^ 1);
+            fence_after_sync();
+            const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
+            const int offmin = P.og_offmin[it.g];
+            for (int ch = it.c_begin; ch < it.c_end; ++ch) {
+                mbar_wait(a_full + stage, phase);
+                if (!P.b_resident) mbar_wait(b_full + stage, phase);
+                fence_after_sync();
+                const uint32_t a_stage = stage0 + stage * stage_stride;
+                const uint32_t b_base = P.b_resident ? bres_addr : a_stage + P.a_stage_bytes;
+                if (elect_one()) {
+                    for (int t = t0; t < t1; ++t) {
+                        const uint32_t a_tap = a_stage + P.tap_plane[t] * P.plane_bytes +
+                                               (uint32_t)(P.tap_shift[t] - offmin) * 64u;
+                        for (int j = 0; j < P.CC / 4; ++j) {
+                            const uint64_t bd =
+                                smem_desc(b_base + ((t - t0) * (P.CC / 2) + 2 * j) * b_lbo, b_lbo, 128);
+                            const uint32_t acc = (ch != it.c_begin || t != t0 || j != 0) ? 1u : 0u;
+                            for (int gi = 0; gi < it.ntl; ++gi) {
+                                const uint64_t ad =
+                                    smem_desc(a_tap + (uint32_t)(gi * kTilePix) * 64u + 2u * j * P.a_lbo, P.a_lbo, 128);
+                                mma_bf16_ss(tmem + (uint32_t)((abuf * P.G + gi) * P.N_tile), ad, bd, idesc, acc);
+                            }
+                        }
+                    }
+                    mma_commit(a_empty + stage);
+                }
+                __syncwarp();
+                if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+            }
+            if (elect_one()) mma_commit(acc_full + abuf);
+            __syncwarp();
+            if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+        }
+    }
+
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 8) {
+        fence_after_sync();
+        tmem_dealloc_dyn(tmem, P.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------ weight repack
+// B for tap t, chunk ch, N tile nt: [kc][n][8 elements], element (k = kc*8+e, n):
+//   forward : B[n=(c',d3)][k=(c,d2)]  = K[p][q][c][c'][d2][d3]
+//   dgrad   : B[n=(c,d2)][k=(c',d3)]  = K[p][q][c][c'][d2][d3]
+// K is viewed as [KHv][KWv][Cv][Coutv][4][4] (a full-extent layer is viewed as
+// 1x1 over Cv = KH*KW*C channels, the same memory).
+struct PackArgs {
+    const __nv_bfloat16 *K;
+    uint8_t *dst;
+    int KWv, Cv, Coutv;
+    int dgrad;
+    int CS, NCH, CC, nchunks, ntaps, N_tile, n_ntiles;
+    int tap_p[kMaxTaps], tap_q[kMaxTaps];
+};
+
+__global__ void __launch_bounds__(256) pack_weights_kernel(const __grid_constant__ PackArgs A) {
+    const int kcpc = A.CC / 2;
+    const long long total = (long long)A.n_ntiles * A.nchunks * A.ntaps * kcpc * A.N_tile;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    long long r = idx;
+    const int n = (int)(r % A.N_tile); r /= A.N_tile;
+    const int kc = (int)(r % kcpc); r /= kcpc;
+    const int t = (int)(r % A.ntaps); r /= A.ntaps;
+    const int ch = (int)(r % A.nchunks);
+    const int nt = (int)(r / A.nchunks);
+    const int ng = nt * A.N_tile + n;
+    const int oc = ng >> 2, dn = ng & 3;
+    const int p = A.tap_p[t], q = A.tap_q[t];
+    __align__(16) __nv_bfloat16 vals[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int kl = kc * 8 + e;
+        const int cs = ch * A.CC + (kl >> 2);
+        const int dk = kl & 3;
+        __nv_bfloat16 w = __float2bfloat16_rn(0.f);
+        if (cs < A.CS && oc < A.NCH) {
+            size_t off;
+            if (!A.dgrad)  // K[p][q][c=cs][c'=oc][d2=dk][d3=dn]
+                off = ((((size_t)p * A.KWv + q) * A.Cv + cs) * A.Coutv + oc) * 16 + dk * 4 + dn;
+            else           // K[p][q][c=oc][c'=cs][d2=dn][d3=dk]
+                off = ((((size_t)p * A.KWv + q) * A.Cv + oc) * A.Coutv + cs) * 16 + dn * 4 + dk;
+            w = A.K[off];
+        }
+        vals[e] = w;
+    }
+    *reinterpret_cast<uint4 *>(A.dst + idx * 16) = *reinterpret_cast<const uint4 *>(vals);
+}
+
+// ------------------------------------------------------------------ split-K finalize
+__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ ConvMma P) {
+    // one thread per (virtual row R = u*4 + d1, output channel)
+    const long long rows = (long long)P.Bn * P.Hg * P.Wg * 4;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * P.NCH) return;
+    const int ch = (int)(idx % P.NCH);
+    const long long R = idx / P.NCH;
+    const int u = (int)(R >> 2), d1 = (int)(R & 3);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const uint32_t b = P.fd_HgWg.div((uint32_t)u);
+    const uint32_t rr = (uint32_t)u - b * HgWg;
+    const uint32_t Y = P.fd_Wg.div(rr);
+    const uint32_t X = rr - Y * (uint32_t)P.Wg;
+    const int g = 0;  // split-K is planned only for single-group problems
+    const int oy = P.og_s * (int)Y + P.og_oy[g];
+    const int ox = P.og_s * (int)X + P.og_ox[g];
+    if (oy >= P.out_H || ox >= P.out_W) return;
+    const size_t rows_total = (size_t)P.n_mtiles * 128;
+    const size_t ntot = (size_t)P.n_ntiles * P.N_tile;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int ks = 0; ks < P.ksplit; ++ks) {
+        const float4 v = *reinterpret_cast<const float4 *>(P.part + ((size_t)ks * rows_total + R) * ntot + ch * 4);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const size_t opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t *>(&lo);
+    w.y = *reinterpret_cast<uint32_t *>(&hi);
+    *reinterpret_cast<uint2 *>(P.out + (opix * P.NCH + ch) * 16 + d1 * 4) = w;
+}
+
+// ------------------------------------------------------------------ planning
+struct Plan {
+    bool ok = false;
+    ConvMma P{};
+    PackArgs pack{};
+    size_t wpack_bytes = 0, part_bytes = 0;
+};
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+constexpr uint32_t kSmemLimit = 227 * 1024;
+
+Plan make_plan(const Problem &p, bool dgrad) {
+    Plan pl;
+    ConvMma &P = pl.P;
+    if (p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return pl;
+    const bool full_extent = (p.KH == p.H && p.KW == p.W);
+    const int s = (int)p.s;
+    P.Bn = (int)p.B;
+    int KWv, Cv, Coutv;
+    std::vector<int> tp, tq, tplane, tshift, tgroup;
+    if (full_extent) {
+        // fully-connected capsule layer viewed as a 1x1 convolution over
+        // KH*KW*C channels (reading R18)
+        const int Ceff = (int)(p.KH * p.KW * p.C);
+        KWv = 1; Cv = Ceff; Coutv = (int)p.Cout;
+        P.src_H = P.src_W = 1;
+        P.src_vH = P.src_vW = 1;
+        P.Hg = P.Wg = 1;
+        P.npl = 1; P.pl_s = 1; P.pl_oy[0] = P.pl_ox[0] = 0;
+        P.CS = dgrad ? (int)p.Cout : Ceff;
+        P.NCH = dgrad ? Ceff : (int)p.Cout;
+        P.nog = 1; P.og_s = 1; P.og_oy[0] = P.og_ox[0] = 0;
+        P.out_H = P.out_W = 1;
+        tp.push_back(0); tq.push_back(0); tplane.push_back(0); tshift.push_back(0); tgroup.push_back(0);
+    } else {
+        if (s > 2 || p.KH * p.KW > kMaxTaps) return pl;
+        if (dgrad && (p.KH < s || p.KW < s)) return pl;   // a dI phase with no taps
+        KWv = (int)p.KW; Cv = (int)p.C; Coutv = (int)p.Cout;
+        P.Hg = ceil_div(p.H, s);
+        P.Wg = ceil_div(p.W, s);
+        if (!dgrad) {
+            P.CS = (int)p.C; P.NCH = (int)p.Cout;
+            P.src_H = (int)p.H; P.src_W = (int)p.W;
+            P.src_vH = (int)p.H; P.src_vW = (int)p.W;
+            P.pl_s = s;
+            int plane_of[2][2] = {{-1, -1}, {-1, -1}};
+            P.npl = 0;
+            for (int pp = 0; pp < p.KH; ++pp)
+                for (int qq = 0; qq < p.KW; ++qq) {
+                    const int a = pp % s, b = qq % s;
+                    if (plane_of[a][b] < 0) {
+                        plane_of[a][b] = P.npl;
+                        P.pl_oy[P.npl] = a; P.pl_ox[P.npl] = b;
+                        ++P.npl;
+                    }
+                    tp.push_back(pp); tq.push_back(qq);
+                    tplane.push_back(plane_of[a][b]);
+                    tshift.push_back((pp / s) * P.Wg + qq / s);
+                    tgroup.push_back(0);
+                }
+            P.nog = 1; P.og_s = 1; P.og_oy[0] = P.og_ox[0] = 0;
+            P.out_H = (int)p.Ho; P.out_W = (int)p.Wo;
+        } else {
+            P.CS = (int)p.Cout; P.NCH = (int)p.C;
+            P.src_H = (int)p.Ho; P.src_W = (int)p.Wo;
+            P.src_vH = (int)p.Ho; P.src_vW = (int)p.Wo;
+            P.npl = 1; P.pl_s = 1; P.pl_oy[0] = P.pl_ox[0] = 0;
+            P.nog = s * s; P.og_s = s;
+            P.out_H = (int)p.H; P.out_W = (int)p.W;
+            for (int a = 0; a < s; ++a)
+                for (int b = 0; b < s; ++b) {
+                    const int g = a * s + b;
+                    P.og_oy[g] = a; P.og_ox[g] = b;
+                    for (int pp = a; pp < p.KH; pp += s)
+                        for (int qq = b; qq < p.KW; qq += s) {
+                            tp.push_back(pp); tq.push_back(qq); tplane.push_back(0);
+                            tshift.push_back(-((pp / s) * P.Wg + qq / s));
+                            tgroup.push_back(g);
+                        }
+                }
+        }
+    }
+    P.ntaps = (int)tp.size();
+    for (int t = 0; t < P.ntaps; ++t) {
+        P.tap_p[t] = tp[t]; P.tap_q[t] = tq[t]; P.tap_plane[t] = tplane[t]; P.tap_shift[t] = tshift[t];
+    }
+    int max_taps_g = 0, max_span = 0;
+    for (int g = 0; g < P.nog; ++g) {
+        int t0 = P.ntaps, t1 = 0, mn = 1 << 30, mx = -(1 << 30);
+        for (int t = 0; t < P.ntaps; ++t)
+            if (tgroup[t] == g) { t0 = std::min(t0, t); t1 = std::max(t1, t + 1); mn = std::min(mn, tshift[t]); mx = std::max(mx, tshift[t]); }
+        if (t1 <= t0) return pl;
+        P.og_t0[g] = t0; P.og_t1[g] = t1; P.og_offmin[g] = mn;
+        max_taps_g = std::max(max_taps_g, t1 - t0);
+        max_span = std::max(max_span, mx - mn);
+    }
+    const long long vtotal = (long long)P.Bn * P.Hg * P.Wg;
+    if (vtotal * 4 >= (1ll << 31) || (long long)P.src_H * P.src_W * P.Bn >= (1ll << 31)) return pl;
+
+    // ---- N tiling
+    const int N = P.NCH * 4;
+    P.n_ntiles = ceil_div(N, 256);
+    P.N_tile = ceil_div(ceil_div(N, P.n_ntiles), 16) * 16;
+    // ---- channel chunks, split-K, tiles per item, stages
+    P.CSpad = ceil_div(P.CS, 4) * 4;
+    P.n_mtiles = ceil_div(vtotal, kTilePix);
+    const int nsm = device_info().num_sms;
+    const long long base_items = (long long)P.nog * P.n_ntiles * P.n_mtiles;
+    std::vector<int> ccs;
+    for (int cc = P.CSpad; cc >= 4; cc -= 4)
+        if (P.CSpad % cc == 0 && (cc <= 64 || cc == P.CSpad)) ccs.push_back(cc);
+    bool found = false;
+    for (int cc : ccs) {
+        const int nchunks = P.CSpad / cc;
+        int ksplit = 1;
+        if (base_items < nsm && P.nog == 1) ksplit = std::min(nchunks, ceil_div(2 * nsm, base_items));
+        for (int G : {8, 4, 2, 1}) {
+            if (2 * G * P.N_tile > 512) continue;
+            const long long items = (long long)P.nog * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
+            if (G > 1 && items < 2 * nsm) continue;
+            const int win_px = ((G * kTilePix + max_span) + 1) & ~1;
+            const uint32_t a_lbo = (uint32_t)win_px * 64;
+            const uint32_t plane = (uint32_t)(cc / 2) * a_lbo;
+            const uint32_t a_stage = (uint32_t)P.npl * plane;
+            const uint32_t b_stage = (uint32_t)max_taps_g * (cc / 2) * P.N_tile * 16;
+            const bool bres = (P.nog == 1 && nchunks == 1 && P.n_ntiles == 1);
+            int best_st = 0;
+            for (int st = std::min(kMaxStages, 4); st >= 2; --st) {
+                const uint64_t bytes = 1024 + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
+                if (bytes <= kSmemLimit) { best_st = st; break; }
+            }
+            if (!best_st) continue;
+            if (a_lbo >= (1u << 18) || b_stage >= (1u << 20)) continue;
+            P.CC = cc; P.nchunks = nchunks; P.ksplit = ksplit; P.G = G;
+            P.win_px = win_px; P.a_lbo = a_lbo; P.plane_bytes = plane;
+            P.a_stage_bytes = a_stage; P.b_stage_bytes = b_stage;
+            P.b_resident = bres ? 1 : 0; P.nstages = best_st;
+            P.smem_bytes = 1024 + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
+            found = true;
+            break;
+        }
+        if (found) break;
+    }
+    if (!found) return pl;
+    P.n_igroups = ceil_div(P.n_mtiles, P.G);
+    P.n_items = P.nog * P.n_igroups * P.n_ntiles * P.ksplit;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * P.G * P.N_tile)) cols <<= 1;
+    P.tmem_cols = cols;
+    P.fd_Wg.init((uint32_t)P.Wg);
+    P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
+    P.fd_units.init((uint32_t)(2 * P.CC));
+
+    pl.wpack_bytes = align256((size_t)P.n_ntiles * P.nchunks * P.ntaps * (P.CC / 2) * P.N_tile * 16);
+    pl.part_bytes = P.ksplit > 1 ? align256((size_t)P.ksplit * P.n_mtiles * 128 * P.n_ntiles * P.N_tile * 4) : 0;
+
+    PackArgs &A = pl.pack;
+    A.KWv = KWv; A.Cv = Cv; A.Coutv = Coutv; A.dgrad = dgrad ? 1 : 0;
+    A.CS = P.CS; A.NCH = P.NCH; A.CC = P.CC; A.nchunks = P.nchunks; A.ntaps = P.ntaps;
+    A.N_tile = P.N_tile; A.n_ntiles = P.n_ntiles;
+    for (int t = 0; t < P.ntaps; ++t) { A.tap_p[t] = P.tap_p[t]; A.tap_q[t] = P.tap_q[t]; }
+    pl.ok = true;
+    return pl;
+}
+
+cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+    ConvMma &P = pl.P;
+    if (ws_bytes < pl.wpack_bytes + pl.part_bytes) return cudaErrorInvalidValue;
+    static const bool debug = getenv("CAPSCONV_DEBUG") != nullptr;
+    if (debug)
+        fprintf(stderr,
+                "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
+                "nchunks=%d ksplit=%d G=%d mtiles=%d items=%d win_px=%d stages=%d bres=%d smem=%u tmem=%u\n",
+                pl.pack.dgrad ? "dgrad" : "fwd", P.CS, P.NCH, P.Hg, P.Wg, P.npl, P.nog, P.ntaps, P.N_tile,
+                P.n_ntiles, P.CC, P.nchunks, P.ksplit, P.G, P.n_mtiles, P.n_items, P.win_px, P.nstages,
+                P.b_resident, P.smem_bytes, P.tmem_cols);
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    P.src = static_cast<const __nv_bfloat16 *>(src);
+    P.wpack = w;
+    P.out = static_cast<__nv_bfloat16 *>(out);
+    P.part = pl.part_bytes ? reinterpret_cast<float *>(w + pl.wpack_bytes) : nullptr;
+    pl.pack.K = static_cast<const __nv_bfloat16 *>(K);
+    pl.pack.dst = w;
+    const long long npack = (long long)pl.wpack_bytes / 16;
+    pack_weights_kernel<<<(unsigned)((npack + 255) / 256), 256, 0, st>>>(pl.pack);
+    note_launches(1);
+    static bool attr_set = false;  // per process; the attribute is per function
+    if (!attr_set) {
+        cudaFuncSetAttribute(conv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
+        attr_set = true;
+    }
+    const int grid = std::min(P.n_items, device_info().num_sms);
+    conv_mma_kernel<<<grid, kConvThreads, P.smem_bytes, st>>>(P);
+    note_launches(1);
+    if (P.ksplit > 1) {
+        const long long n = (long long)P.Bn * P.Hg * P.Wg * 4 * P.NCH;
+        finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P);
+        note_launches(1);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool mma_supported(capsconv_op_t op, const Problem &p) {
+    if (op == CAPSCONV_OP_BWD_KERNEL) return false;
+    return make_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
+}
+
+size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
+    if (op == CAPSCONV_OP_BWD_KERNEL) return 0;
+    Plan pl = make_plan(p, op == CAPSCONV_OP_BWD_DATA);
+    return pl.ok ? pl.wpack_bytes + pl.part_bytes : 0;
+}
+
+cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
+                    cudaStream_t st) {
+    Plan pl = make_plan(p, false);
+    if (!pl.ok) return cudaErrorNotSupported;
+    return run_plan(pl, I, K, O, ws, ws_bytes, st);
+}
+
+cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,
+                         cudaStream_t st) {
+    Plan pl = make_plan(p, true);
+    if (!pl.ok) return cudaErrorNotSupported;
+    return run_plan(pl, dO, K, dI, ws, ws_bytes, st);
+}
+
 cudaError_t mma_bwd_kernel(const Problem &, const void *, const void *, float *, void *, size_t, cudaStream_t) {
     return cudaErrorNotSupported;
 }
