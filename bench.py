@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the capsule convolution (arXiv 2104.02621) on B200.
+
+Metric (BASELINE.json): capsule-conv TFLOP/s fwd+bwd, and % of the HBM /
+tensor roofline.  Default workload (N = 1): BASELINE.json configs[4], the
+CapsNet stack -- 3 capsule conv layers + the FC capsule layer -- forward and
+backward on a global batch of 1024, bf16, synthetic seeded inputs and
+random-init weights.  With torchrun (N > 1) the global batch is sharded across
+the ranks and every layer's dK is all-reduced over NCCL ("strong" scaling).
+
+A step = forward of every layer + (dK, dI) of every layer in reverse order
+(+ the dK all-reduces).  Algorithmic flops per layer pass = 2*M*N*K with
+M = B*Ho*Wo*D1, N = Cout*D3, K = KH*KW*C*D2; fwd+bwd = 3x forward.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                        [--config stack|layer_s1|layer_s2|fc] [--dtype bf16|fp32]
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import capsinputs  # noqa: E402
+
+METRIC = "capsule-conv TFLOP/s fwd+bwd at 1/2/4/8 B200; % of tensor/HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="stack", choices=["stack", "layer_s1", "layer_s2", "fc"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-overlap", action="store_true", help="all-reduce on the compute stream")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- workload
+def workload(cfg: str, world: int):
+    """(specs, H, W, D, global_batch, name) of the benchmarked workload."""
+    from paper_2104_02621_b200.stack import LayerSpec
+    if cfg == "stack":
+        specs = [LayerSpec(*l) for l in capsinputs.STACK_LAYERS]
+        si = capsinputs.STACK_INPUT
+        return specs, si["H"], si["W"], si["D"], capsinputs.STACK_BATCH, "capsnet_stack_3conv_fc_b1024"
+    L = capsinputs.CONFIGS[cfg]
+    return [LayerSpec(L.C, L.Cout, L.KH, L.KW, L.stride)], L.H, L.W, L.D1, L.B, "single_layer_" + cfg
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "src": "measured"}
+    except Exception:
+        # fallback of /opt/skills/guides/B200_PROFILING.md
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+# ---------------------------------------------------------------- clocks
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- per-call timer
+class CallTimer:
+    """CUDA events around every C-ABI call of a step, on the launching stream."""
+
+    def __init__(self):
+        self.pending = []
+        self.open = {}
+
+    def begin(self, li, kind):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.open[(li, kind)] = e
+
+    def end(self, li, kind):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pending.append(((li, kind), self.open.pop((li, kind)), e))
+
+    def collect(self):
+        out = {}
+        for key, a, b in self.pending:
+            out.setdefault(key, []).append(a.elapsed_time(b))
+        self.pending = []
+        return out
+
+
+def pass_bytes(st, li, kind, elem):
+    """Algorithmic HBM bytes of one pass: every operand moved once
+    (SURVEY §8(d)): fwd |I|+|K|+|O|; dI |dO|+|K|+|dI|; dK |I|+|dO|+4|dK|."""
+    sp = st.specs[li]
+    h, w = st.hw[li]
+    ho, wo = st.hw[li + 1]
+    D = st.D
+    nI = st.batch * h * w * sp.C * D * D
+    nO = st.batch * ho * wo * sp.Cout * D * D
+    nK = sp.KH * sp.KW * sp.C * sp.Cout * D * D
+    if kind == "fwd":
+        return (nI + nK + nO) * elem
+    if kind == "dI":
+        return (nO + nK + nI) * elem
+    return (nI + nO) * elem + 4 * nK
+
+
+# ---------------------------------------------------------------- reference (oracle) arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    oracle.build()
+    specs, H, W, D, gbatch, name = workload(args.config, 1)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    flops_per_image, Ks, strides, layers = stack_oracle_setup(specs, H, W, D, dtype)
+
+    Xa, dYa = stack_oracle_inputs(layers, specs, H, W, D, gbatch, dtype, gbatch)
+
+    def one(b):
+        t0 = time.perf_counter()
+        oracle.stack_fwd_bwd(Xa[:b], Ks, strides, dYa[:b], dtype == torch.bfloat16)
+        return time.perf_counter() - t0
+
+    t1 = one(1)
+    budget = min(1.5, 120.0 / max(1, args.steps + args.warmup))
+    b = int(max(1, min(gbatch, budget / max(t1, 1e-6))))
+    for _ in range(args.warmup):
+        one(b)
+    ts = [one(b) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    tf = flops_per_image * b / t / 1e12
+    cores = oracle.num_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "global_batch": gbatch, "sample_batch": b, "io_dtype": args.dtype},
+        "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": "oracle (C, fp64, OpenMP) %s fwd+bwd on %d of %d images per step" % (name, b, gbatch)},
+        "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def stack_oracle_setup(specs, H, W, D, dtype):
+    import oracle
+    layers, Ks, strides = [], [], []
+    h, w = H, W
+    flops = 0
+    for li, sp in enumerate(specs):
+        L = capsinputs.Layer(B=1, H=h, W=w, C=sp.C, Cout=sp.Cout, KH=sp.KH, KW=sp.KW, D1=D, D2=D, D3=D,
+                             stride=sp.stride)
+        layers.append(L)
+        Ks.append(capsinputs.make_kernel(L, dtype=dtype, layer_idx=li).to(torch.float64).numpy())
+        strides.append(sp.stride)
+        ho, wo = oracle.output_dims(h, w, sp.KH, sp.KW, sp.stride)
+        flops += 3 * 2 * ho * wo * D * sp.Cout * D * sp.KH * sp.KW * sp.C * D
+        h, w = ho, wo
+    return flops, Ks, strides, layers
+
+
+def stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch):
+    import oracle
+    L0 = layers[0].with_batch(gbatch)
+    X = capsinputs.make_input(L0, dtype=dtype, batch=b).to(torch.float64).numpy()
+    h, w = H, W
+    for sp in specs:
+        h, w = oracle.output_dims(h, w, sp.KH, sp.KW, sp.stride)
+    dY = capsinputs.make_grad_output((b, h, w, specs[-1].Cout, D, D), dtype=dtype, layer_idx=len(specs)).to(
+        torch.float64).numpy()
+    return X, dY
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    import paper_2104_02621_b200 as pkg
+    from paper_2104_02621_b200.stack import CapsStack, shard_range
+    pkg.load_library()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    elem = 2 if dtype == torch.bfloat16 else 4
+    specs, H, W, D, gbatch, name = workload(args.config, world)
+    lo, hi = shard_range(gbatch, rank, world)
+    batch = hi - lo
+
+    # seeded weights (identical on every rank) and this rank's shard of the global batch
+    weights, h, w = [], H, W
+    for li, sp in enumerate(specs):
+        L = capsinputs.Layer(B=gbatch, H=h, W=w, C=sp.C, Cout=sp.Cout, KH=sp.KH, KW=sp.KW, D1=D, D2=D, D3=D,
+                             stride=sp.stride)
+        weights.append(capsinputs.make_kernel(L, dtype=dtype, layer_idx=li))
+        h, w = pkg.output_dims(h, w, sp.KH, sp.KW, sp.stride)
+    L0 = capsinputs.Layer(B=gbatch, H=H, W=W, C=specs[0].C, Cout=specs[0].Cout, KH=specs[0].KH, KW=specs[0].KW,
+                          D1=D, D2=D, D3=D, stride=specs[0].stride)
+    X_host = capsinputs.make_input(L0, dtype=dtype, batch_offset=lo, batch=batch).pin_memory()
+    dY_host = capsinputs.make_grad_output((gbatch, h, w, specs[-1].Cout, D, D), dtype=dtype, layer_idx=len(specs),
+                                          batch_offset=lo, batch=batch).pin_memory()
+    X = X_host.to(dev)
+    dY = dY_host.to(dev)
+
+    st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap)
+    gflops = st.step_flops(batch=gbatch)          # whole-job algorithmic flops per step
+    peaks = load_peaks()
+
+    # L2 flush buffer: 2x the L2 size, rewritten between timed steps
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 64 << 20), dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        st.step(X, dY)
+    torch.cuda.synchronize()
+
+    timer = CallTimer()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    n0 = pkg.launch_count()
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record()
+            st.step(X, dY, timer=timer)
+            ends[i].record()
+        torch.cuda.synchronize()
+        barrier()
+    launches = pkg.launch_count() - n0
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    calls = timer.collect()
+    ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = gflops / (ms_max * 1e-3) / 1e12
+
+    # ---- per-pass breakdown and the dominant kernel's roofline
+    per_pass, best = {}, None
+    t_roof_sum = 0.0
+    for (li, kind), v in sorted(calls.items()):
+        avg = sum(v) / len(v)
+        byts = pass_bytes(st, li, kind, elem)
+        fl = st.layer_flops(li)
+        gbs = byts / (avg * 1e-3) / 1e9
+        tr = max(byts / (peaks["hbm_gbs"] * 1e9), fl / (peaks["bf16_tflops"] * 1e12)) * 1e3
+        t_roof_sum += tr
+        per_pass["L%d_%s" % (li + 1, kind)] = {"ms": round(avg, 5), "GB_s": round(gbs, 1),
+                                                "TFLOP_s": round(fl / (avg * 1e-3) / 1e12, 1),
+                                                "roof_frac": round(tr / avg, 3)}
+        if best is None or avg > best[1]:
+            best = ((li, kind), avg, byts)
+    (bli, bkind), bavg, bbytes = best
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get("L%d_%s" % (bli + 1, bkind))
+    except Exception:
+        pass
+    achieved = bbytes / (bavg * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "kernel": "L%d_%s" % (bli + 1, bkind), "bytes_per_launch": bbytes,
+                "peak_src": peaks["src"], "step_frac": round(t_roof_sum / ms, 4)}
+
+    # ---- e2e: same steps through the public API with host buffers
+    dk_host = torch.empty(sum(k.numel() for k in st.dK), dtype=torch.float32).pin_memory()
+    e2e_start, e2e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e2e_start.record()
+    for i in range(args.steps):
+        xd = X_host.to(dev, non_blocking=True)
+        gd = dY_host.to(dev, non_blocking=True)
+        dks = st.step(xd, gd)
+        off = 0
+        for k in dks:
+            dk_host[off:off + k.numel()].copy_(k.reshape(-1), non_blocking=True)
+            off += k.numel()
+    e2e_end.record()
+    torch.cuda.synchronize()
+    e2e_ms = e2e_start.elapsed_time(e2e_end) / args.steps
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e = {"value": gflops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "h2d_bytes_per_step": X_host.numel() * X_host.element_size() + dY_host.numel() * dY_host.element_size(),
+           "d2h_bytes_per_step": dk_host.numel() * 4, "ms_per_step": e2e_ms}
+
+    # ---- CPU baseline: the oracle as it stands, on host cores, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            oracle.build()
+            fl1, Ks, strides, layers = stack_oracle_setup(specs, H, W, D, dtype)
+            Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, 1, dtype, gbatch)
+            t0 = time.perf_counter()
+            oracle.stack_fwd_bwd(Xs, Ks, strides, dYs, dtype == torch.bfloat16)
+            t1 = time.perf_counter() - t0
+            b = int(max(1, min(gbatch, 10.0 / max(t1, 1e-6))))
+            Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch)
+            t0 = time.perf_counter()
+            oracle.stack_fwd_bwd(Xs, Ks, strides, dYs, dtype == torch.bfloat16)
+            tb = time.perf_counter() - t0
+            cpu = {"value": fl1 * b / tb / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                   "sample": "oracle (C, fp64, OpenMP) %s fwd+bwd on %d of %d images, %.1f s" % (name, b, gbatch, tb)}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": None, "kind": "oracle", "sample": "failed: %s" % e}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 5), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded capsinputs; random-init weights)",
+            "config": {"workload": name, "global_batch": gbatch, "per_rank_batch": batch,
+                       "layers": ["%dx%d s%d %d->%d" % (s.KH, s.KW, s.stride, s.C, s.Cout) for s in specs],
+                       "input": "%dx%dx%d capsules %dx%d" % (H, W, specs[0].C, D, D),
+                       "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
+                       "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "per_pass": per_pass,
+            "flops_per_step": gflops,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
