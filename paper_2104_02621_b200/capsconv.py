@@ -86,11 +86,18 @@ def launch_count() -> int:
     return int(load_library().capsconv_launch_count())
 
 
+_dims_cache = {}
+
+
 def output_dims(H: int, W: int, KH: int, KW: int, stride: int) -> Tuple[int, int]:
-    lib = load_library()
-    ho, wo = ctypes.c_int64(), ctypes.c_int64()
-    _check(lib.capsconv_output_dims(H, W, KH, KW, stride, ctypes.byref(ho), ctypes.byref(wo)), "output_dims")
-    return ho.value, wo.value
+    key = (H, W, KH, KW, stride)
+    v = _dims_cache.get(key)
+    if v is None:
+        lib = load_library()
+        ho, wo = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.capsconv_output_dims(H, W, KH, KW, stride, ctypes.byref(ho), ctypes.byref(wo)), "output_dims")
+        v = _dims_cache[key] = (ho.value, wo.value)
+    return v
 
 
 def _dt(dtype) -> int:
@@ -99,11 +106,22 @@ def _dt(dtype) -> int:
     return _DT[dtype]
 
 
+_ws_size_cache = {}
+
+
 def workspace_bytes(op: int, dtype, ext) -> int:
-    lib = load_library()
-    out = ctypes.c_size_t()
-    _check(lib.capsconv_workspace_bytes(op, _dt(dtype), *ext, ctypes.byref(out)), "workspace_bytes")
-    return out.value
+    key = (op, dtype, tuple(ext), _device_key())
+    v = _ws_size_cache.get(key)
+    if v is None:
+        lib = load_library()
+        out = ctypes.c_size_t()
+        _check(lib.capsconv_workspace_bytes(op, _dt(dtype), *ext, ctypes.byref(out)), "workspace_bytes")
+        v = _ws_size_cache[key] = out.value
+    return v
+
+
+def _device_key():
+    return torch.cuda.current_device() if torch.cuda.is_available() else -1
 
 
 def select_path(op: int, dtype, ext) -> int:

@@ -28,8 +28,8 @@ namespace capsconv {
 
 constexpr int kTilePix = 32;     // M = 128 rows = 32 pixels x D1 (=4)
 constexpr int kMaxTaps = 64;
-constexpr int kProducerThreads = 128;
-constexpr int kEpilogueThreads = 128;
+constexpr int kProducerThreads = 256;
+constexpr int kEpilogueThreads = 256;   // two warps per TMEM lane quarter
 constexpr int kConvThreads = kProducerThreads + kEpilogueThreads + 32;  // + MMA warp
 
 // n / d for n < 2^31 by multiply-high (host-computed magic).
@@ -79,10 +79,10 @@ struct ConvMma {
     int n_mtiles;              // ceil(Bn*Hg*Wg / kTilePix)
     int n_igroups;             // ceil(n_mtiles / G)
     int n_items;
-    FastDiv fd_units;          // units per pixel in a chunk = 2*cc (per chunk, uniform unless last)
+    FastDiv fd_units;          // 8-byte pieces per pixel in a chunk = 4*CC
     // ---- shared memory plan
     int win_px;                // window pixels (max over groups, even)
-    uint32_t a_lbo;            // win_px*4*16
+    uint32_t a_lbo;            // win_px*4*16 + 64 (bank stagger)
     uint32_t plane_bytes;      // (CC/2) * a_lbo
     uint32_t a_stage_bytes;    // npl * plane_bytes
     uint32_t b_stage_bytes;    // max taps-per-group * (CC/2) * N_tile * 16
@@ -90,6 +90,8 @@ struct ConvMma {
     int b_resident;            // one B stage for the whole kernel
     uint32_t smem_bytes;
     uint32_t tmem_cols;
+    int dbg;                   // bench-only bits: 1 skip loads, 2 skip MMAs, 4 skip stores
+    unsigned long long *trace; // debug: globaltimer stamps of CTA 0 [role][item][4]
 };
 
 }  // namespace capsconv

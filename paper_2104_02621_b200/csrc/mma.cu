@@ -2,13 +2,13 @@
 // one shifted-window implicit GEMM (conv_mma.cuh), plus host planning.
 //
 // Roles in a CTA (288 threads, persistent over work items):
-//   warps 0-3  producers: stage the source window of the current channel chunk
+//   warps 0-7  producers: stage the source window of the current channel chunk
 //              into shared memory (16-byte coalesced loads; each 16 B holds
 //              two D1 rows of one capsule, stored as two 8-byte pieces into the
 //              K-major rows (pixel, d1) -- the D1 repack of SURVEY H1); one
 //              thread also streams the prepacked weights with bulk copies.
-//   warps 4-7  epilogue: TMEM -> registers -> bf16 -> capsule layout in HBM.
-//   warp 8     MMA issuer: for every tap, the same window at a different row
+//   warps 8-15 epilogue (two per TMEM lane quarter, alternating tiles): TMEM -> registers -> bf16 -> capsule layout in HBM.
+//   warp 16    MMA issuer: for every tap, the same window at a different row
 //              offset; accumulators stay in TMEM across taps and chunks
 //              (the paper's output_reduce, becomes free).
 #include <cuda_bf16.h>
@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "conv_mma.cuh"
@@ -59,60 +60,117 @@ __device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
     return it;
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(role, idx, ev)                                                                      \
+    do {                                                                                          \
+        if (P.trace && blockIdx.x == 0 && (idx) < 64)                                             \
+            P.trace[((role) * 64 + (idx)) * 4 + (ev)] = gtime();                                  \
+    } while (0)
+
 __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
     asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 
 // ------------------------------------------------------------------ producers
+// cp.async of one 8-byte piece; src_bytes = 0 writes zeros (invalid pixel).
+__device__ __forceinline__ void cp_async8_zfill(uint32_t dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// Stage the window of channel chunk `ch` into the K-major A layout with
+// cp.async: each 16-byte global unit (capsule (pixel, c), rows d1 = 2i, 2i+1)
+// becomes two 8-byte pieces in rows (pixel, 2i) and (pixel, 2i+1) of k-chunk
+// c/2 (half c%2).  Nothing waits here: completion is signalled on the stage's
+// mbarrier, so several stages are in flight at once.
 __device__ __forceinline__ void load_window(const ConvMma &P, const Item &it, int ch, uint32_t a_stage, int tid) {
+    // Pieces of 8 bytes; consecutive lanes take consecutive pieces of one
+    // pixel (a warp instruction reads up to 256 contiguous bytes).  A 16-byte
+    // capsule unit (channel c, rows 2i, 2i+1) is two pieces, stored in rows
+    // (pixel, d1) of k-chunk c/2, half c%2, of the K-major window.
+    // Pixels are walked with an incremental (b, Y, X) counter: no division in
+    // the steady state.
     const int cc = P.CC;
-    const int upp = 2 * cc;                       // 16-byte units per pixel in this chunk
-    const int total = P.npl * P.win_px * upp;
-    const int vbase = it.tile0 * kTilePix + P.og_offmin[it.g];
+    const int ppp = 4 * cc;                       // pieces per pixel in this chunk
+    const int lane = tid & 31, warp = tid >> 5;
+    const int wp = ppp >= 32 ? 1 : 32 / ppp;      // pixels per warp iteration
+    const int lane_pix = ppp >= 32 ? 0 : lane / ppp;
+    const int r0 = ppp >= 32 ? lane : lane - lane_pix * ppp;
+    const int step = (kProducerThreads / 32) * wp;
     const int vtotal = P.Bn * P.Hg * P.Wg;
     const int c_src0 = ch * cc;
-    const uint4 *src = reinterpret_cast<const uint4 *>(P.src);
+    const uint2 *src = reinterpret_cast<const uint2 *>(P.src);
     const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
-    constexpr int kBatch = 8;
-    for (int L0 = tid; L0 < total; L0 += kProducerThreads * kBatch) {
-        uint4 v[kBatch];
-        uint32_t dst[kBatch];
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            const int L = L0 + j * kProducerThreads;
-            v[j] = make_uint4(0, 0, 0, 0);
-            dst[j] = 0xFFFFFFFFu;
-            if (L < total) {
-                const int pix = (int)P.fd_units.div((uint32_t)L);
-                const int u2 = L - pix * upp;
-                const int c = u2 >> 1, i = u2 & 1;
-                int k = 0, vl = pix;
-                while (vl >= P.win_px) { vl -= P.win_px; ++k; }
-                const int vv = vbase + vl;
-                dst[j] = a_stage + k * P.plane_bytes + (c >> 1) * P.a_lbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
-                         (c & 1) * 8u;
-                if (vv >= 0 && vv < vtotal && c_src0 + c < P.CS) {
-                    const uint32_t b = P.fd_HgWg.div((uint32_t)vv);
-                    const uint32_t rr = (uint32_t)vv - b * HgWg;
-                    const uint32_t Y = P.fd_Wg.div(rr);
-                    const uint32_t X = rr - Y * (uint32_t)P.Wg;
-                    const int sy = P.pl_s * (int)Y + P.pl_oy[k];
-                    const int sx = P.pl_s * (int)X + P.pl_ox[k];
-                    if (sy < P.src_vH && sx < P.src_vW) {
-                        const size_t pixel = ((size_t)b * P.src_H + sy) * P.src_W + sx;
-                        // 16-byte unit index: pixel * (CS*16*2/16) + channel*2 + i
-                        v[j] = __ldg(src + pixel * (size_t)(P.CS * 2) + (size_t)(c_src0 + c) * 2 + i);
-                    }
-                }
+    const int vl0 = warp * wp + lane_pix;
+    const int v_first = it.tile0 * kTilePix + P.og_offmin[it.g] + vl0;
+    // decode of the first pixel (may be negative -> before the batch)
+    int b = 0, Y = 0, X = 0;
+    if (v_first >= 0) {
+        b = (int)P.fd_HgWg.div((uint32_t)v_first);
+        const uint32_t rr = (uint32_t)v_first - (uint32_t)b * HgWg;
+        Y = (int)P.fd_Wg.div(rr);
+        X = (int)rr - Y * P.Wg;
+    }
+    const int sX = step % P.Wg, sY = (step / P.Wg) % P.Hg, sB = step / (int)HgWg;  // step decomposed
+    for (int k = 0; k < P.npl; ++k) {
+        const uint32_t plane = a_stage + k * P.plane_bytes;
+        int vb = b, vy = Y, vx = X, vv = v_first;
+        for (int vl = vl0; vl < P.win_px; vl += step) {
+            const int sy = P.pl_s * vy + P.pl_oy[k];
+            const int sx = P.pl_s * vx + P.pl_ox[k];
+            const bool pix_ok = vv >= 0 && vv < vtotal && sy < P.src_vH && sx < P.src_vW;
+            const uint2 *pp = src + (((size_t)vb * P.src_H + sy) * P.src_W + sx) * (size_t)(P.CS * 4) + c_src0 * 4;
+            const uint32_t drow = plane + (uint32_t)vl * 64u;
+            for (int r = r0; r < ppp; r += 32) {
+                const int c = r >> 2, d1 = r & 3;
+                const bool ok = pix_ok && (c_src0 + c < P.CS);
+                cp_async8_zfill(drow + (c >> 1) * P.a_lbo + d1 * 16u + (c & 1) * 8u, ok ? (const void *)(pp + r) : (const void *)src,
+                                ok ? 8u : 0u);
+            }
+            // advance (b, Y, X) by `step` pixels
+            vv += step;
+            vx += sX; vy += sY; vb += sB;
+            if (vx >= P.Wg) { vx -= P.Wg; ++vy; }
+            if (vy >= P.Hg) { vy -= P.Hg; ++vb; }
+            if (vv == 0 || (vv > 0 && vv - step < 0)) {   // crossed into the batch from negative indices
+                vb = (int)P.fd_HgWg.div((uint32_t)vv);
+                const uint32_t rr = (uint32_t)vv - (uint32_t)vb * HgWg;
+                vy = (int)P.fd_Wg.div(rr);
+                vx = (int)rr - vy * P.Wg;
             }
         }
+    }
+}
+
+// Epilogue store of 16 accumulator columns (4 output channels x 4) of one row
+// (virtual pixel u, capsule row d1): bf16 into the capsule layout, or fp32
+// split-K partials.
+__device__ __forceinline__ void epi_store16(const ConvMma &P, const Item &it, const float (&v)[16], int n0, int u,
+                                            int d1, bool valid, size_t opix) {
+    if (P.ksplit == 1) {
+        if (!valid) return;
 #pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            if (dst[j] != 0xFFFFFFFFu) {
-                st_shared_v2(dst[j], v[j].x, v[j].y);          // row d1 = 2i
-                st_shared_v2(dst[j] + 16u, v[j].z, v[j].w);    // row d1 = 2i + 1
+        for (int j = 0; j < 4; ++j) {
+            const int ch = it.nt * (P.N_tile / 4) + n0 / 4 + j;
+            if (ch < P.NCH) {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(v[4 * j], v[4 * j + 1]);
+                __nv_bfloat162 hi = __floats2bfloat162_rn(v[4 * j + 2], v[4 * j + 3]);
+                uint2 w;
+                w.x = *reinterpret_cast<uint32_t *>(&lo);
+                w.y = *reinterpret_cast<uint32_t *>(&hi);
+                *reinterpret_cast<uint2 *>(P.out + (opix * P.NCH + ch) * 16 + d1 * 4) = w;
             }
         }
+    } else if (u < P.Bn * P.Hg * P.Wg) {
+        const size_t rows_total = (size_t)P.n_mtiles * 128;
+        const size_t ntot = (size_t)P.n_ntiles * P.N_tile;
+        float *dst = P.part + ((size_t)it.ks * rows_total + (size_t)u * 4 + d1) * ntot + (size_t)it.nt * P.N_tile + n0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            reinterpret_cast<float4 *>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     }
 }
 
@@ -146,13 +204,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         mbar_init(b_res, 1);
         mbar_fence_init();
     }
-    if (warp == 8) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
+    constexpr int kEpiWarp0 = kProducerThreads / 32;
+    constexpr int kMmaWarp = kEpiWarp0 + kEpilogueThreads / 32;
+    if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
+    if (warp < kEpiWarp0) {
         // ================================================= producers
         const int tid = threadIdx.x;
         if (P.b_resident && tid == 0) {
@@ -164,8 +224,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         uint32_t phase = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             const Item it = decode_item(P, item);
+            const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
             for (int ch = it.c_begin; ch < it.c_end; ++ch) {
+                if (tid == 0) TRACE(0, ii, 0);
                 mbar_wait(a_empty + stage, phase ^ 1);
+                if (tid == 0) TRACE(0, ii, 1);
                 const uint32_t a_stage = stage0 + stage * stage_stride;
                 if (!P.b_resident && tid == 0) {
                     const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
@@ -175,15 +238,16 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     mbar_arrive_expect_tx(b_full + stage, bytes);
                     bulk_g2s_u32(a_stage + P.a_stage_bytes, P.wpack + off, bytes, b_full + stage);
                 }
-                load_window(P, it, ch, a_stage, tid);
-                fence_proxy_async_smem();
-                mbar_arrive(a_full + stage);
+                if (!(P.dbg & 1)) load_window(P, it, ch, a_stage, tid);
+                cp_async_mbar_arrive(a_full + stage);   // arrives when this thread's copies land
+                if (tid == 0) TRACE(0, ii, 2);
                 if (++stage == P.nstages) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp < 8) {
+    } else if (warp < kMmaWarp) {
         // ================================================= epilogue
-        const int wq = warp - 4;
+        const int wq = warp & 3;   // TMEM lane quarter this warp may access
+        const int ehalf = (warp - kEpiWarp0) >> 2;   // which of the two warps of this quarter
         const int row = wq * 32 + lane;
         const int vtotal = P.Bn * P.Hg * P.Wg;
         const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
@@ -191,9 +255,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         uint32_t aphase = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             const Item it = decode_item(P, item);
+            const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
+            if (row == 0) TRACE(2, ii, 0);
             mbar_wait(acc_full + abuf, aphase);
+            if (row == 0) TRACE(2, ii, 1);
             fence_after_sync();
-            for (int gi = 0; gi < it.ntl; ++gi) {
+            for (int gi = ehalf; gi < ((P.dbg & 32) ? 0 : it.ntl); gi += 2) {
                 const int u = (it.tile0 + gi) * kTilePix + (row >> 2);
                 const int d1 = row & 3;
                 bool valid = u < vtotal;
@@ -209,44 +276,32 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
                 }
                 const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)((abuf * P.G + gi) * P.N_tile);
-                for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
-                    float v[16];
-                    tmem_ld16(tcol + n0, v);
-                    tmem_wait_ld();
-                    if (P.ksplit == 1) {
-                        if (valid) {
+                for (int n0 = 0; n0 < P.N_tile; n0 += 32) {
+                    float va[16], vb[16];
+                    const bool two = n0 + 16 < P.N_tile;
+                    if (!(P.dbg & 16)) {
+                        tmem_ld16(tcol + n0, va);
+                        if (two) tmem_ld16(tcol + n0 + 16, vb);
+                        tmem_wait_ld();
+                    } else {
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const int ch = it.nt * (P.N_tile / 4) + n0 / 4 + j;
-                                if (ch < P.NCH) {
-                                    __nv_bfloat162 lo = __floats2bfloat162_rn(v[4 * j], v[4 * j + 1]);
-                                    __nv_bfloat162 hi = __floats2bfloat162_rn(v[4 * j + 2], v[4 * j + 3]);
-                                    uint2 w;
-                                    w.x = *reinterpret_cast<uint32_t *>(&lo);
-                                    w.y = *reinterpret_cast<uint32_t *>(&hi);
-                                    *reinterpret_cast<uint2 *>(P.out + (opix * P.NCH + ch) * 16 + d1 * 4) = w;
-                                }
-                            }
-                        }
-                    } else if (u < vtotal) {
-                        const size_t rows_total = (size_t)P.n_mtiles * 128;
-                        const size_t ntot = (size_t)P.n_ntiles * P.N_tile;
-                        float *dst = P.part + ((size_t)it.ks * rows_total + (size_t)u * 4 + d1) * ntot +
-                                     (size_t)it.nt * P.N_tile + n0;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            reinterpret_cast<float4 *>(dst)[j] =
-                                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        for (int e = 0; e < 16; ++e) va[e] = vb[e] = (float)e;
+                    }
+                    if (!(P.dbg & 4)) {
+                        epi_store16(P, it, va, n0, u, d1, valid, opix);
+                        if (two) epi_store16(P, it, vb, n0 + 16, u, d1, valid, opix);
                     }
                 }
             }
+            if (row == 0) TRACE(2, ii, 2);
             fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty + abuf);
+            if (row == 0) TRACE(2, ii, 3);
             if (++abuf == 2) { abuf = 0; aphase ^= 1; }
         }
     } else {
-        // ================================================= MMA issuer (warp 8)
+        // ================================================= MMA issuer
         const uint32_t idesc = idesc_bf16(128, P.N_tile, 0, 0);
         const uint32_t b_lbo = (uint32_t)P.N_tile * 16;
         int stage = 0;
@@ -256,28 +311,43 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         if (P.b_resident) mbar_wait(b_res, 0);
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             const Item it = decode_item(P, item);
+            const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
+            if (lane == 0) TRACE(1, ii, 0);
             mbar_wait(acc_empty + abuf, aphase ^ 1);
+            if (lane == 0) TRACE(1, ii, 1);
             fence_after_sync();
             const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
             const int offmin = P.og_offmin[it.g];
             for (int ch = it.c_begin; ch < it.c_end; ++ch) {
                 mbar_wait(a_full + stage, phase);
                 if (!P.b_resident) mbar_wait(b_full + stage, phase);
+                if (lane == 0) TRACE(1, ii, 2);
+                fence_proxy_async_smem();   // cp.async (generic proxy) data -> tensor core (async proxy)
                 fence_after_sync();
                 const uint32_t a_stage = stage0 + stage * stage_stride;
                 const uint32_t b_base = P.b_resident ? bres_addr : a_stage + P.a_stage_bytes;
+                // descriptors: the 14-bit start-address field (16-byte units) is the low
+                // bits, so a byte offset is added as (offset >> 4).
+                const uint64_t a_desc0 = smem_desc(a_stage, P.a_lbo, 128);
+                const uint64_t b_desc0 = smem_desc(b_base, b_lbo, 128);
+                const uint32_t d0 = tmem + (uint32_t)(abuf * P.G * P.N_tile);
+                const int ksteps = P.CC / 4;
                 if (elect_one()) {
+                    if (!(P.dbg & 2))
                     for (int t = t0; t < t1; ++t) {
-                        const uint32_t a_tap = a_stage + P.tap_plane[t] * P.plane_bytes +
-                                               (uint32_t)(P.tap_shift[t] - offmin) * 64u;
-                        for (int j = 0; j < P.CC / 4; ++j) {
-                            const uint64_t bd =
-                                smem_desc(b_base + ((t - t0) * (P.CC / 2) + 2 * j) * b_lbo, b_lbo, 128);
+                        const uint64_t a_tap = a_desc0 + ((P.tap_plane[t] * P.plane_bytes +
+                                                           (uint32_t)(P.tap_shift[t] - offmin) * 64u) >> 4);
+                        const uint64_t b_tap = b_desc0 + (((t - t0) * (P.CC / 2) * b_lbo) >> 4);
+                        for (int j = 0; j < ksteps; ++j) {
+                            const uint64_t bd = b_tap + ((2u * j * b_lbo) >> 4);
+                            const uint64_t aj = a_tap + ((2u * j * P.a_lbo) >> 4);
                             const uint32_t acc = (ch != it.c_begin || t != t0 || j != 0) ? 1u : 0u;
+                            uint32_t d = d0;
+                            uint64_t ad = aj;
                             for (int gi = 0; gi < it.ntl; ++gi) {
-                                const uint64_t ad =
-                                    smem_desc(a_tap + (uint32_t)(gi * kTilePix) * 64u + 2u * j * P.a_lbo, P.a_lbo, 128);
-                                mma_bf16_ss(tmem + (uint32_t)((abuf * P.G + gi) * P.N_tile), ad, bd, idesc, acc);
+                                mma_bf16_ss(d, ad, bd, idesc, acc);
+                                d += (uint32_t)P.N_tile;
+                                ad += (kTilePix * 64) >> 4;
                             }
                         }
                     }
@@ -288,13 +358,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             }
             if (elect_one()) mma_commit(acc_full + abuf);
             __syncwarp();
+            if (lane == 0) TRACE(1, ii, 3);
             if (++abuf == 2) { abuf = 0; aphase ^= 1; }
         }
     }
 
     fence_before_sync();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         fence_after_sync();
         tmem_dealloc_dyn(tmem, P.tmem_cols);
     }
@@ -501,12 +572,17 @@ Plan make_plan(const Problem &p, bool dgrad) {
         const int nchunks = P.CSpad / cc;
         int ksplit = 1;
         if (base_items < nsm && P.nog == 1) ksplit = std::min(nchunks, ceil_div(2 * nsm, base_items));
+        static const int force_g = getenv("CAPSCONV_FORCE_G") ? atoi(getenv("CAPSCONV_FORCE_G")) : 0;
         for (int G : {8, 4, 2, 1}) {
+            if (force_g && G != force_g) continue;
             if (2 * G * P.N_tile > 512) continue;
             const long long items = (long long)P.nog * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
-            if (G > 1 && items < 2 * nsm) continue;
+            if (G > 1 && items < 2 * nsm && !force_g) continue;
             const int win_px = ((G * kTilePix + max_span) + 1) & ~1;
-            const uint32_t a_lbo = (uint32_t)win_px * 64;
+            // k-chunk planes staggered by 64 bytes mod 128: a warp's 32 pieces
+            // (c, d1) of one pixel then cover every bank exactly twice (two
+            // wavefronts, the minimum for 256 bytes)
+            const uint32_t a_lbo = (uint32_t)win_px * 64 + 64;
             const uint32_t plane = (uint32_t)(cc / 2) * a_lbo;
             const uint32_t a_stage = (uint32_t)P.npl * plane;
             const uint32_t b_stage = (uint32_t)max_taps_g * (cc / 2) * P.N_tile * 16;
@@ -516,7 +592,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
                 const uint64_t bytes = 1024 + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
                 if (bytes <= kSmemLimit) { best_st = st; break; }
             }
-            if (!best_st) continue;
+            if (!best_st || (best_st < 3 && G > 1 && !force_g)) continue;
             if (a_lbo >= (1u << 18) || b_stage >= (1u << 20)) continue;
             P.CC = cc; P.nchunks = nchunks; P.ksplit = ksplit; P.G = G;
             P.win_px = win_px; P.a_lbo = a_lbo; P.plane_bytes = plane;
@@ -536,7 +612,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
     P.tmem_cols = cols;
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
-    P.fd_units.init((uint32_t)(2 * P.CC));
+    P.fd_units.init((uint32_t)(4 * P.CC));
 
     pl.wpack_bytes = align256((size_t)P.n_ntiles * P.nchunks * P.ntaps * (P.CC / 2) * P.N_tile * 16);
     pl.part_bytes = P.ksplit > 1 ? align256((size_t)P.ksplit * P.n_mtiles * 128 * P.n_ntiles * P.N_tile * 4) : 0;
@@ -555,6 +631,8 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
     ConvMma &P = pl.P;
     if (ws_bytes < pl.wpack_bytes + pl.part_bytes) return cudaErrorInvalidValue;
     static const bool debug = getenv("CAPSCONV_DEBUG") != nullptr;
+    static const int dbg_bits = getenv("CAPSCONV_MMA_DBG") ? atoi(getenv("CAPSCONV_MMA_DBG")) : 0;
+    P.dbg = dbg_bits;
     if (debug)
         fprintf(stderr,
                 "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
@@ -578,8 +656,32 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
         attr_set = true;
     }
     const int grid = std::min(P.n_items, device_info().num_sms);
+    static const bool tracing = getenv("CAPSCONV_TRACE") != nullptr;
+    P.trace = nullptr;
+    if (tracing) {
+        cudaMalloc(&P.trace, 3 * 64 * 4 * sizeof(unsigned long long));
+        cudaMemset(P.trace, 0, 3 * 64 * 4 * sizeof(unsigned long long));
+    }
     conv_mma_kernel<<<grid, kConvThreads, P.smem_bytes, st>>>(P);
     note_launches(1);
+    if (tracing) {
+        std::vector<unsigned long long> h(3 * 64 * 4);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), P.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        cudaFree(P.trace);
+        unsigned long long t0 = ~0ull;
+        for (auto v : h) if (v && v < t0) t0 = v;
+        const char *names[3] = {"prod", "mma ", "epi "};
+        for (int i = 0; i < 20; ++i)
+            for (int r = 0; r < 3; ++r) {
+                fprintf(stderr, "[trace] item %2d %s", i, names[r]);
+                for (int e = 0; e < 4; ++e) {
+                    unsigned long long v = h[(r * 64 + i) * 4 + e];
+                    fprintf(stderr, " %8lld", v ? (long long)(v - t0) : -1ll);
+                }
+                fprintf(stderr, "\n");
+            }
+    }
     if (P.ksplit > 1) {
         const long long n = (long long)P.Bn * P.Hg * P.Wg * 4 * P.NCH;
         finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P);
@@ -588,29 +690,55 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
     return cudaGetLastError();
 }
 
+// Plans depend only on (op, extents, device): cache them (host planning costs
+// microseconds; a training step calls the same shapes every iteration).
+struct PlanKey {
+    int op, dt, dev, nsm;
+    int64_t e[11];
+    bool operator==(const PlanKey &o) const {
+        if (op != o.op || dt != o.dt || dev != o.dev || nsm != o.nsm) return false;
+        for (int i = 0; i < 11; ++i)
+            if (e[i] != o.e[i]) return false;
+        return true;
+    }
+};
+
+const Plan &cached_plan(const Problem &p, bool dgrad) {
+    static std::mutex mu;
+    static std::vector<std::pair<PlanKey, Plan>> cache;
+    const DeviceInfo &di = device_info();
+    PlanKey k{dgrad ? 1 : 0, (int)p.dt, di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s}};
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto &kv : cache)
+        if (kv.first == k) return kv.second;
+    if (cache.size() > 256) cache.clear();
+    cache.emplace_back(k, make_plan(p, dgrad));
+    return cache.back().second;
+}
+
 }  // namespace
 
 bool mma_supported(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return false;
-    return make_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
+    return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }
 
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return 0;
-    Plan pl = make_plan(p, op == CAPSCONV_OP_BWD_DATA);
+    const Plan &pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
     return pl.ok ? pl.wpack_bytes + pl.part_bytes : 0;
 }
 
 cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
-    Plan pl = make_plan(p, false);
+    Plan pl = cached_plan(p, false);
     if (!pl.ok) return cudaErrorNotSupported;
     return run_plan(pl, I, K, O, ws, ws_bytes, st);
 }
 
 cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,
                          cudaStream_t st) {
-    Plan pl = make_plan(p, true);
+    Plan pl = cached_plan(p, true);
     if (!pl.ok) return cudaErrorNotSupported;
     return run_plan(pl, dO, K, dI, ws, ws_bytes, st);
 }

@@ -142,9 +142,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+#ifndef CAPSCONV_MBAR_POLL
+#define CAPSCONV_MBAR_POLL 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if CAPSCONV_MBAR_POLL
+    while (!mbar_test_wait(bar, parity)) {
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 
 // ---------------------------------------------------------------- bulk copies (TMA engine, 1-D)
