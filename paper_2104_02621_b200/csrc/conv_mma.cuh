@@ -21,6 +21,7 @@
 // are zero in shared memory; invalid output rows are computed and dropped.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -30,7 +31,7 @@ constexpr int kTilePix = 32;     // M = 128 rows = 32 pixels x D1 (=4)
 constexpr int kMaxTaps = 64;
 constexpr int kProducerThreads = 256;
 constexpr int kEpilogueThreads = 256;   // two warps per TMEM lane quarter
-constexpr int kConvThreads = kProducerThreads + kEpilogueThreads + 32;  // + MMA warp
+constexpr int kConvThreads = kProducerThreads + kEpilogueThreads + 64;  // + MMA warp + TMA warp
 
 // n / d for n < 2^31 by multiply-high (host-computed magic).
 struct FastDiv {
@@ -48,6 +49,14 @@ struct FastDiv {
 };
 
 struct ConvMma {
+    // ---- TMA descriptor of the source (natural layout), see tma.h
+    alignas(64) CUtensorMap tmap;
+    int stg_batch_mode;        // 0: one copy per virtual row (box Wg px); 1: Hg*Wg == 1, box of BB images
+    int BB;
+    int stg_cap_px;            // staging capacity per plane, pixels
+    uint32_t stg_plane_bytes;  // stg_cap_px * CC * 32
+    uint32_t stg_bytes;        // npl * stg_plane_bytes
+    int nstg;                  // staging buffers (1 or 2)
     // ---- tensors
     const __nv_bfloat16 *src;  // A source, natural capsule layout, pixel = CS*16 elements
     const uint8_t *wpack;      // prepacked B: [ntile][chunk][tap][kc][N_tile][16 B]
@@ -82,7 +91,7 @@ struct ConvMma {
     FastDiv fd_units;          // 8-byte pieces per pixel in a chunk = 4*CC
     // ---- shared memory plan
     int win_px;                // window pixels (max over groups, even)
-    uint32_t a_lbo;            // win_px*4*16 + 64 (bank stagger)
+    uint32_t a_lbo;            // win_px*4*16 + 16 (bank stagger)
     uint32_t plane_bytes;      // (CC/2) * a_lbo
     uint32_t a_stage_bytes;    // npl * plane_bytes
     uint32_t b_stage_bytes;    // max taps-per-group * (CC/2) * N_tile * 16

@@ -53,4 +53,10 @@ cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *
 cudaError_t mma_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK,
                            void *ws, size_t ws_bytes, cudaStream_t st);
 
+// tcgen05 kernel gradient (wgrad.cu)
+bool wgrad_supported(const Problem &p);
+size_t wgrad_workspace_bytes(const Problem &p);
+cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
+                      cudaStream_t st);
+
 }  // namespace capsconv

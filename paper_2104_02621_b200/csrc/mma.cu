@@ -21,6 +21,7 @@
 
 #include "conv_mma.cuh"
 #include "internal.h"
+#include "tma.h"
 #include "umma.cuh"
 
 namespace capsconv {
@@ -30,15 +31,6 @@ namespace {
 
 constexpr int kMaxStages = 8;
 
-__device__ __forceinline__ void tmem_alloc_dyn(uint32_t *dst, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst)),
-                 "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc_dyn(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
-}
 
 struct Item {
     int g, ig, nt, ks;
@@ -60,88 +52,91 @@ __device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
     return it;
 }
 
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 #define TRACE(role, idx, ev)                                                                      \
     do {                                                                                          \
         if (P.trace && blockIdx.x == 0 && (idx) < 64)                                             \
             P.trace[((role) * 64 + (idx)) * 4 + (ev)] = gtime();                                  \
     } while (0)
 
-__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
-}
 
 // ------------------------------------------------------------------ producers
-// cp.async of one 8-byte piece; src_bytes = 0 writes zeros (invalid pixel).
-__device__ __forceinline__ void cp_async8_zfill(uint32_t dst, const void *src, uint32_t src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+
+// Window of virtual pixels [v0, v0 + len) of the current item; with the
+// staging layout of whole virtual rows the window starts `off` pixels in.
+__device__ __forceinline__ int window_v0(const ConvMma &P, const Item &it) {
+    return it.tile0 * kTilePix + P.og_offmin[it.g];
+}
+__device__ __forceinline__ int staging_off(const ConvMma &P, int v0) {
+    return P.stg_batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
 }
 
-// Stage the window of channel chunk `ch` into the K-major A layout with
-// cp.async: each 16-byte global unit (capsule (pixel, c), rows d1 = 2i, 2i+1)
-// becomes two 8-byte pieces in rows (pixel, 2i) and (pixel, 2i+1) of k-chunk
-// c/2 (half c%2).  Nothing waits here: completion is signalled on the stage's
-// mbarrier, so several stages are in flight at once.
-__device__ __forceinline__ void load_window(const ConvMma &P, const Item &it, int ch, uint32_t a_stage, int tid) {
-    // Pieces of 8 bytes; consecutive lanes take consecutive pieces of one
-    // pixel (a warp instruction reads up to 256 contiguous bytes).  A 16-byte
-    // capsule unit (channel c, rows 2i, 2i+1) is two pieces, stored in rows
-    // (pixel, d1) of k-chunk c/2, half c%2, of the K-major window.
-    // Pixels are walked with an incremental (b, Y, X) counter: no division in
-    // the steady state.
-    const int cc = P.CC;
-    const int ppp = 4 * cc;                       // pieces per pixel in this chunk
-    const int lane = tid & 31, warp = tid >> 5;
-    const int wp = ppp >= 32 ? 1 : 32 / ppp;      // pixels per warp iteration
-    const int lane_pix = ppp >= 32 ? 0 : lane / ppp;
-    const int r0 = ppp >= 32 ? lane : lane - lane_pix * ppp;
-    const int step = (kProducerThreads / 32) * wp;
-    const int vtotal = P.Bn * P.Hg * P.Wg;
-    const int c_src0 = ch * cc;
-    const uint2 *src = reinterpret_cast<const uint2 *>(P.src);
-    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
-    const int vl0 = warp * wp + lane_pix;
-    const int v_first = it.tile0 * kTilePix + P.og_offmin[it.g] + vl0;
-    // decode of the first pixel (may be negative -> before the batch)
-    int b = 0, Y = 0, X = 0;
-    if (v_first >= 0) {
-        b = (int)P.fd_HgWg.div((uint32_t)v_first);
-        const uint32_t rr = (uint32_t)v_first - (uint32_t)b * HgWg;
-        Y = (int)P.fd_Wg.div(rr);
-        X = (int)rr - Y * P.Wg;
-    }
-    const int sX = step % P.Wg, sY = (step / P.Wg) % P.Hg, sB = step / (int)HgWg;  // step decomposed
+// TMA thread: stage the natural-layout source pixels covering the window of
+// channel chunk `ch` for every plane.  Rows mode: one box per virtual row
+// (Wg pixels, every pl_s-th source pixel, rows/batches outside the tensor
+// read as zero).  Batch mode (Hg*Wg == 1): boxes of BB images.
+__device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &it, int ch, uint32_t stg,
+                                                  uint32_t mbar) {
+    const int v0 = window_v0(P, it);
+    const int len = P.win_px;
+    const int c0 = ch * P.CC * 16;
+    const uint32_t px_bytes = (uint32_t)P.CC * 32u;
+    uint32_t bytes = 0;
     for (int k = 0; k < P.npl; ++k) {
-        const uint32_t plane = a_stage + k * P.plane_bytes;
-        int vb = b, vy = Y, vx = X, vv = v_first;
-        for (int vl = vl0; vl < P.win_px; vl += step) {
-            const int sy = P.pl_s * vy + P.pl_oy[k];
-            const int sx = P.pl_s * vx + P.pl_ox[k];
-            const bool pix_ok = vv >= 0 && vv < vtotal && sy < P.src_vH && sx < P.src_vW;
-            const uint2 *pp = src + (((size_t)vb * P.src_H + sy) * P.src_W + sx) * (size_t)(P.CS * 4) + c_src0 * 4;
-            const uint32_t drow = plane + (uint32_t)vl * 64u;
-            for (int r = r0; r < ppp; r += 32) {
-                const int c = r >> 2, d1 = r & 3;
-                const bool ok = pix_ok && (c_src0 + c < P.CS);
-                cp_async8_zfill(drow + (c >> 1) * P.a_lbo + d1 * 16u + (c & 1) * 8u, ok ? (const void *)(pp + r) : (const void *)src,
-                                ok ? 8u : 0u);
+        const uint32_t base = stg + k * P.stg_plane_bytes;
+        if (P.stg_batch_mode) {
+            for (int b0 = v0; b0 < v0 + len; b0 += P.BB) {
+                tma::load4d(base + (uint32_t)(b0 - v0) * px_bytes, &P.tmap, c0, 0, 0, b0, mbar);
+                bytes += (uint32_t)P.BB * px_bytes;
             }
-            // advance (b, Y, X) by `step` pixels
-            vv += step;
-            vx += sX; vy += sY; vb += sB;
-            if (vx >= P.Wg) { vx -= P.Wg; ++vy; }
-            if (vy >= P.Hg) { vy -= P.Hg; ++vb; }
-            if (vv == 0 || (vv > 0 && vv - step < 0)) {   // crossed into the batch from negative indices
-                vb = (int)P.fd_HgWg.div((uint32_t)vv);
-                const uint32_t rr = (uint32_t)vv - (uint32_t)vb * HgWg;
-                vy = (int)P.fd_Wg.div(rr);
-                vx = (int)rr - vy * P.Wg;
+        } else {
+            const int Ra = floor_div(v0, P.Wg), Rb = floor_div(v0 + len - 1, P.Wg);
+            for (int R = Ra; R <= Rb; ++R) {
+                const int b = floor_div(R, P.Hg);
+                const int Y = R - b * P.Hg;
+                tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px_bytes, &P.tmap, c0, P.pl_ox[k],
+                            P.pl_s * Y + P.pl_oy[k], b, mbar);
+                bytes += (uint32_t)P.Wg * px_bytes;
             }
         }
+    }
+    return bytes;
+}
+
+__device__ __forceinline__ uint32_t staging_bytes(const ConvMma &P, const Item &it) {
+    const int v0 = window_v0(P, it);
+    const uint32_t px_bytes = (uint32_t)P.CC * 32u;
+    uint32_t per_plane;
+    if (P.stg_batch_mode) {
+        per_plane = (uint32_t)((P.win_px + P.BB - 1) / P.BB) * P.BB * px_bytes;
+    } else {
+        const int Ra = floor_div(v0, P.Wg), Rb = floor_div(v0 + P.win_px - 1, P.Wg);
+        per_plane = (uint32_t)((Rb - Ra + 1) * P.Wg) * px_bytes;
+    }
+    return per_plane * P.npl;
+}
+
+
+// Producers: repack the staged natural layout [pixel][c][d1][d2] into the
+// K-major window rows (pixel, d1) x k-chunks (c pair, d2): each 16-byte unit
+// (c, rows 2i, 2i+1) becomes two 8-byte pieces (the D1 repack of SURVEY H1).
+__device__ __forceinline__ void repack_window(const ConvMma &P, const Item &it, uint32_t stg, uint32_t a_stage,
+                                              int tid) {
+    const int upp = 2 * P.CC;
+    const int total = P.npl * P.win_px * upp;
+    const int off = staging_off(P, window_v0(P, it));
+    const uint32_t px_bytes = (uint32_t)P.CC * 32u;
+#pragma unroll 4
+    for (int L = tid; L < total; L += kProducerThreads) {
+        const int pix = (int)P.fd_units.div((uint32_t)L);
+        const int u2 = L - pix * upp;
+        const int c = u2 >> 1, i = u2 & 1;
+        int k = 0, vl = pix;
+        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+        const uint4 v = ld_shared_v4(stg + k * P.stg_plane_bytes + (uint32_t)(vl + off) * px_bytes + (uint32_t)u2 * 16u);
+        const uint32_t dst = a_stage + k * P.plane_bytes + (c >> 1) * P.a_lbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
+                             (c & 1) * 8u;
+        st_shared_v2(dst, v.x, v.y);          // row d1 = 2i
+        st_shared_v2(dst + 16u, v.z, v.w);    // row d1 = 2i + 1
     }
 }
 
@@ -183,8 +178,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
     uint64_t *acc_full = bars + 3 * kMaxStages;
     uint64_t *acc_empty = acc_full + 2;
     uint64_t *b_res = acc_empty + 2;
+    uint64_t *stg_full = b_res + 1;
+    uint64_t *stg_empty = stg_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + 512);
-    const uint32_t stage0 = smem_u32(smem_raw) + 1024;
+    const uint32_t stg0 = smem_u32(smem_raw) + 1024;
+    const uint32_t stage0 = stg0 + P.nstg * P.stg_bytes;
     const uint32_t stage_stride = P.a_stage_bytes + (P.b_resident ? 0u : P.b_stage_bytes);
     const uint32_t bres_addr = stage0 + P.nstages * stage_stride;
 
@@ -202,10 +200,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             mbar_init(acc_empty + i, kEpilogueThreads / 32);
         }
         mbar_init(b_res, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(stg_full + i, 1);
+            mbar_init(stg_empty + i, kProducerThreads);
+        }
         mbar_fence_init();
     }
     constexpr int kEpiWarp0 = kProducerThreads / 32;
     constexpr int kMmaWarp = kEpiWarp0 + kEpilogueThreads / 32;
+    constexpr int kTmaWarp = kMmaWarp + 1;
     if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
     fence_before_sync();
     __syncthreads();
@@ -220,15 +223,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             mbar_arrive_expect_tx(b_res, bytes);
             bulk_g2s_u32(bres_addr, P.wpack, bytes, b_res);
         }
-        int stage = 0;
-        uint32_t phase = 0;
+        int stage = 0, sb = 0;
+        uint32_t phase = 0, sphase = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             const Item it = decode_item(P, item);
             const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
             for (int ch = it.c_begin; ch < it.c_end; ++ch) {
                 if (tid == 0) TRACE(0, ii, 0);
                 mbar_wait(a_empty + stage, phase ^ 1);
-                if (tid == 0) TRACE(0, ii, 1);
                 const uint32_t a_stage = stage0 + stage * stage_stride;
                 if (!P.b_resident && tid == 0) {
                     const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
@@ -238,10 +240,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     mbar_arrive_expect_tx(b_full + stage, bytes);
                     bulk_g2s_u32(a_stage + P.a_stage_bytes, P.wpack + off, bytes, b_full + stage);
                 }
-                if (!(P.dbg & 1)) load_window(P, it, ch, a_stage, tid);
-                cp_async_mbar_arrive(a_full + stage);   // arrives when this thread's copies land
+                mbar_wait(stg_full + sb, sphase);
+                if (tid == 0) TRACE(0, ii, 1);
+                if (!(P.dbg & 1)) repack_window(P, it, stg0 + sb * P.stg_bytes, a_stage, tid);
+                fence_proxy_async_smem();
+                mbar_arrive(a_full + stage);
+                mbar_arrive(stg_empty + sb);
                 if (tid == 0) TRACE(0, ii, 2);
                 if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+                if (++sb == P.nstg) { sb = 0; sphase ^= 1; }
             }
         }
     } else if (warp < kMmaWarp) {
@@ -299,6 +306,29 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             if (lane == 0) mbar_arrive(acc_empty + abuf);
             if (row == 0) TRACE(2, ii, 3);
             if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+        }
+    } else if (warp == kTmaWarp) {
+        // ================================================= TMA staging
+        if (lane == 0) {
+            tma::prefetch_desc(&P.tmap);
+            int sb = 0;
+            uint32_t sphase = 0;
+            for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+                const Item it = decode_item(P, item);
+                for (int ch = it.c_begin; ch < it.c_end; ++ch) {
+                    mbar_wait(stg_empty + sb, sphase ^ 1);
+                    const uint32_t stg = stg0 + sb * P.stg_bytes;
+                    const uint32_t mb = smem_u32(stg_full + sb);
+                    if (!(P.dbg & 1)) {
+                        // arm with the exact byte count, then issue the copies
+                        mbar_arrive_expect_tx(stg_full + sb, staging_bytes(P, it));
+                        issue_staging(P, it, ch, stg, mb);
+                    } else {
+                        mbar_arrive(stg_full + sb);
+                    }
+                    if (++sb == P.nstg) { sb = 0; sphase ^= 1; }
+                }
+            }
         }
     } else {
         // ================================================= MMA issuer
@@ -565,8 +595,8 @@ Plan make_plan(const Problem &p, bool dgrad) {
     const int nsm = device_info().num_sms;
     const long long base_items = (long long)P.nog * P.n_ntiles * P.n_mtiles;
     std::vector<int> ccs;
-    for (int cc = P.CSpad; cc >= 4; cc -= 4)
-        if (P.CSpad % cc == 0 && (cc <= 64 || cc == P.CSpad)) ccs.push_back(cc);
+    for (int cc = std::min(P.CSpad, 16); cc >= 4; cc -= 4)   // TMA box: cc*16 <= 256 elements
+        if (P.CSpad % cc == 0) ccs.push_back(cc);
     bool found = false;
     for (int cc : ccs) {
         const int nchunks = P.CSpad / cc;
@@ -579,26 +609,37 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const long long items = (long long)P.nog * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
             if (G > 1 && items < 2 * nsm && !force_g) continue;
             const int win_px = ((G * kTilePix + max_span) + 1) & ~1;
-            // k-chunk planes staggered by 64 bytes mod 128: a warp's 32 pieces
-            // (c, d1) of one pixel then cover every bank exactly twice (two
-            // wavefronts, the minimum for 256 bytes)
-            const uint32_t a_lbo = (uint32_t)win_px * 64 + 64;
+            // k-chunk planes staggered by 16 bytes mod 128: the repack's 8-byte
+            // stores of a warp (lanes = (pixel, c, i) units) then hit every
+            // bank exactly twice -- two wavefronts, the minimum for 256 bytes
+            const uint32_t a_lbo = (uint32_t)win_px * 64 + 16;
             const uint32_t plane = (uint32_t)(cc / 2) * a_lbo;
             const uint32_t a_stage = (uint32_t)P.npl * plane;
             const uint32_t b_stage = (uint32_t)max_taps_g * (cc / 2) * P.N_tile * 16;
             const bool bres = (P.nog == 1 && nchunks == 1 && P.n_ntiles == 1);
-            int best_st = 0;
-            for (int st = std::min(kMaxStages, 4); st >= 2; --st) {
-                const uint64_t bytes = 1024 + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
-                if (bytes <= kSmemLimit) { best_st = st; break; }
-            }
-            if (!best_st || (best_st < 3 && G > 1 && !force_g)) continue;
+            // staging of the natural layout (whole virtual rows, or BB-image boxes)
+            const bool batch_mode = (P.Hg * P.Wg == 1);
+            if (!batch_mode && P.Wg * s > 256) continue;
+            const int BB = std::min(win_px, 256);
+            const int cap = batch_mode ? ceil_div(win_px, BB) * BB : ((win_px - 1) / P.Wg + 2) * P.Wg;
+            const uint32_t stg_plane = (uint32_t)cap * cc * 32;
+            const uint32_t stg = (uint32_t)P.npl * stg_plane;
+            int best_st = 0, best_nstg = 0;
+            for (int nstg = 2; nstg >= 1 && !best_st; --nstg)
+                for (int st = std::min(kMaxStages, 4); st >= (nstg == 2 ? 2 : 3); --st) {
+                    const uint64_t bytes = 1024 + (uint64_t)nstg * stg + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) +
+                                           (bres ? b_stage : 0);
+                    if (bytes <= kSmemLimit) { best_st = st; best_nstg = nstg; break; }
+                }
+            if (!best_st) continue;
+            P.stg_batch_mode = batch_mode ? 1 : 0; P.BB = BB; P.stg_cap_px = cap;
+            P.stg_plane_bytes = stg_plane; P.stg_bytes = stg; P.nstg = best_nstg;
             if (a_lbo >= (1u << 18) || b_stage >= (1u << 20)) continue;
             P.CC = cc; P.nchunks = nchunks; P.ksplit = ksplit; P.G = G;
             P.win_px = win_px; P.a_lbo = a_lbo; P.plane_bytes = plane;
             P.a_stage_bytes = a_stage; P.b_stage_bytes = b_stage;
             P.b_resident = bres ? 1 : 0; P.nstages = best_st;
-            P.smem_bytes = 1024 + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
+            P.smem_bytes = 1024 + best_nstg * stg + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
             found = true;
             break;
         }
@@ -612,7 +653,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
     P.tmem_cols = cols;
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
-    P.fd_units.init((uint32_t)(4 * P.CC));
+    P.fd_units.init((uint32_t)(2 * P.CC));
 
     pl.wpack_bytes = align256((size_t)P.n_ntiles * P.nchunks * P.ntaps * (P.CC / 2) * P.N_tile * 16);
     pl.part_bytes = P.ksplit > 1 ? align256((size_t)P.ksplit * P.n_mtiles * 128 * P.n_ntiles * P.N_tile * 4) : 0;
@@ -630,18 +671,13 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
                      cudaStream_t st) {
     ConvMma &P = pl.P;
     if (ws_bytes < pl.wpack_bytes + pl.part_bytes) return cudaErrorInvalidValue;
-    static const bool debug = getenv("CAPSCONV_DEBUG") != nullptr;
     static const int dbg_bits = getenv("CAPSCONV_MMA_DBG") ? atoi(getenv("CAPSCONV_MMA_DBG")) : 0;
     P.dbg = dbg_bits;
-    if (debug)
-        fprintf(stderr,
-                "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
-                "nchunks=%d ksplit=%d G=%d mtiles=%d items=%d win_px=%d stages=%d bres=%d smem=%u tmem=%u\n",
-                pl.pack.dgrad ? "dgrad" : "fwd", P.CS, P.NCH, P.Hg, P.Wg, P.npl, P.nog, P.ntaps, P.N_tile,
-                P.n_ntiles, P.CC, P.nchunks, P.ksplit, P.G, P.n_mtiles, P.n_items, P.win_px, P.nstages,
-                P.b_resident, P.smem_bytes, P.tmem_cols);
     uint8_t *w = static_cast<uint8_t *>(ws);
     P.src = static_cast<const __nv_bfloat16 *>(src);
+    if (!make_capsule_tmap(&P.tmap, src, P.Bn, P.src_H, P.src_W, P.CS, P.CC, P.stg_batch_mode ? 1 : P.Wg, 1,
+                           P.stg_batch_mode ? P.BB : 1, P.stg_batch_mode ? 1 : P.pl_s))
+        return cudaErrorInvalidValue;
     P.wpack = w;
     P.out = static_cast<__nv_bfloat16 *>(out);
     P.part = pl.part_bytes ? reinterpret_cast<float *>(w + pl.wpack_bytes) : nullptr;
@@ -713,18 +749,29 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
         if (kv.first == k) return kv.second;
     if (cache.size() > 256) cache.clear();
     cache.emplace_back(k, make_plan(p, dgrad));
-    return cache.back().second;
+    const Plan &pl = cache.back().second;
+    if (getenv("CAPSCONV_DEBUG") && pl.ok) {
+        const ConvMma &P = pl.P;
+        fprintf(stderr,
+                "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
+                "nchunks=%d ksplit=%d G=%d mtiles=%d items=%d win_px=%d stages=%d bres=%d smem=%u tmem=%u nstg=%d "
+                "stg_cap=%d batch=%d\n",
+                dgrad ? "dgrad" : "fwd", P.CS, P.NCH, P.Hg, P.Wg, P.npl, P.nog, P.ntaps, P.N_tile, P.n_ntiles, P.CC,
+                P.nchunks, P.ksplit, P.G, P.n_mtiles, P.n_items, P.win_px, P.nstages, P.b_resident, P.smem_bytes,
+                P.tmem_cols, P.nstg, P.stg_cap_px, P.stg_batch_mode);
+    }
+    return pl;
 }
 
 }  // namespace
 
 bool mma_supported(capsconv_op_t op, const Problem &p) {
-    if (op == CAPSCONV_OP_BWD_KERNEL) return false;
+    if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_supported(p);
     return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }
 
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
-    if (op == CAPSCONV_OP_BWD_KERNEL) return 0;
+    if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_workspace_bytes(p);
     const Plan &pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
     return pl.ok ? pl.wpack_bytes + pl.part_bytes : 0;
 }
@@ -743,8 +790,9 @@ cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *
     return run_plan(pl, dO, K, dI, ws, ws_bytes, st);
 }
 
-cudaError_t mma_bwd_kernel(const Problem &, const void *, const void *, float *, void *, size_t, cudaStream_t) {
-    return cudaErrorNotSupported;
+cudaError_t mma_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
+                           cudaStream_t st) {
+    return wgrad_run(p, I, dO, dK, ws, ws_bytes, st);
 }
 
 }  // namespace capsconv

@@ -1,0 +1,622 @@
+// wgrad.cu -- the kernel gradient dK on tcgen05 / TMEM.
+//
+// Algorithm 4 (output_extend -> strided_batched_matrix_
+// multiply(O'_d, I') -> reduce to K_diff), read as the adjoint (DESIGN.md
+// R10/R11):
+//     dK[p,q,c,c',d2,d3] = sum_{b,x',y',d1} I[b, x's+p, y's+q, c, d1, d2] * dO[b,x',y',c',d1,d3]
+// is one long-K GEMM per tap with M = (c, d2), N = (c', d3) and the reduction
+// K = (virtual pixel v, d1).  The paper's replicated I'/O'_d buffers and its
+// separate reduction pass become: a TMA-staged window of I and dO per stage,
+// repacked in shared memory into MN-major operands (the D1 row transpose of a
+// capsule is an 8-byte shuffle no TMA layout can express), and fp32
+// accumulation in TMEM across the whole pixel range of a work item.
+//
+// M packing: one 128-row M tile holds several *slots* (tap, channel range);
+// each slot is the staged input window read at that tap's shift, so small
+// C (4*C < 128) still fills the tensor core.  Work items = (M tile, split of
+// the pixel range); split partials are summed in a fixed order by a
+// finalize kernel (deterministic, no atomics).
+//
+// Roles (320 threads): warps 0-3 repack, warps 4-7 epilogue, warp 8 MMA,
+// warp 9 TMA.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
+#include "conv_mma.cuh"
+#include "internal.h"
+#include "tma.h"
+#include "umma.cuh"
+
+namespace capsconv {
+using namespace umma;
+
+namespace {
+
+constexpr int kWRepack = 256, kWEpi = 128;
+constexpr int kWThreads = kWRepack + kWEpi + 64;
+constexpr int kWMaxTiles = 96;
+constexpr int kWMaxSlots = 4;
+constexpr int kWMaxStages = 4;
+
+struct WSlot {
+    int tap, plane, shift, c0, cn, row0;   // rows [row0, row0 + 4*cn) of the tile
+    FastDiv fd_upp;                        // 2*cn units per pixel
+};
+
+struct WTile {
+    int nslots;
+    WSlot slot[kWMaxSlots];
+    int np;                                // distinct input planes staged for this tile
+    int plane[kWMaxSlots];
+    int minsh[kWMaxSlots], span[kWMaxSlots];
+    int c_lo, c_hi;                        // staged channel range
+};
+
+struct WgradMma {
+    alignas(64) CUtensorMap tm_I;
+    alignas(64) CUtensorMap tm_O;
+    float *part;                           // [ksplit][KH*KW*C*Cout*16] (ksplit > 1) or dK itself
+    int Bn, Hg, Wg, vtotal;
+    FastDiv fd_Wg, fd_HgWg;
+    int batch_mode;                        // Hg*Wg == 1 (fully-connected view)
+    int C, Cout, ntaps, s;
+    int pl_oy[4], pl_ox[4];
+    int n_mtiles;
+    WTile tile[kWMaxTiles];
+    int N_tile;
+    int KP;                                // virtual pixels per stage (multiple of 4)
+    int ksplit, kpix;                      // pixels per split (multiple of KP)
+    int n_items;
+    int CBI, CBO;                          // channels per TMA box (I, dO)
+    FastDiv fd_uppO;                       // 2*Cout units per pixel
+    int capI, capO;                        // staging capacity (pixels) per I plane / for dO
+    uint32_t stgI_plane, stgI_bytes, stgO_bytes, stg_bytes;
+    uint32_t a_sbo, a_bytes, b_sbo, b_bytes;
+    int nstg, nstages;
+    uint32_t smem_bytes, tmem_cols;
+    unsigned long long *trace;             // debug: globaltimer stamps of CTA 0 [role][stage][4]
+};
+#define WTRACE(role, idx, ev)                                                              \
+    do {                                                                                   \
+        if (P.trace && blockIdx.x == 0 && (idx) < 64) P.trace[((role) * 64 + (idx)) * 4 + (ev)] = gtime(); \
+    } while (0)
+
+__device__ __forceinline__ void wdecode(const WgradMma &P, int item, int &mt, int &ks, int &p0, int &p1) {
+    ks = item % P.ksplit;
+    mt = item / P.ksplit;
+    p0 = ks * P.kpix;
+    p1 = min(P.vtotal, p0 + P.kpix);
+}
+
+// Rows mode: the window [v0, v0 + len) as whole virtual rows; returns the
+// staging pixel offset of v0.  Batch mode: boxes of KP images at v0.
+__device__ __forceinline__ uint32_t w_stage_window(const WgradMma &P, const CUtensorMap *tm, int v0, int len,
+                                                   int cb, int nbox, int c_first, int ox, int oy, int cs, int cap,
+                                                   uint32_t dst, uint32_t mbar, bool issue) {
+    const uint32_t px = (uint32_t)cb * 32u;
+    uint32_t bytes = 0;
+    for (int bx = 0; bx < nbox; ++bx) {
+        const uint32_t base = dst + (uint32_t)bx * cap * px;
+        const int c0 = (c_first + bx * cb) * 16;
+        if (P.batch_mode) {
+            if (issue) tma::load4d(base, tm, c0, 0, 0, v0, mbar);
+            bytes += (uint32_t)P.KP * px;
+        } else {
+            const int Ra = floor_div(v0, P.Wg), Rb = floor_div(v0 + len - 1, P.Wg);
+            for (int R = Ra; R <= Rb; ++R) {
+                const int b = floor_div(R, P.Hg);
+                const int Y = R - b * P.Hg;
+                if (issue) tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px, tm, c0, ox, cs * Y + oy, b, mbar);
+                bytes += (uint32_t)P.Wg * px;
+            }
+        }
+    }
+    return bytes;
+}
+
+__device__ __forceinline__ int w_off(const WgradMma &P, int v0) {
+    return P.batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
+}
+
+__device__ __forceinline__ uint32_t w_issue(const WgradMma &P, const WTile &T, int v0, uint32_t stg, uint32_t mbar,
+                                            bool issue) {
+    uint32_t bytes = 0;
+    const int ci = T.c_hi - T.c_lo;
+    const int nbI = (ci + P.CBI - 1) / P.CBI;
+    for (int k = 0; k < T.np; ++k) {
+        const int pl = T.plane[k];
+        bytes += w_stage_window(P, &P.tm_I, v0 + T.minsh[k], P.KP + T.span[k], P.CBI, nbI, T.c_lo, P.pl_ox[pl],
+                                P.pl_oy[pl], P.s, P.capI, stg + k * P.stgI_plane, mbar, issue);
+    }
+    const int nbO = (P.Cout + P.CBO - 1) / P.CBO;
+    bytes += w_stage_window(P, &P.tm_O, v0, P.KP, P.CBO, nbO, 0, 0, 0, 1, P.capO, stg + P.stgI_bytes, mbar, issue);
+    return bytes;
+}
+
+// Repack staged natural-layout capsules into the MN-major operands:
+//   A (rows m = slot (c, d2), k-rows (v, d1)): m-group g = row/8 is a plane of
+//     KP*4 rows x 16 bytes (a_sbo apart); a capsule unit (c, rows d1 = 2i, 2i+1)
+//     becomes two 8-byte pieces at k-rows (v, 2i) and (v, 2i+1), half (c & 1).
+//   B (columns n = (c', d3)) likewise from dO.
+__device__ __forceinline__ void w_repack(const WgradMma &P, const WTile &T, int v0, uint32_t stg, uint32_t a,
+                                         uint32_t b, int tid) {
+    const int KP = P.KP;
+    // ---- B from dO: units (v, c', i)
+    {
+        const int offO = w_off(P, v0);
+        const uint32_t base = stg + P.stgI_bytes;
+        const int upp = 2 * P.Cout;
+        const int total = KP * upp;
+        const uint32_t pxb = (uint32_t)P.CBO * 32u;
+#pragma unroll 4
+        for (int L = tid; L < total; L += kWRepack) {
+            const int vl = (int)P.fd_uppO.div((uint32_t)L);
+            const int u = L - vl * upp;
+            const int c = u >> 1, i = u & 1;
+            const int bx = c / P.CBO, cc = c - bx * P.CBO;
+            const uint4 v = ld_shared_v4(base + (uint32_t)bx * P.capO * pxb + (uint32_t)(vl + offO) * pxb +
+                                         (uint32_t)(cc * 32 + i * 16));
+            const uint32_t dst = b + (uint32_t)(c >> 1) * P.b_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u + (c & 1) * 8u;
+            st_shared_v2(dst, v.x, v.y);
+            st_shared_v2(dst + 16u, v.z, v.w);
+        }
+    }
+    // ---- A from I: per slot, units (v, c, i) read at the slot's shift
+    const uint32_t pxb = (uint32_t)P.CBI * 32u;
+    for (int j = 0; j < T.nslots; ++j) {
+        const WSlot &S = T.slot[j];
+        int k = 0;
+        while (T.plane[k] != S.plane) ++k;
+        const int vs = v0 + S.shift;                 // first staged pixel this slot reads
+        const int w0 = v0 + T.minsh[k];              // first pixel of the staged window of plane k
+        const int off = w_off(P, w0) + (vs - w0);
+        const uint32_t base = stg + k * P.stgI_plane;
+        const int upp = 2 * S.cn;
+        const int total = KP * upp;
+#pragma unroll 4
+        for (int L = tid; L < total; L += kWRepack) {
+            const int vl = (int)S.fd_upp.div((uint32_t)L);
+            const int u = L - vl * upp;
+            const int cl = u >> 1, i = u & 1;
+            const int c = S.c0 + cl - T.c_lo;
+            const int bx = c / P.CBI, cc = c - bx * P.CBI;
+            const uint4 v = ld_shared_v4(base + (uint32_t)bx * P.capI * pxb + (uint32_t)(vl + off) * pxb +
+                                         (uint32_t)(cc * 32 + i * 16));
+            const int row = S.row0 + cl * 4;         // first m row of channel cl (d2 = 0)
+            const uint32_t dst = a + (uint32_t)(row >> 3) * P.a_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
+                                 (uint32_t)((row & 7) * 2);
+            st_shared_v2(dst, v.x, v.y);
+            st_shared_v2(dst + 16u, v.z, v.w);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_constant__ WgradMma P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
+    uint64_t *stg_full = bars, *stg_empty = bars + 2;
+    uint64_t *op_full = bars + 4, *op_empty = op_full + kWMaxStages;
+    uint64_t *acc_full = op_empty + kWMaxStages, *acc_empty = acc_full + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + 512);
+    const uint32_t stg0 = smem_u32(smem_raw) + 1024;
+    const uint32_t op0 = stg0 + P.nstg * P.stg_bytes;
+    const uint32_t op_stride = P.a_bytes + P.b_bytes;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    constexpr int kEpi0 = kWRepack / 32, kMma = kEpi0 + kWEpi / 32, kTma = kMma + 1;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(stg_full + i, 1);
+            mbar_init(stg_empty + i, kWRepack);
+            mbar_init(acc_full + i, 1);
+            mbar_init(acc_empty + i, kWEpi / 32);
+        }
+        for (int s = 0; s < P.nstages; ++s) {
+            mbar_init(op_full + s, kWRepack);
+            mbar_init(op_empty + s, 1);
+        }
+        mbar_fence_init();
+    }
+    if (warp == kMma) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == kTma) {
+        if (lane == 0) {
+            tma::prefetch_desc(&P.tm_I);
+            tma::prefetch_desc(&P.tm_O);
+            int sb = 0;
+            uint32_t sph = 0;
+            for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+                int mt, ks, p0, p1;
+                wdecode(P, item, mt, ks, p0, p1);
+                const WTile &T = P.tile[mt];
+                for (int v0 = p0; v0 < p1; v0 += P.KP) {
+                    const int si = (v0 - p0) / P.KP;
+                    WTRACE(0, si, 0);
+                    mbar_wait(stg_empty + sb, sph ^ 1);
+                    WTRACE(0, si, 1);
+                    const uint32_t stg = stg0 + sb * P.stg_bytes;
+                    mbar_arrive_expect_tx(stg_full + sb, w_issue(P, T, v0, stg, 0, false));
+                    w_issue(P, T, v0, stg, smem_u32(stg_full + sb), true);
+                    WTRACE(0, si, 2);
+                    if (++sb == P.nstg) { sb = 0; sph ^= 1; }
+                }
+            }
+        }
+    } else if (warp < kEpi0) {
+        const int tid = threadIdx.x;
+        int sb = 0, st = 0;
+        uint32_t sph = 0, ph = 0;
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            int mt, ks, p0, p1;
+            wdecode(P, item, mt, ks, p0, p1);
+            const WTile &T = P.tile[mt];
+            for (int v0 = p0; v0 < p1; v0 += P.KP) {
+                const int si = (v0 - p0) / P.KP;
+                if (tid == 0) WTRACE(1, si, 0);
+                mbar_wait(stg_full + sb, sph);
+                if (tid == 0) WTRACE(1, si, 1);
+                mbar_wait(op_empty + st, ph ^ 1);
+                if (tid == 0) WTRACE(1, si, 2);
+                const uint32_t a = op0 + st * op_stride;
+                w_repack(P, T, v0, stg0 + sb * P.stg_bytes, a, a + P.a_bytes, tid);
+                fence_proxy_async_smem();
+                if (tid == 0) WTRACE(1, si, 3);
+                mbar_arrive(op_full + st);
+                mbar_arrive(stg_empty + sb);
+                if (++sb == P.nstg) { sb = 0; sph ^= 1; }
+                if (++st == P.nstages) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == kMma) {
+        const uint32_t idesc = idesc_bf16(128, P.N_tile, 1, 1);
+        int st = 0, abuf = 0;
+        uint32_t ph = 0, aph = 0;
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            int mt, ks, p0, p1;
+            wdecode(P, item, mt, ks, p0, p1);
+            mbar_wait(acc_empty + abuf, aph ^ 1);
+            fence_after_sync();
+            const uint32_t d = tmem + (uint32_t)(abuf * P.N_tile);
+            bool first = true;
+            for (int v0 = p0; v0 < p1; v0 += P.KP) {
+                const int si = (v0 - p0) / P.KP;
+                if (lane == 0) WTRACE(2, si, 0);
+                mbar_wait(op_full + st, ph);
+                if (lane == 0) WTRACE(2, si, 1);
+                fence_after_sync();
+                const uint32_t a = op0 + st * op_stride;
+                const uint64_t ad0 = smem_desc(a, 128, P.a_sbo);
+                const uint64_t bd0 = smem_desc(a + P.a_bytes, 128, P.b_sbo);
+                if (elect_one()) {
+                    for (int kk = 0; kk < P.KP / 4; ++kk) {   // 16 k-rows (4 pixels) per MMA
+                        mma_bf16_ss(d, ad0 + (uint64_t)(kk * 16), bd0 + (uint64_t)(kk * 16), idesc,
+                                    (first && kk == 0) ? 0u : 1u);
+                    }
+                    mma_commit(op_empty + st);
+                }
+                __syncwarp();
+                first = false;
+                if (++st == P.nstages) { st = 0; ph ^= 1; }
+            }
+            if (elect_one()) mma_commit(acc_full + abuf);
+            __syncwarp();
+            if (++abuf == 2) { abuf = 0; aph ^= 1; }
+        }
+    } else {
+        // epilogue: TMEM rows (slot, c, d2) x columns (c', d3) -> fp32 dK (or split partial)
+        const int wq = warp & 3;
+        const int row = wq * 32 + lane;
+        const size_t nk = (size_t)P.ntaps * P.C * P.Cout * 16;
+        int abuf = 0;
+        uint32_t aph = 0;
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            int mt, ks, p0, p1;
+            wdecode(P, item, mt, ks, p0, p1);
+            const WTile &T = P.tile[mt];
+            int tap = -1, c = 0, d2 = row & 3;
+            for (int j = 0; j < T.nslots; ++j) {
+                const WSlot &S = T.slot[j];
+                if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
+                    tap = S.tap;
+                    c = S.c0 + ((row - S.row0) >> 2);
+                }
+            }
+            mbar_wait(acc_full + abuf, aph);
+            fence_after_sync();
+            float *dst = P.part + (size_t)ks * nk + (((size_t)tap * P.C + c) * P.Cout) * 16 + d2 * 4;
+            const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(abuf * P.N_tile);
+            for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
+                float v[16];
+                tmem_ld16(tcol + n0, v);
+                tmem_wait_ld();
+                if (tap >= 0 && c < P.C) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int co = n0 / 4 + j;
+                        if (co < P.Cout)
+                            *reinterpret_cast<float4 *>(dst + (size_t)co * 16) =
+                                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    }
+                }
+            }
+            fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + abuf);
+            if (++abuf == 2) { abuf = 0; aph ^= 1; }
+        }
+    }
+
+    fence_before_sync();
+    __syncthreads();
+    if (warp == kMma) {
+        fence_after_sync();
+        tmem_dealloc_dyn(tmem, P.tmem_cols);
+    }
+}
+
+__global__ void __launch_bounds__(256) w_finalize(const float *__restrict__ part, float *__restrict__ dK, int64_t n,
+                                                  int ksplit) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float acc = 0.f;
+    for (int k = 0; k < ksplit; ++k) acc += part[(int64_t)k * n + i];
+    dK[i] = acc;
+}
+
+// ------------------------------------------------------------------ planning
+struct WPlan {
+    bool ok = false;
+    WgradMma P{};
+    size_t part_bytes = 0;
+    // tensor-map geometry
+    int64_t I_B, I_H, I_W, I_C, O_B, O_H, O_W, O_C;
+};
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+constexpr uint32_t kWSmemLimit = 227 * 1024;
+
+WPlan make_wplan(const Problem &p) {
+    WPlan pl;
+    WgradMma &P = pl.P;
+    if (p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return pl;
+    const bool fc = (p.KH == p.H && p.KW == p.W);
+    const int s = fc ? 1 : (int)p.s;
+    if (s > 2) return pl;
+    P.s = s;
+    std::vector<int> tplane, tshift;
+    if (fc) {
+        // fully-connected view: one pixel per image, C_eff = KH*KW*C channels, one tap
+        P.C = (int)(p.KH * p.KW * p.C);
+        P.Cout = (int)p.Cout;
+        P.Bn = (int)p.B; P.Hg = 1; P.Wg = 1; P.batch_mode = 1;
+        P.ntaps = 1;
+        P.pl_oy[0] = P.pl_ox[0] = 0;
+        tplane.push_back(0); tshift.push_back(0);
+        pl.I_B = p.B; pl.I_H = 1; pl.I_W = 1; pl.I_C = P.C;
+        pl.O_B = p.B; pl.O_H = 1; pl.O_W = 1; pl.O_C = p.Cout;
+    } else {
+        if (p.KH * p.KW > kMaxTaps) return pl;
+        P.C = (int)p.C; P.Cout = (int)p.Cout;
+        P.Bn = (int)p.B;
+        P.Hg = cdiv(p.H, s); P.Wg = cdiv(p.W, s); P.batch_mode = 0;
+        if (P.Wg * s > 256) return pl;
+        P.ntaps = (int)(p.KH * p.KW);
+        int plane_of[2][2] = {{-1, -1}, {-1, -1}}, npl = 0;
+        for (int pp = 0; pp < p.KH; ++pp)
+            for (int qq = 0; qq < p.KW; ++qq) {
+                const int a = pp % s, b = qq % s;
+                if (plane_of[a][b] < 0) { plane_of[a][b] = npl; P.pl_oy[npl] = a; P.pl_ox[npl] = b; ++npl; }
+                tplane.push_back(plane_of[a][b]);
+                tshift.push_back((pp / s) * P.Wg + qq / s);
+            }
+        pl.I_B = p.B; pl.I_H = p.H; pl.I_W = p.W; pl.I_C = p.C;
+        pl.O_B = p.B; pl.O_H = p.Ho; pl.O_W = p.Wo; pl.O_C = p.Cout;
+    }
+    const long long vt = (long long)P.Bn * P.Hg * P.Wg;
+    if (vt * 4 >= (1ll << 31)) return pl;
+    P.vtotal = (int)vt;
+    P.N_tile = cdiv(P.Cout * 4, 16) * 16;
+    if (P.N_tile > 256) return pl;
+    // ---- M tiles: slots (tap, channel range); channels in pairs (C odd -> padded slot rows)
+    const int cpad = (P.C + 1) & ~1;
+    std::vector<WTile> tiles;
+    if (4 * cpad <= 128) {
+        const int per = 128 / (4 * cpad);
+        for (int t0 = 0; t0 < P.ntaps; t0 += per) {
+            WTile T{};
+            T.nslots = std::min(per, P.ntaps - t0);
+            if (T.nslots > kWMaxSlots) return pl;
+            T.c_lo = 0; T.c_hi = P.C;
+            for (int j = 0; j < T.nslots; ++j) {
+                T.slot[j] = WSlot{t0 + j, tplane[t0 + j], tshift[t0 + j], 0, cpad, j * 4 * cpad, {}};
+                T.slot[j].fd_upp.init((uint32_t)(2 * cpad));
+            }
+            tiles.push_back(T);
+        }
+    } else {
+        for (int t = 0; t < P.ntaps; ++t)
+            for (int c0 = 0; c0 < P.C; c0 += 32) {
+                WTile T{};
+                T.nslots = 1;
+                const int cn = std::min(32, P.C - c0);
+                T.slot[0] = WSlot{t, tplane[t], tshift[t], c0, (cn + 1) & ~1, 0, {}};
+                T.slot[0].fd_upp.init((uint32_t)(2 * ((cn + 1) & ~1)));
+                T.c_lo = c0; T.c_hi = std::min(P.C, c0 + ((cn + 1) & ~1));
+                tiles.push_back(T);
+            }
+    }
+    if ((int)tiles.size() > kWMaxTiles) return pl;
+    P.n_mtiles = (int)tiles.size();
+    for (int i = 0; i < P.n_mtiles; ++i) {
+        WTile &T = tiles[i];
+        T.np = 0;
+        for (int j = 0; j < T.nslots; ++j) {
+            int k = 0;
+            while (k < T.np && T.plane[k] != T.slot[j].plane) ++k;
+            if (k == T.np) { T.plane[k] = T.slot[j].plane; T.minsh[k] = 1 << 30; T.span[k] = -(1 << 30); ++T.np; }
+            T.minsh[k] = std::min(T.minsh[k], T.slot[j].shift);
+            T.span[k] = std::max(T.span[k], T.slot[j].shift);
+        }
+        for (int k = 0; k < T.np; ++k) T.span[k] -= T.minsh[k];
+        P.tile[i] = T;
+    }
+    int max_span = 0, max_np = 1, max_ci = 0;
+    for (auto &T : tiles) {
+        for (int k = 0; k < T.np; ++k) max_span = std::max(max_span, T.span[k]);
+        max_np = std::max(max_np, T.np);
+        max_ci = std::max(max_ci, T.c_hi - T.c_lo);
+    }
+    P.CBI = std::min(16, max_ci);
+    P.CBO = std::min(16, P.Cout);
+    const int nbI = cdiv(max_ci, P.CBI), nbO = cdiv(P.Cout, P.CBO);
+    // ---- pixels per stage, staging / operand buffers
+    bool found = false;
+    for (int KP : {32, 64, 16}) {
+        if (P.batch_mode && KP > 256) continue;
+        const int capI = P.batch_mode ? KP : ((KP + max_span - 1) / P.Wg + 2) * P.Wg;
+        const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wg;
+        const uint32_t stgI_plane = (uint32_t)nbI * capI * P.CBI * 32;
+        const uint32_t stgI = (uint32_t)max_np * stgI_plane;
+        const uint32_t stgO = (uint32_t)nbO * capO * P.CBO * 32;
+        const uint32_t stg = stgI + stgO;
+        const uint32_t sbo = (uint32_t)KP * 64 + 16;     // plane stride, bank staggered
+        const uint32_t abytes = 16 * sbo, bbytes = (uint32_t)(P.N_tile / 8) * sbo;
+        for (int nstg = 2; nstg >= 1 && !found; --nstg)
+            for (int ns = 3; ns >= 2; --ns) {
+                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * (abytes + bbytes);
+                if (tot <= kWSmemLimit) {
+                    P.KP = KP; P.capI = capI; P.capO = capO; P.stgI_plane = stgI_plane; P.stgI_bytes = stgI;
+                    P.stgO_bytes = stgO; P.stg_bytes = stg; P.a_sbo = sbo; P.b_sbo = sbo; P.a_bytes = abytes;
+                    P.b_bytes = bbytes; P.nstg = nstg; P.nstages = ns; P.smem_bytes = (uint32_t)tot;
+                    found = true;
+                    break;
+                }
+            }
+        if (found) break;
+    }
+    if (!found) return pl;
+    // ---- split of the pixel range so that items fill the machine
+    const int nsm = device_info().num_sms;
+    const int nstage_total = cdiv(P.vtotal, P.KP);
+    int ks = std::max(1, std::min(nstage_total, cdiv(2 * nsm, P.n_mtiles)));
+    const int stages_per = cdiv(nstage_total, ks);
+    P.kpix = stages_per * P.KP;
+    P.ksplit = cdiv(P.vtotal, P.kpix);
+    P.n_items = P.n_mtiles * P.ksplit;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * P.N_tile)) cols <<= 1;
+    P.tmem_cols = cols;
+    P.fd_Wg.init((uint32_t)P.Wg);
+    P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
+    P.fd_uppO.init((uint32_t)(2 * P.Cout));
+    const size_t nk = (size_t)P.ntaps * P.C * P.Cout * 16;
+    pl.part_bytes = P.ksplit > 1 ? ((size_t)P.ksplit * nk * 4 + 255) & ~(size_t)255 : 0;
+    pl.ok = true;
+    return pl;
+}
+
+struct WKey {
+    int dev, nsm;
+    int64_t e[11];
+    bool operator==(const WKey &o) const {
+        if (dev != o.dev || nsm != o.nsm) return false;
+        for (int i = 0; i < 11; ++i)
+            if (e[i] != o.e[i]) return false;
+        return true;
+    }
+};
+
+const WPlan &cached_wplan(const Problem &p) {
+    static std::mutex mu;
+    static std::vector<std::pair<WKey, WPlan>> cache;
+    const DeviceInfo &di = device_info();
+    WKey k{di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s}};
+    if (p.dt != CAPSCONV_BF16) k.e[7] = -1;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto &kv : cache)
+        if (kv.first == k) return kv.second;
+    if (cache.size() > 256) cache.clear();
+    cache.emplace_back(k, make_wplan(p));
+    const WPlan &pl = cache.back().second;
+    if (getenv("CAPSCONV_DEBUG") && pl.ok) {
+        const WgradMma &P = pl.P;
+        fprintf(stderr,
+                "[capsconv] wgrad plan: C=%d Cout=%d Hg=%d Wg=%d taps=%d mtiles=%d N_tile=%d KP=%d ksplit=%d "
+                "items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u\n",
+                P.C, P.Cout, P.Hg, P.Wg, P.ntaps, P.n_mtiles, P.N_tile, P.KP, P.ksplit, P.n_items, P.capI, P.capO,
+                P.nstg, P.nstages, P.smem_bytes);
+    }
+    return pl;
+}
+
+}  // namespace
+
+bool wgrad_supported(const Problem &p) { return cached_wplan(p).ok; }
+
+size_t wgrad_workspace_bytes(const Problem &p) {
+    const WPlan &pl = cached_wplan(p);
+    return pl.ok ? pl.part_bytes : 0;
+}
+
+cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
+                      cudaStream_t st) {
+    WPlan pl = cached_wplan(p);
+    if (!pl.ok || ws_bytes < pl.part_bytes) return cudaErrorNotSupported;
+    WgradMma &P = pl.P;
+    const int boxw = P.batch_mode ? 1 : P.Wg;
+    const int boxb = P.batch_mode ? P.KP : 1;
+    if (!make_capsule_tmap(&P.tm_I, I, pl.I_B, pl.I_H, pl.I_W, pl.I_C, P.CBI, boxw, 1, boxb, P.batch_mode ? 1 : P.s))
+        return cudaErrorInvalidValue;
+    if (!make_capsule_tmap(&P.tm_O, dO, pl.O_B, pl.O_H, pl.O_W, pl.O_C, P.CBO, boxw, 1, boxb, 1))
+        return cudaErrorInvalidValue;
+    P.part = P.ksplit > 1 ? static_cast<float *>(ws) : dK;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmemLimit);
+        attr = true;
+    }
+    const int grid = std::min(P.n_items, device_info().num_sms);
+    static const bool tracing = getenv("CAPSCONV_TRACE") != nullptr;
+    P.trace = nullptr;
+    if (tracing) {
+        cudaMalloc(&P.trace, 3 * 64 * 4 * 8);
+        cudaMemset(P.trace, 0, 3 * 64 * 4 * 8);
+    }
+    wgrad_kernel<<<grid, kWThreads, P.smem_bytes, st>>>(P);
+    note_launches(1);
+    if (tracing) {
+        std::vector<unsigned long long> h(3 * 64 * 4);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), P.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        cudaFree(P.trace);
+        unsigned long long t0 = ~0ull;
+        for (auto v : h) if (v && v < t0) t0 = v;
+        const char *names[3] = {"tma ", "rpk ", "mma "};
+        for (int i = 0; i < 12; ++i)
+            for (int r = 0; r < 3; ++r) {
+                fprintf(stderr, "[wtrace] stage %2d %s", i, names[r]);
+                for (int e = 0; e < 4; ++e) {
+                    unsigned long long v = h[(r * 64 + i) * 4 + e];
+                    fprintf(stderr, " %8lld", v ? (long long)(v - t0) : -1ll);
+                }
+                fprintf(stderr, "\n");
+            }
+    }
+    if (P.ksplit > 1) {
+        const int64_t n = (int64_t)P.ntaps * P.C * P.Cout * 16;
+        w_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P.part, dK, n, P.ksplit);
+        note_launches(1);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace capsconv

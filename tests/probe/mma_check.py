@@ -17,8 +17,9 @@ for case in cases:
     Ho, Wo = oracle.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
     dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), dtype=torch.bfloat16)
     Id, Kd, dOd = I.cuda(), K.cuda(), dO.cuda()
-    paths = [cc.select_path(op, torch.bfloat16, (L.B, L.H, L.W, L.C, L.Cout, L.KH, L.KW, 4, 4, 4, L.stride)) for op in (0, 1)]
-    O = cc.fwd(Id, Kd, L.stride); dI = cc.bwd_data(dOd, Kd, L.stride, L.H, L.W); torch.cuda.synchronize()
+    paths = [cc.select_path(op, torch.bfloat16, (L.B, L.H, L.W, L.C, L.Cout, L.KH, L.KW, 4, 4, 4, L.stride)) for op in (0, 1, 2)]
+    O = cc.fwd(Id, Kd, L.stride); dI = cc.bwd_data(dOd, Kd, L.stride, L.H, L.W); dK = cc.bwd_kernel(Id, dOd, L.stride, L.KH, L.KW); torch.cuda.synchronize()
+    rdK, adK = oracle.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
     rO, aO = oracle.fwd(to_np(I), to_np(K), L.stride)
     rdI, adI = oracle.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
-    print(case, "paths", paths, "fwd err %.2e" % rel_err(to_np(O), rO, aO), "dI err %.2e" % rel_err(to_np(dI), rdI, adI), flush=True)
+    print(case, "paths", paths, "fwd err %.2e" % rel_err(to_np(O), rO, aO), "dI err %.2e" % rel_err(to_np(dI), rdI, adI), "dK err %.2e" % rel_err(to_np(dK), rdK, adK), flush=True)

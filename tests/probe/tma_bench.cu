@@ -1,0 +1,57 @@
+// TMA throughput microbenchmark: every CTA (one per SM) streams `iters` rounds
+// of `nbox` copies into shared memory (mode 0: 4-D tensor boxes of the capsule
+// map; mode 1: 1-D bulk copies of the same byte count), one mbarrier per round.
+#include <cuda.h>
+#include <cstdio>
+#include "umma.cuh"
+#include "tma.h"
+using namespace capsconv;
+using namespace capsconv::umma;
+
+__global__ void tbench(const __grid_constant__ CUtensorMap tm, const uint8_t *src, int mode, int nbox, int iters,
+                       int box_bytes, int W, int nrows_total, unsigned long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const uint32_t dst = smem_u32(smem);
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        mbar_arrive_expect_tx(&bar, (uint32_t)(nbox * box_bytes));
+        for (int b = 0; b < nbox; ++b) {
+            const int row = (blockIdx.x * 37 + it * nbox + b + blockIdx.x * iters * nbox) % nrows_total;
+            if (mode == 0) tma::load4d(dst + b * box_bytes, &tm, 0, 0, row % 24, row / 24, smem_u32(&bar));
+            else bulk_g2s_u32(dst + b * box_bytes, src + (size_t)row * W * 256, box_bytes, &bar);
+        }
+        mbar_wait(&bar, it & 1);
+    }
+    unsigned long long t1 = clock64();
+    if (blockIdx.x == 0) *out = t1 - t0;
+}
+
+extern "C" double tma_bench(int mode, int nbox, int iters, int W, int rows_per_box, int B) {
+    // tensor: B images of 24 x W pixels, 8 channels x 16 bf16 (256 B / pixel)
+    const int64_t H = 24, CS = 8;
+    uint8_t *src;
+    cudaMalloc(&src, (size_t)B * H * W * 256);
+    cudaMemset(src, 1, (size_t)B * H * W * 256);
+    CUtensorMap tm;
+    if (!make_capsule_tmap(&tm, src, B, H, W, CS, 8, W, rows_per_box, 1, 1)) return -2;
+    unsigned long long *d;
+    cudaMalloc(&d, 8);
+    const int box_bytes = W * 256 * rows_per_box;
+    cudaFuncSetAttribute(tbench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    tbench<<<148, 32, 200 * 1024>>>(tm, src, mode, nbox, iters, box_bytes, W, (int)(B * H - 8), d);
+    cudaDeviceSynchronize();
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    tbench<<<148, 32, 200 * 1024>>>(tm, src, mode, nbox, iters, box_bytes, W, (int)(B * H - 8), d);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaDeviceSynchronize();
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    cudaFree(src); cudaFree(d);
+    if (e != cudaSuccess) return -1;
+    const double bytes = 148.0 * iters * nbox * box_bytes;
+    return bytes / (ms * 1e-3) / 1e9;   // GB/s chip-wide
+}
