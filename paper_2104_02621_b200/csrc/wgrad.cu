@@ -17,8 +17,18 @@
 // the pixel range); split partials are summed in a fixed order by a
 // finalize kernel (deterministic, no atomics).
 //
-// Roles (320 threads): warps 0-3 repack, warps 4-7 epilogue, warp 8 MMA,
-// warp 9 TMA.
+// Operands: A (rows m = slot (c, d2), K = (v, d1)) lives in TENSOR MEMORY:
+// loader warps read each capsule row from the staged window (one 8-byte load
+// per lane), transpose the 4x4 capsule in registers (d1 <-> d2, two shuffle
+// rounds) and write the slot's shifted copy with tcgen05.st straight into the
+// lane quarter it owns -- no shared-memory round trip for the replicated
+// operand, and the TS-form MMA avoids re-reading A from shared memory
+// (measured ~2x cheaper than SS at N = 32).  B (dO, columns (c', d3)) is one
+// MN-major shared-memory operand.  A CTA accumulates a group of M tiles over
+// a pixel range, so the staged window is shared by all the taps it holds.
+//
+// Roles (416 threads): warps 0-7 loaders (two per TMEM lane quarter), warps
+// 8-11 epilogue, warp 12 MMA, warp 13 TMA.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -37,8 +47,8 @@ using namespace umma;
 
 namespace {
 
-constexpr int kWRepack = 256, kWEpi = 128;
-constexpr int kWThreads = kWRepack + kWEpi + 64;
+constexpr int kWLoad = 256, kWEpi = 128;
+constexpr int kWThreads = kWLoad + kWEpi + 64;
 constexpr int kWMaxTiles = 96;
 constexpr int kWMaxSlots = 4;
 constexpr int kWMaxStages = 4;
@@ -68,6 +78,11 @@ struct WgradMma {
     int pl_oy[4], pl_ox[4];
     int n_mtiles;
     WTile tile[kWMaxTiles];
+    int TG, n_groups;                      // M tiles per CTA group, groups
+    int g_np[kWMaxTiles];                  // per group: staged I planes (union over its tiles)
+    int g_plane[kWMaxTiles][4], g_minsh[kWMaxTiles][4], g_span[kWMaxTiles][4];
+    int g_clo[kWMaxTiles], g_chi[kWMaxTiles];
+    uint32_t acc_cols, abuf_cols;          // TMEM: accumulators, then A buffers
     int N_tile;
     int KP;                                // virtual pixels per stage (multiple of 4)
     int ksplit, kpix;                      // pixels per split (multiple of KP)
@@ -76,7 +91,7 @@ struct WgradMma {
     FastDiv fd_uppO;                       // 2*Cout units per pixel
     int capI, capO;                        // staging capacity (pixels) per I plane / for dO
     uint32_t stgI_plane, stgI_bytes, stgO_bytes, stg_bytes;
-    uint32_t a_sbo, a_bytes, b_sbo, b_bytes;
+    uint32_t b_sbo, b_bytes;
     int nstg, nstages;
     uint32_t smem_bytes, tmem_cols;
     unsigned long long *trace;             // debug: globaltimer stamps of CTA 0 [role][stage][4]
@@ -88,7 +103,7 @@ struct WgradMma {
 
 __device__ __forceinline__ void wdecode(const WgradMma &P, int item, int &mt, int &ks, int &p0, int &p1) {
     ks = item % P.ksplit;
-    mt = item / P.ksplit;
+    mt = item / P.ksplit;                  // group index
     p0 = ks * P.kpix;
     p1 = min(P.vtotal, p0 + P.kpix);
 }
@@ -123,75 +138,116 @@ __device__ __forceinline__ int w_off(const WgradMma &P, int v0) {
     return P.batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
 }
 
-__device__ __forceinline__ uint32_t w_issue(const WgradMma &P, const WTile &T, int v0, uint32_t stg, uint32_t mbar,
+__device__ __forceinline__ uint32_t w_issue(const WgradMma &P, int g, int v0, uint32_t stg, uint32_t mbar,
                                             bool issue) {
     uint32_t bytes = 0;
-    const int ci = T.c_hi - T.c_lo;
+    const int ci = P.g_chi[g] - P.g_clo[g];
     const int nbI = (ci + P.CBI - 1) / P.CBI;
-    for (int k = 0; k < T.np; ++k) {
-        const int pl = T.plane[k];
-        bytes += w_stage_window(P, &P.tm_I, v0 + T.minsh[k], P.KP + T.span[k], P.CBI, nbI, T.c_lo, P.pl_ox[pl],
-                                P.pl_oy[pl], P.s, P.capI, stg + k * P.stgI_plane, mbar, issue);
+    for (int k = 0; k < P.g_np[g]; ++k) {
+        const int pl = P.g_plane[g][k];
+        bytes += w_stage_window(P, &P.tm_I, v0 + P.g_minsh[g][k], P.KP + P.g_span[g][k], P.CBI, nbI, P.g_clo[g],
+                                P.pl_ox[pl], P.pl_oy[pl], P.s, P.capI, stg + k * P.stgI_plane, mbar, issue);
     }
     const int nbO = (P.Cout + P.CBO - 1) / P.CBO;
     bytes += w_stage_window(P, &P.tm_O, v0, P.KP, P.CBO, nbO, 0, 0, 0, 1, P.capO, stg + P.stgI_bytes, mbar, issue);
     return bytes;
 }
 
-// Repack staged natural-layout capsules into the MN-major operands:
-//   A (rows m = slot (c, d2), k-rows (v, d1)): m-group g = row/8 is a plane of
-//     KP*4 rows x 16 bytes (a_sbo apart); a capsule unit (c, rows d1 = 2i, 2i+1)
-//     becomes two 8-byte pieces at k-rows (v, 2i) and (v, 2i+1), half (c & 1).
-//   B (columns n = (c', d3)) likewise from dO.
-__device__ __forceinline__ void w_repack(const WgradMma &P, const WTile &T, int v0, uint32_t stg, uint32_t a,
-                                         uint32_t b, int tid) {
-    const int KP = P.KP;
-    // ---- B from dO: units (v, c', i)
-    {
-        const int offO = w_off(P, v0);
-        const uint32_t base = stg + P.stgI_bytes;
-        const int upp = 2 * P.Cout;
-        const int total = KP * upp;
-        const uint32_t pxb = (uint32_t)P.CBO * 32u;
+// dO -> B: MN-major shared-memory operand, columns n = (c', d3) in groups of
+// 8 (c' pair), k-rows (v, d1) at 16 bytes; a capsule unit (c', d1 rows 2i,
+// 2i+1) becomes two 8-byte pieces (the D1 transpose).
+__device__ __forceinline__ void w_load_B(const WgradMma &P, int v0, uint32_t stg, uint32_t b, int tid) {
+    const int offO = w_off(P, v0);
+    const uint32_t base = stg + P.stgI_bytes;
+    const int upp = 2 * P.Cout;
+    const int total = P.KP * upp;
+    const uint32_t pxb = (uint32_t)P.CBO * 32u;
 #pragma unroll 4
-        for (int L = tid; L < total; L += kWRepack) {
-            const int vl = (int)P.fd_uppO.div((uint32_t)L);
-            const int u = L - vl * upp;
-            const int c = u >> 1, i = u & 1;
-            const int bx = c / P.CBO, cc = c - bx * P.CBO;
-            const uint4 v = ld_shared_v4(base + (uint32_t)bx * P.capO * pxb + (uint32_t)(vl + offO) * pxb +
-                                         (uint32_t)(cc * 32 + i * 16));
-            const uint32_t dst = b + (uint32_t)(c >> 1) * P.b_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u + (c & 1) * 8u;
-            st_shared_v2(dst, v.x, v.y);
-            st_shared_v2(dst + 16u, v.z, v.w);
-        }
+    for (int L = tid; L < total; L += kWLoad) {
+        const int vl = (int)P.fd_uppO.div((uint32_t)L);
+        const int u = L - vl * upp;
+        const int c = u >> 1, i = u & 1;
+        const int bx = c / P.CBO, cc = c - bx * P.CBO;
+        const uint4 v = ld_shared_v4(base + (uint32_t)bx * P.capO * pxb + (uint32_t)(vl + offO) * pxb +
+                                     (uint32_t)(cc * 32 + i * 16));
+        const uint32_t dst = b + (uint32_t)(c >> 1) * P.b_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u + (c & 1) * 8u;
+        st_shared_v2(dst, v.x, v.y);
+        st_shared_v2(dst + 16u, v.z, v.w);
     }
-    // ---- A from I: per slot, units (v, c, i) read at the slot's shift
+}
+
+// 4x4 transpose of bf16 capsule rows across the 4 lanes of a group:
+// lane d1 holds row d1 (lo = d2 0..1, hi = d2 2..3); afterwards lane d2 holds
+// column d2 (lo = d1 0..1, hi = d1 2..3).
+__device__ __forceinline__ void transpose4x4(uint32_t &lo, uint32_t &hi, int r) {
+    const uint32_t t = (r & 2) ? lo : hi;
+    const uint32_t x = __shfl_xor_sync(0xffffffffu, t, 2);
+    if (r & 2) lo = x; else hi = x;
+    const uint32_t plo = __shfl_xor_sync(0xffffffffu, lo, 1);
+    const uint32_t phi = __shfl_xor_sync(0xffffffffu, hi, 1);
+    if (r & 1) {
+        lo = __byte_perm(lo, plo, 0x3276);
+        hi = __byte_perm(hi, phi, 0x3276);
+    } else {
+        lo = __byte_perm(lo, plo, 0x5410);
+        hi = __byte_perm(hi, phi, 0x5410);
+    }
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+// I -> A in TMEM for every tile of the group: this warp owns lane quarter q
+// (rows q*32 .. q*32+31 of each tile) and the k-steps kk = half (mod 2).
+// Lane group g = lane/4 is one (slot, channel); lane & 3 is the capsule row d1
+// when loading and the column d2 after the transpose.
+__device__ __forceinline__ void w_load_A(const WgradMma &P, int g, int v0, uint32_t stg, uint32_t tm_a, int q,
+                                         int half, int lane) {
+    const int nbI = 1;  // (channel boxes handled through bx below)
+    (void)nbI;
     const uint32_t pxb = (uint32_t)P.CBI * 32u;
-    for (int j = 0; j < T.nslots; ++j) {
-        const WSlot &S = T.slot[j];
-        int k = 0;
-        while (T.plane[k] != S.plane) ++k;
-        const int vs = v0 + S.shift;                 // first staged pixel this slot reads
-        const int w0 = v0 + T.minsh[k];              // first pixel of the staged window of plane k
-        const int off = w_off(P, w0) + (vs - w0);
-        const uint32_t base = stg + k * P.stgI_plane;
-        const int upp = 2 * S.cn;
-        const int total = KP * upp;
-#pragma unroll 4
-        for (int L = tid; L < total; L += kWRepack) {
-            const int vl = (int)S.fd_upp.div((uint32_t)L);
-            const int u = L - vl * upp;
-            const int cl = u >> 1, i = u & 1;
-            const int c = S.c0 + cl - T.c_lo;
-            const int bx = c / P.CBI, cc = c - bx * P.CBI;
-            const uint4 v = ld_shared_v4(base + (uint32_t)bx * P.capI * pxb + (uint32_t)(vl + off) * pxb +
-                                         (uint32_t)(cc * 32 + i * 16));
-            const int row = S.row0 + cl * 4;         // first m row of channel cl (d2 = 0)
-            const uint32_t dst = a + (uint32_t)(row >> 3) * P.a_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
-                                 (uint32_t)((row & 7) * 2);
-            st_shared_v2(dst, v.x, v.y);
-            st_shared_v2(dst + 16u, v.z, v.w);
+    const int row = q * 32 + lane;
+    const int d1 = lane & 3;
+    const int nk = P.KP / 4;
+    for (int tt = 0; tt < P.TG; ++tt) {
+        const int mt = g * P.TG + tt;
+        if (mt >= P.n_mtiles) break;
+        const WTile &T = P.tile[mt];
+        // which slot / channel this lane's row belongs to
+        int j = -1;
+        for (int s2 = 0; s2 < T.nslots; ++s2)
+            if (row >= T.slot[s2].row0 && row < T.slot[s2].row0 + 4 * T.slot[s2].cn) j = s2;
+        uint32_t src = 0;
+        bool ok = false;
+        if (j >= 0) {
+            const WSlot &S = T.slot[j];
+            const int c = S.c0 + ((row - S.row0) >> 2);
+            int k = 0;
+            while (P.g_plane[g][k] != S.plane) ++k;
+            const int w0 = v0 + P.g_minsh[g][k];
+            const int off = w_off(P, w0) + (v0 + S.shift - w0);
+            const int cl = c - P.g_clo[g];
+            const int bx = cl / P.CBI, cc = cl - bx * P.CBI;
+            ok = c < P.C;
+            src = stg + k * P.stgI_plane + (uint32_t)bx * P.capI * pxb + (uint32_t)off * pxb + (uint32_t)(cc * 32 + d1 * 8);
+        }
+        for (int kk = half; kk < nk; kk += 2) {
+            uint32_t r[8];
+#pragma unroll
+            for (int px = 0; px < 4; ++px) {
+                uint32_t lo = 0, hi = 0;
+                if (ok) {
+                    const uint32_t a = src + (uint32_t)(kk * 4 + px) * pxb;
+                    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(a));
+                }
+                transpose4x4(lo, hi, d1);
+                r[2 * px] = lo;
+                r[2 * px + 1] = hi;
+            }
+            tmem_st8(tm_a + ((uint32_t)(q * 32) << 16) + (uint32_t)((tt * nk + kk) * 8), r);
         }
     }
 }
@@ -199,34 +255,36 @@ __device__ __forceinline__ void w_repack(const WgradMma &P, const WTile &T, int 
 __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_constant__ WgradMma P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *stg_full = bars, *stg_empty = bars + 2;
-    uint64_t *op_full = bars + 4, *op_empty = op_full + kWMaxStages;
+    uint64_t *stg_full = bars, *stg_empty = bars + 4;
+    uint64_t *op_full = bars + 8, *op_empty = op_full + kWMaxStages;
     uint64_t *acc_full = op_empty + kWMaxStages, *acc_empty = acc_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + 512);
     const uint32_t stg0 = smem_u32(smem_raw) + 1024;
     const uint32_t op0 = stg0 + P.nstg * P.stg_bytes;
-    const uint32_t op_stride = P.a_bytes + P.b_bytes;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    constexpr int kEpi0 = kWRepack / 32, kMma = kEpi0 + kWEpi / 32, kTma = kMma + 1;
+    constexpr int kEpi0 = kWLoad / 32, kMma = kEpi0 + kWEpi / 32, kTma = kMma + 1;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(stg_full + i, 1);
-            mbar_init(stg_empty + i, kWRepack);
+            mbar_init(stg_empty + i, kWLoad);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(acc_full + i, 1);
             mbar_init(acc_empty + i, kWEpi / 32);
         }
         for (int s = 0; s < P.nstages; ++s) {
-            mbar_init(op_full + s, kWRepack);
+            mbar_init(op_full + s, kWLoad);
             mbar_init(op_empty + s, 1);
         }
         mbar_fence_init();
     }
-    if (warp == kMma) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
+    if (warp == kMma) tmem_alloc_dyn(tmem_slot, 512);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tmem_slot;
+    const int nk = P.KP / 4;
 
     if (warp == kTma) {
         if (lane == 0) {
@@ -235,40 +293,44 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             int sb = 0;
             uint32_t sph = 0;
             for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-                int mt, ks, p0, p1;
-                wdecode(P, item, mt, ks, p0, p1);
-                const WTile &T = P.tile[mt];
+                int g, ks, p0, p1;
+                wdecode(P, item, g, ks, p0, p1);
                 for (int v0 = p0; v0 < p1; v0 += P.KP) {
                     const int si = (v0 - p0) / P.KP;
                     WTRACE(0, si, 0);
                     mbar_wait(stg_empty + sb, sph ^ 1);
                     WTRACE(0, si, 1);
                     const uint32_t stg = stg0 + sb * P.stg_bytes;
-                    mbar_arrive_expect_tx(stg_full + sb, w_issue(P, T, v0, stg, 0, false));
-                    w_issue(P, T, v0, stg, smem_u32(stg_full + sb), true);
+                    mbar_arrive_expect_tx(stg_full + sb, w_issue(P, g, v0, stg, 0, false));
+                    w_issue(P, g, v0, stg, smem_u32(stg_full + sb), true);
                     WTRACE(0, si, 2);
                     if (++sb == P.nstg) { sb = 0; sph ^= 1; }
                 }
             }
         }
     } else if (warp < kEpi0) {
+        // ---------------------------------------------------------- loaders
         const int tid = threadIdx.x;
+        const int q = warp & 3, half = warp >> 2;
         int sb = 0, st = 0;
         uint32_t sph = 0, ph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-            int mt, ks, p0, p1;
-            wdecode(P, item, mt, ks, p0, p1);
-            const WTile &T = P.tile[mt];
+            int g, ks, p0, p1;
+            wdecode(P, item, g, ks, p0, p1);
             for (int v0 = p0; v0 < p1; v0 += P.KP) {
                 const int si = (v0 - p0) / P.KP;
                 if (tid == 0) WTRACE(1, si, 0);
                 mbar_wait(stg_full + sb, sph);
                 if (tid == 0) WTRACE(1, si, 1);
                 mbar_wait(op_empty + st, ph ^ 1);
+                fence_after_sync();
                 if (tid == 0) WTRACE(1, si, 2);
-                const uint32_t a = op0 + st * op_stride;
-                w_repack(P, T, v0, stg0 + sb * P.stg_bytes, a, a + P.a_bytes, tid);
+                const uint32_t stg = stg0 + sb * P.stg_bytes;
+                w_load_B(P, v0, stg, op0 + st * P.b_bytes, tid);
+                w_load_A(P, g, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, half, lane);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 fence_proxy_async_smem();
+                fence_before_sync();
                 if (tid == 0) WTRACE(1, si, 3);
                 mbar_arrive(op_full + st);
                 mbar_arrive(stg_empty + sb);
@@ -277,15 +339,15 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             }
         }
     } else if (warp == kMma) {
-        const uint32_t idesc = idesc_bf16(128, P.N_tile, 1, 1);
+        const uint32_t idesc = idesc_bf16(128, P.N_tile, 0, 1);
         int st = 0, abuf = 0;
         uint32_t ph = 0, aph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-            int mt, ks, p0, p1;
-            wdecode(P, item, mt, ks, p0, p1);
+            int g, ks, p0, p1;
+            wdecode(P, item, g, ks, p0, p1);
+            const int ntl = min(P.TG, P.n_mtiles - g * P.TG);
             mbar_wait(acc_empty + abuf, aph ^ 1);
             fence_after_sync();
-            const uint32_t d = tmem + (uint32_t)(abuf * P.N_tile);
             bool first = true;
             for (int v0 = p0; v0 < p1; v0 += P.KP) {
                 const int si = (v0 - p0) / P.KP;
@@ -293,13 +355,18 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 mbar_wait(op_full + st, ph);
                 if (lane == 0) WTRACE(2, si, 1);
                 fence_after_sync();
-                const uint32_t a = op0 + st * op_stride;
-                const uint64_t ad0 = smem_desc(a, 128, P.a_sbo);
-                const uint64_t bd0 = smem_desc(a + P.a_bytes, 128, P.b_sbo);
+                const uint64_t bd0 = smem_desc(op0 + st * P.b_bytes, 128, P.b_sbo);
+                const uint32_t a0 = tmem + P.acc_cols + (uint32_t)st * P.abuf_cols;
                 if (elect_one()) {
-                    for (int kk = 0; kk < P.KP / 4; ++kk) {   // 16 k-rows (4 pixels) per MMA
-                        mma_bf16_ss(d, ad0 + (uint64_t)(kk * 16), bd0 + (uint64_t)(kk * 16), idesc,
-                                    (first && kk == 0) ? 0u : 1u);
+                    for (int tt = 0; tt < ntl; ++tt) {
+                        const uint32_t d = tmem + (uint32_t)(tt * P.N_tile);
+                        for (int kk = 0; kk < nk; ++kk) {
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+                                "r"(a0 + (uint32_t)((tt * nk + kk) * 8)), "l"(bd0 + (uint64_t)(kk * 16)), "r"(idesc),
+                                "r"((first && kk == 0) ? 0u : 1u));
+                        }
                     }
                     mma_commit(op_empty + st);
                 }
@@ -309,49 +376,53 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             }
             if (elect_one()) mma_commit(acc_full + abuf);
             __syncwarp();
-            if (++abuf == 2) { abuf = 0; aph ^= 1; }
+            aph ^= 1;   // one accumulator set (abuf stays 0)
         }
     } else {
-        // epilogue: TMEM rows (slot, c, d2) x columns (c', d3) -> fp32 dK (or split partial)
+        // ---------------------------------------------------------- epilogue
         const int wq = warp & 3;
         const int row = wq * 32 + lane;
-        const size_t nk = (size_t)P.ntaps * P.C * P.Cout * 16;
+        const size_t nkel = (size_t)P.ntaps * P.C * P.Cout * 16;
         int abuf = 0;
         uint32_t aph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-            int mt, ks, p0, p1;
-            wdecode(P, item, mt, ks, p0, p1);
-            const WTile &T = P.tile[mt];
-            int tap = -1, c = 0, d2 = row & 3;
-            for (int j = 0; j < T.nslots; ++j) {
-                const WSlot &S = T.slot[j];
-                if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
-                    tap = S.tap;
-                    c = S.c0 + ((row - S.row0) >> 2);
-                }
-            }
+            int g, ks, p0, p1;
+            wdecode(P, item, g, ks, p0, p1);
+            const int ntl = min(P.TG, P.n_mtiles - g * P.TG);
             mbar_wait(acc_full + abuf, aph);
             fence_after_sync();
-            float *dst = P.part + (size_t)ks * nk + (((size_t)tap * P.C + c) * P.Cout) * 16 + d2 * 4;
-            const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(abuf * P.N_tile);
-            for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
-                float v[16];
-                tmem_ld16(tcol + n0, v);
-                tmem_wait_ld();
-                if (tap >= 0 && c < P.C) {
+            for (int tt = 0; tt < ntl; ++tt) {
+                const WTile &T = P.tile[g * P.TG + tt];
+                int tap = -1, c = 0;
+                const int d2 = row & 3;
+                for (int j = 0; j < T.nslots; ++j) {
+                    const WSlot &S = T.slot[j];
+                    if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
+                        tap = S.tap;
+                        c = S.c0 + ((row - S.row0) >> 2);
+                    }
+                }
+                float *dst = P.part + (size_t)ks * nkel + (((size_t)(tap < 0 ? 0 : tap) * P.C + c) * P.Cout) * 16 + d2 * 4;
+                const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(tt * P.N_tile);
+                for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
+                    float v[16];
+                    tmem_ld16(tcol + n0, v);
+                    tmem_wait_ld();
+                    if (tap >= 0 && c < P.C) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int co = n0 / 4 + j;
-                        if (co < P.Cout)
-                            *reinterpret_cast<float4 *>(dst + (size_t)co * 16) =
-                                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int co = n0 / 4 + jj;
+                            if (co < P.Cout)
+                                *reinterpret_cast<float4 *>(dst + (size_t)co * 16) =
+                                    make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+                        }
                     }
                 }
             }
             fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty + abuf);
-            if (++abuf == 2) { abuf = 0; aph ^= 1; }
+            aph ^= 1;
         }
     }
 
@@ -359,7 +430,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     __syncthreads();
     if (warp == kMma) {
         fence_after_sync();
-        tmem_dealloc_dyn(tmem, P.tmem_cols);
+        tmem_dealloc_dyn(tmem, 512);
     }
 }
 
@@ -469,52 +540,79 @@ WPlan make_wplan(const Problem &p) {
         for (int k = 0; k < T.np; ++k) T.span[k] -= T.minsh[k];
         P.tile[i] = T;
     }
-    int max_span = 0, max_np = 1, max_ci = 0;
-    for (auto &T : tiles) {
-        for (int k = 0; k < T.np; ++k) max_span = std::max(max_span, T.span[k]);
-        max_np = std::max(max_np, T.np);
-        max_ci = std::max(max_ci, T.c_hi - T.c_lo);
-    }
-    P.CBI = std::min(16, max_ci);
+    const int nsm = device_info().num_sms;
     P.CBO = std::min(16, P.Cout);
-    const int nbI = cdiv(max_ci, P.CBI), nbO = cdiv(P.Cout, P.CBO);
-    // ---- pixels per stage, staging / operand buffers
+    const int nbO = cdiv(P.Cout, P.CBO);
+    static const int force_tg = getenv("CAPSCONV_WG_TG") ? atoi(getenv("CAPSCONV_WG_TG")) : 0;
     bool found = false;
-    for (int KP : {32, 64, 16}) {
-        if (P.batch_mode && KP > 256) continue;
-        const int capI = P.batch_mode ? KP : ((KP + max_span - 1) / P.Wg + 2) * P.Wg;
-        const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wg;
-        const uint32_t stgI_plane = (uint32_t)nbI * capI * P.CBI * 32;
-        const uint32_t stgI = (uint32_t)max_np * stgI_plane;
-        const uint32_t stgO = (uint32_t)nbO * capO * P.CBO * 32;
-        const uint32_t stg = stgI + stgO;
-        const uint32_t sbo = (uint32_t)KP * 64 + 16;     // plane stride, bank staggered
-        const uint32_t abytes = 16 * sbo, bbytes = (uint32_t)(P.N_tile / 8) * sbo;
-        for (int nstg = 2; nstg >= 1 && !found; --nstg)
-            for (int ns = 3; ns >= 2; --ns) {
-                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * (abytes + bbytes);
-                if (tot <= kWSmemLimit) {
-                    P.KP = KP; P.capI = capI; P.capO = capO; P.stgI_plane = stgI_plane; P.stgI_bytes = stgI;
-                    P.stgO_bytes = stgO; P.stg_bytes = stg; P.a_sbo = sbo; P.b_sbo = sbo; P.a_bytes = abytes;
-                    P.b_bytes = bbytes; P.nstg = nstg; P.nstages = ns; P.smem_bytes = (uint32_t)tot;
-                    found = true;
-                    break;
+    // tiles per CTA group: as many as TMEM holds (shared staged window), then
+    // pixels per stage and pipeline depths that fit shared memory
+    for (int TG = std::min(P.n_mtiles, 8); TG >= 1 && !found; --TG) {
+        if (force_tg && TG != force_tg) continue;
+        const int ngroups = cdiv(P.n_mtiles, TG);
+        // group unions
+        int gmax_np = 1, gmax_span = 0, gmax_ci = 0;
+        for (int g = 0; g < ngroups; ++g) {
+            int np = 0, plane[4], mn[4], mx[4], clo = 1 << 30, chi = 0;
+            for (int mt = g * TG; mt < std::min(P.n_mtiles, (g + 1) * TG); ++mt) {
+                const WTile &T = P.tile[mt];
+                clo = std::min(clo, T.c_lo); chi = std::max(chi, T.c_hi);
+                for (int j = 0; j < T.nslots; ++j) {
+                    int k = 0;
+                    while (k < np && plane[k] != T.slot[j].plane) ++k;
+                    if (k == np) { if (np == 4) return pl; plane[k] = T.slot[j].plane; mn[k] = 1 << 30; mx[k] = -(1 << 30); ++np; }
+                    mn[k] = std::min(mn[k], T.slot[j].shift);
+                    mx[k] = std::max(mx[k], T.slot[j].shift);
                 }
             }
-        if (found) break;
+            P.g_np[g] = np;
+            for (int k = 0; k < np; ++k) {
+                P.g_plane[g][k] = plane[k]; P.g_minsh[g][k] = mn[k]; P.g_span[g][k] = mx[k] - mn[k];
+                gmax_span = std::max(gmax_span, mx[k] - mn[k]);
+            }
+            P.g_clo[g] = clo; P.g_chi[g] = chi;
+            gmax_np = std::max(gmax_np, np);
+            gmax_ci = std::max(gmax_ci, chi - clo);
+        }
+        P.CBI = std::min(16, gmax_ci);
+        const int nbI = cdiv(gmax_ci, P.CBI);
+        for (int KP : {64, 32, 16}) {
+            const uint32_t acc = (uint32_t)(TG * P.N_tile);
+            const uint32_t abuf = (uint32_t)(2 * TG * KP);      // TG tiles x KP/4 k-steps x 8 columns
+            int ns = 0;
+            for (int n = 3; n >= 2; --n)
+                if (acc + n * abuf <= 512) { ns = n; break; }
+            if (!ns) continue;
+            const int capI = P.batch_mode ? KP : ((KP + gmax_span - 1) / P.Wg + 2) * P.Wg;
+            const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wg;
+            const uint32_t stgI_plane = (uint32_t)nbI * capI * P.CBI * 32;
+            const uint32_t stgI = (uint32_t)gmax_np * stgI_plane;
+            const uint32_t stgO = (uint32_t)nbO * capO * P.CBO * 32;
+            const uint32_t stg = stgI + stgO;
+            const uint32_t sbo = (uint32_t)KP * 64 + 16;
+            const uint32_t bbytes = (uint32_t)(P.N_tile / 8) * sbo;
+            for (int nstg = 3; nstg >= 2 && !found; --nstg) {
+                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes;
+                if (tot > kWSmemLimit) continue;
+                P.TG = TG; P.n_groups = ngroups;
+                P.KP = KP; P.capI = capI; P.capO = capO; P.stgI_plane = stgI_plane; P.stgI_bytes = stgI;
+                P.stgO_bytes = stgO; P.stg_bytes = stg; P.b_sbo = sbo; P.b_bytes = bbytes;
+                P.nstg = nstg; P.nstages = ns; P.smem_bytes = (uint32_t)tot;
+                P.acc_cols = acc; P.abuf_cols = abuf;
+                found = true;
+            }
+            if (found) break;
+        }
     }
     if (!found) return pl;
     // ---- split of the pixel range so that items fill the machine
-    const int nsm = device_info().num_sms;
     const int nstage_total = cdiv(P.vtotal, P.KP);
-    int ks = std::max(1, std::min(nstage_total, cdiv(2 * nsm, P.n_mtiles)));
+    int ks = std::max(1, std::min(nstage_total, cdiv(2 * nsm, P.n_groups)));
     const int stages_per = cdiv(nstage_total, ks);
     P.kpix = stages_per * P.KP;
     P.ksplit = cdiv(P.vtotal, P.kpix);
-    P.n_items = P.n_mtiles * P.ksplit;
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(2 * P.N_tile)) cols <<= 1;
-    P.tmem_cols = cols;
+    P.n_items = P.n_groups * P.ksplit;
+    P.tmem_cols = 512;
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_uppO.init((uint32_t)(2 * P.Cout));
@@ -550,10 +648,10 @@ const WPlan &cached_wplan(const Problem &p) {
     if (getenv("CAPSCONV_DEBUG") && pl.ok) {
         const WgradMma &P = pl.P;
         fprintf(stderr,
-                "[capsconv] wgrad plan: C=%d Cout=%d Hg=%d Wg=%d taps=%d mtiles=%d N_tile=%d KP=%d ksplit=%d "
-                "items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u\n",
-                P.C, P.Cout, P.Hg, P.Wg, P.ntaps, P.n_mtiles, P.N_tile, P.KP, P.ksplit, P.n_items, P.capI, P.capO,
-                P.nstg, P.nstages, P.smem_bytes);
+                "[capsconv] wgrad plan: C=%d Cout=%d Hg=%d Wg=%d taps=%d mtiles=%d TG=%d groups=%d N_tile=%d KP=%d "
+                "ksplit=%d items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u acc=%u abuf=%u\n",
+                P.C, P.Cout, P.Hg, P.Wg, P.ntaps, P.n_mtiles, P.TG, P.n_groups, P.N_tile, P.KP, P.ksplit, P.n_items,
+                P.capI, P.capO, P.nstg, P.nstages, P.smem_bytes, P.acc_cols, P.abuf_cols);
     }
     return pl;
 }

@@ -16,18 +16,20 @@ __global__ void tbench(const __grid_constant__ CUtensorMap tm, const uint8_t *sr
     __syncthreads();
     if (threadIdx.x != 0) return;
     const uint32_t dst = smem_u32(smem);
-    unsigned long long t0 = clock64();
+    unsigned long long t0 = clock64(), tissue = 0;
     for (int it = 0; it < iters; ++it) {
+        unsigned long long ta = clock64();
         mbar_arrive_expect_tx(&bar, (uint32_t)(nbox * box_bytes));
         for (int b = 0; b < nbox; ++b) {
             const int row = (blockIdx.x * 37 + it * nbox + b + blockIdx.x * iters * nbox) % nrows_total;
             if (mode == 0) tma::load4d(dst + b * box_bytes, &tm, 0, 0, row % 24, row / 24, smem_u32(&bar));
             else bulk_g2s_u32(dst + b * box_bytes, src + (size_t)row * W * 256, box_bytes, &bar);
         }
+        tissue += clock64() - ta;
         mbar_wait(&bar, it & 1);
     }
     unsigned long long t1 = clock64();
-    if (blockIdx.x == 0) *out = t1 - t0;
+    if (blockIdx.x == 0) { out[0] = t1 - t0; out[1] = tissue; }
 }
 
 extern "C" double tma_bench(int mode, int nbox, int iters, int W, int rows_per_box, int B) {
@@ -39,7 +41,7 @@ extern "C" double tma_bench(int mode, int nbox, int iters, int W, int rows_per_b
     CUtensorMap tm;
     if (!make_capsule_tmap(&tm, src, B, H, W, CS, 8, W, rows_per_box, 1, 1)) return -2;
     unsigned long long *d;
-    cudaMalloc(&d, 8);
+    cudaMalloc(&d, 16);
     const int box_bytes = W * 256 * rows_per_box;
     cudaFuncSetAttribute(tbench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     tbench<<<148, 32, 200 * 1024>>>(tm, src, mode, nbox, iters, box_bytes, W, (int)(B * H - 8), d);
@@ -50,6 +52,10 @@ extern "C" double tma_bench(int mode, int nbox, int iters, int W, int rows_per_b
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long h[2];
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    printf("   [cta0: total %llu cyc, issue %llu cyc (%.0f%%), per round total %.0f issue %.0f]\n", h[0], h[1],
+           100.0 * h[1] / h[0], (double)h[0] / iters, (double)h[1] / iters);
     cudaFree(src); cudaFree(d);
     if (e != cudaSuccess) return -1;
     const double bytes = 148.0 * iters * nbox * box_bytes;

@@ -193,3 +193,79 @@ extern "C" double umma_bench(int N, int iters, int a_tmem, int nblocks, int nacc
     if (e != cudaSuccess) return -1.0;
     return (double)h / iters;
 }
+
+// ---------------------------------------------------------------------------
+// TS probe: A (128 x K bf16) written into TMEM with tcgen05.st (lane = row,
+// 32-bit column j = k pair (2j, 2j+1)), B (N x K) K-major in shared memory;
+// D = A * B^T with kind::f16 A-from-TMEM.
+__global__ void probe_ts(const __nv_bfloat16 *A, const __nv_bfloat16 *B, float *D, int N, int K) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    uint8_t *sB = smem;
+    const int Npad = (N + 7) / 8 * 8;
+    const uint32_t b_lbo = Npad * 16, b_sbo = 128;
+    for (int i = tid; i < N * K; i += blockDim.x) {
+        int n = i / K, k = i % K;
+        *(__nv_bfloat16 *)(sB + (k / 8) * b_lbo + n * 16 + (k % 8) * 2) = B[i];
+    }
+    if (warp == 0) tmem_alloc<512>(&tmem_base);
+    if (tid == 0) { mbar_init(&bar, 1); mbar_fence_init(); }
+    fence_proxy_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tm = tmem_base;
+    const uint32_t a_col = 256;   // A at columns [256, 256 + K/2)
+    // each warp writes its lane quarter: row = warp*32 + lane, 8 columns at a time
+    const int row = warp * 32 + lane;
+    for (int j0 = 0; j0 < K / 2; j0 += 8) {
+        uint32_t r[8];
+        for (int j = 0; j < 8; ++j) {
+            __nv_bfloat162 h;
+            h.x = A[row * K + 2 * (j0 + j)];
+            h.y = A[row * K + 2 * (j0 + j) + 1];
+            r[j] = *reinterpret_cast<uint32_t *>(&h);
+        }
+        const uint32_t taddr = tm + ((uint32_t)(warp * 32) << 16) + a_col + j0;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr),
+                     "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                     : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    if (warp == 0) {
+        const uint32_t idesc = idesc_bf16(128, N, 0, 0);
+        if (elect_one()) {
+            for (int ks = 0; ks < K / 16; ++ks) {
+                const uint64_t bd = smem_desc(smem_u32(sB) + ks * 2 * b_lbo, b_lbo, b_sbo);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tm),
+                    "r"(tm + a_col + ks * 8), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1 : 0));
+            }
+            mma_commit(&bar);
+        }
+        __syncwarp();
+    }
+    mbar_wait(&bar, 0);
+    fence_after_sync();
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        float v[8];
+        tmem_ld8(tm + ((uint32_t)(warp * 32) << 16) + c0, v);
+        tmem_wait_ld();
+        for (int j = 0; j < 8 && c0 + j < N; ++j) D[row * N + c0 + j] = v[j];
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+extern "C" int umma_probe_ts(const void *A, const void *B, float *D, int N, int K) {
+    cudaFuncSetAttribute(probe_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    probe_ts<<<1, 128, 65536>>>((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, D, N, K);
+    return (int)cudaDeviceSynchronize();
+}

@@ -73,3 +73,19 @@ def test_umma_layouts(probe, case):
         Aeff = A[shift:shift + 128, :]
     ref = Aeff.double() @ B.double().T
     torch.testing.assert_close(D.cpu().double(), ref, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("N,K", [(32, 16), (32, 64), (48, 32), (128, 32)])
+def test_umma_ts_tmem_a(probe, N, K):
+    """A operand in TMEM written by tcgen05.st (lane = row, 32-bit column j =
+    elements 2j, 2j+1), B in shared memory; kind::f16 TS MMA."""
+    probe.umma_probe_ts.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 2
+    probe.umma_probe_ts.restype = ctypes.c_int
+    g = torch.Generator().manual_seed(3)
+    A = (torch.randint(-4, 5, (128, K), generator=g).float() / 4).to(torch.bfloat16)
+    B = (torch.randint(-4, 5, (N, K), generator=g).float() / 4).to(torch.bfloat16)
+    Ad, Bd = A.cuda(), B.cuda()
+    D = torch.zeros(128, N, dtype=torch.float32, device="cuda")
+    assert probe.umma_probe_ts(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), N, K) == 0
+    ref = A.double() @ B.double().T
+    torch.testing.assert_close(D.cpu().double(), ref, rtol=0, atol=0)
