@@ -27,8 +27,8 @@
 // MN-major shared-memory operand.  A CTA accumulates a group of M tiles over
 // a pixel range, so the staged window is shared by all the taps it holds.
 //
-// Roles (416 threads): warps 0-7 loaders (two per TMEM lane quarter), warps
-// 8-11 epilogue, warp 12 MMA, warp 13 TMA.
+// Roles (576 threads): warps 0-11 loaders (three per TMEM lane quarter),
+// warps 12-15 epilogue, warp 16 MMA, warp 17 TMA.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -47,7 +47,7 @@ using namespace umma;
 
 namespace {
 
-constexpr int kWLoad = 256, kWEpi = 128;
+constexpr int kWLoad = 384, kWEpi = 128;   // three loader warps per TMEM lane quarter
 constexpr int kWThreads = kWLoad + kWEpi + 64;
 constexpr int kWMaxTiles = 96;
 constexpr int kWMaxSlots = 4;
@@ -95,6 +95,11 @@ struct WgradMma {
     int nstg, nstages;
     uint32_t smem_bytes, tmem_cols;
     unsigned long long *trace;             // debug: globaltimer stamps of CTA 0 [role][stage][4]
+    int dbg;                               // bench-only: 1 skip transpose, 2 skip TMEM stores, 4 skip B, 8 skip LDS
+    // contiguous staging (1-D bulk copies): dO always; I when stride 1 (not FC)
+    const uint8_t *I_ptr, *O_ptr;
+    int I_contig;
+    int Ho, Wo;                            // dO extents (rows per image, pixels per row)
 };
 #define WTRACE(role, idx, ev)                                                              \
     do {                                                                                   \
@@ -112,21 +117,26 @@ __device__ __forceinline__ void wdecode(const WgradMma &P, int item, int &mt, in
 // staging pixel offset of v0.  Batch mode: boxes of KP images at v0.
 __device__ __forceinline__ uint32_t w_stage_window(const WgradMma &P, const CUtensorMap *tm, int v0, int len,
                                                    int cb, int nbox, int c_first, int ox, int oy, int cs, int cap,
-                                                   uint32_t dst, uint32_t mbar, bool issue) {
+                                                   uint32_t dst, uint32_t mbar, bool issue, int &box_id, int lane) {
+    // issue: every box gets an index; lane `lane` issues the boxes with index % 32 == lane
     const uint32_t px = (uint32_t)cb * 32u;
     uint32_t bytes = 0;
     for (int bx = 0; bx < nbox; ++bx) {
         const uint32_t base = dst + (uint32_t)bx * cap * px;
         const int c0 = (c_first + bx * cb) * 16;
         if (P.batch_mode) {
-            if (issue) tma::load4d(base, tm, c0, 0, 0, v0, mbar);
+            if (issue && (box_id & 31) == lane) tma::load4d(base, tm, c0, 0, 0, v0, mbar);
+            ++box_id;
             bytes += (uint32_t)P.KP * px;
         } else {
             const int Ra = floor_div(v0, P.Wg), Rb = floor_div(v0 + len - 1, P.Wg);
             for (int R = Ra; R <= Rb; ++R) {
-                const int b = floor_div(R, P.Hg);
-                const int Y = R - b * P.Hg;
-                if (issue) tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px, tm, c0, ox, cs * Y + oy, b, mbar);
+                if (issue && (box_id & 31) == lane) {
+                    const int b = floor_div(R, P.Hg);
+                    const int Y = R - b * P.Hg;
+                    tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px, tm, c0, ox, cs * Y + oy, b, mbar);
+                }
+                ++box_id;
                 bytes += (uint32_t)P.Wg * px;
             }
         }
@@ -138,18 +148,73 @@ __device__ __forceinline__ int w_off(const WgradMma &P, int v0) {
     return P.batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
 }
 
-__device__ __forceinline__ uint32_t w_issue(const WgradMma &P, int g, int v0, uint32_t stg, uint32_t mbar,
-                                            bool issue) {
-    uint32_t bytes = 0;
-    const int ci = P.g_chi[g] - P.g_clo[g];
-    const int nbI = (ci + P.CBI - 1) / P.CBI;
-    for (int k = 0; k < P.g_np[g]; ++k) {
-        const int pl = P.g_plane[g][k];
-        bytes += w_stage_window(P, &P.tm_I, v0 + P.g_minsh[g][k], P.KP + P.g_span[g][k], P.CBI, nbI, P.g_clo[g],
-                                P.pl_ox[pl], P.pl_oy[pl], P.s, P.capI, stg + k * P.stgI_plane, mbar, issue);
+// dO rows [ra, rb) (global row index b*Ho + Y) covering virtual pixels [v0, v0 + KP)
+__device__ __forceinline__ void w_dO_rows(const WgradMma &P, int v0, int &ra, int &rb) {
+    const int Ra = v0 / P.Wg;                       // virtual rows (v0 >= 0 for the forward grid)
+    const int Rb = (min(v0 + P.KP, P.vtotal) - 1) / P.Wg;
+    const int ba = Ra / P.Hg, ya = Ra - ba * P.Hg;
+    const int bb = Rb / P.Hg, yb = Rb - bb * P.Hg;
+    ra = ya < P.Ho ? ba * P.Ho + ya : (ba + 1) * P.Ho;
+    rb = yb < P.Ho ? bb * P.Ho + yb + 1 : (bb + 1) * P.Ho;
+}
+
+__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint32_t bytes, uint64_t *, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
+struct WGroup {
+    int np, nbI, clo;
+    int minsh[4], span[4], ox[4], oy[4];
+};
+
+__device__ __forceinline__ void w_group_setup(const WgradMma &P, int g, WGroup &G) {
+    G.np = P.g_np[g];
+    G.clo = P.g_clo[g];
+    G.nbI = (P.g_chi[g] - G.clo + P.CBI - 1) / P.CBI;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int pl = k < G.np ? P.g_plane[g][k] : 0;
+        G.minsh[k] = k < G.np ? P.g_minsh[g][k] : 0;
+        G.span[k] = k < G.np ? P.g_span[g][k] : 0;
+        G.ox[k] = P.pl_ox[pl];
+        G.oy[k] = P.pl_oy[pl];
     }
-    const int nbO = (P.Cout + P.CBO - 1) / P.CBO;
-    bytes += w_stage_window(P, &P.tm_O, v0, P.KP, P.CBO, nbO, 0, 0, 0, 1, P.capO, stg + P.stgI_bytes, mbar, issue);
+}
+
+__device__ __forceinline__ uint32_t w_issue(const WgradMma &P, const WGroup &G, int v0, uint32_t stg, uint32_t mbar,
+                                            bool issue, int lane) {
+    uint32_t bytes = 0;
+    int box_id = 0;
+    if (P.I_contig) {
+        // stride 1: the window of input pixels is contiguous in memory (one plane, all channels)
+        const int lo = v0 + G.minsh[0];
+        const int hi = min(v0 + P.KP + G.span[0] + G.minsh[0], P.vtotal);
+        if (hi > lo) {
+            const uint32_t nb = (uint32_t)(hi - lo) * P.C * 32u;
+            if (issue && lane == 0) bulk_g2s_u32(stg, P.I_ptr + (size_t)lo * P.C * 32, nb, (uint64_t *)0, mbar);
+            bytes += nb;
+        }
+        ++box_id;
+    } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k >= G.np) break;
+        bytes += w_stage_window(P, &P.tm_I, v0 + G.minsh[k], P.KP + G.span[k], P.CBI, G.nbI, G.clo, G.ox[k],
+                                G.oy[k], P.s, P.capI, stg + k * P.stgI_plane, mbar, issue, box_id, lane);
+    }
+    }
+    // dO: the valid rows of the window are consecutive rows of the dO tensor
+    int ra, rb;
+    w_dO_rows(P, v0, ra, rb);
+    if (rb > ra) {
+        const uint32_t nb = (uint32_t)(rb - ra) * P.Wo * P.Cout * 32u;
+        if (issue && lane == (box_id & 31))
+            bulk_g2s_u32(stg + P.stgI_bytes, P.O_ptr + (size_t)ra * P.Wo * P.Cout * 32, nb, (uint64_t *)0 + 0, mbar);
+        bytes += nb;
+    }
+    ++box_id;
     return bytes;
 }
 
@@ -157,19 +222,31 @@ __device__ __forceinline__ uint32_t w_issue(const WgradMma &P, int g, int v0, ui
 // 8 (c' pair), k-rows (v, d1) at 16 bytes; a capsule unit (c', d1 rows 2i,
 // 2i+1) becomes two 8-byte pieces (the D1 transpose).
 __device__ __forceinline__ void w_load_B(const WgradMma &P, int v0, uint32_t stg, uint32_t b, int tid) {
-    const int offO = w_off(P, v0);
+    // staged dO = whole dO rows [ra, rb); virtual pixel (b, Y, X) is valid for
+    // Y < Ho, X < Wo and then sits at staged pixel (b*Ho + Y - ra)*Wo + X.
+    int ra, rb;
+    w_dO_rows(P, v0, ra, rb);
     const uint32_t base = stg + P.stgI_bytes;
     const int upp = 2 * P.Cout;
     const int total = P.KP * upp;
-    const uint32_t pxb = (uint32_t)P.CBO * 32u;
+    const uint32_t pxb = (uint32_t)P.Cout * 32u;
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
 #pragma unroll 4
     for (int L = tid; L < total; L += kWLoad) {
         const int vl = (int)P.fd_uppO.div((uint32_t)L);
         const int u = L - vl * upp;
         const int c = u >> 1, i = u & 1;
-        const int bx = c / P.CBO, cc = c - bx * P.CBO;
-        const uint4 v = ld_shared_v4(base + (uint32_t)bx * P.capO * pxb + (uint32_t)(vl + offO) * pxb +
-                                     (uint32_t)(cc * 32 + i * 16));
+        const int vv = v0 + vl;
+        const uint32_t bq = P.fd_HgWg.div((uint32_t)vv);
+        const uint32_t rr = (uint32_t)vv - bq * HgWg;
+        const uint32_t Y = P.fd_Wg.div(rr);
+        const uint32_t X = rr - Y * (uint32_t)P.Wg;
+        uint4 v4 = make_uint4(0, 0, 0, 0);
+        if (vv < P.vtotal && (int)Y < P.Ho && (int)X < P.Wo) {
+            const int sp = ((int)bq * P.Ho + (int)Y - ra) * P.Wo + (int)X;
+            v4 = ld_shared_v4(base + (uint32_t)sp * pxb + (uint32_t)(c * 32 + i * 16));
+        }
+        const uint4 v = v4;
         const uint32_t dst = b + (uint32_t)(c >> 1) * P.b_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u + (c & 1) * 8u;
         st_shared_v2(dst, v.x, v.y);
         st_shared_v2(dst + 16u, v.z, v.w);
@@ -194,6 +271,32 @@ __device__ __forceinline__ void transpose4x4(uint32_t &lo, uint32_t &hi, int r) 
     }
 }
 
+// Transpose every staged input capsule in place (rows d1 -> columns d2), once
+// per stage, so the per-slot loads below are plain 8-byte reads of a column.
+// Lane groups of 4 own one 32-byte capsule.
+__device__ __forceinline__ void w_transpose_stage(uint32_t base, uint32_t bytes, int tid) {
+    const int lane = tid & 31;
+    const uint32_t n8 = bytes / 8;                      // 8-byte rows
+    const uint32_t step = (uint32_t)kWLoad;
+    // all lanes of a warp iterate together (shuffles need the full warp)
+    for (uint32_t r0 = (uint32_t)(tid - lane); r0 < n8; r0 += step) {
+        const uint32_t r = r0 + (uint32_t)lane;
+        uint32_t lo = 0, hi = 0;
+        const uint32_t a = base + r * 8u;
+        if (r < n8) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(a));
+        transpose4x4(lo, hi, lane & 3);
+        if (r < n8) st_shared_v2(a, lo, hi);
+    }
+}
+
+__device__ __forceinline__ void st_shared_v4z(uint32_t addr) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};\n" ::"r"(addr), "r"(0) : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
@@ -201,53 +304,87 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
 }
 
 // I -> A in TMEM for every tile of the group: this warp owns lane quarter q
-// (rows q*32 .. q*32+31 of each tile) and the k-steps kk = half (mod 2).
-// Lane group g = lane/4 is one (slot, channel); lane & 3 is the capsule row d1
-// when loading and the column d2 after the transpose.
-__device__ __forceinline__ void w_load_A(const WgradMma &P, int g, int v0, uint32_t stg, uint32_t tm_a, int q,
-                                         int half, int lane) {
-    const int nbI = 1;  // (channel boxes handled through bx below)
-    (void)nbI;
+// (rows q*32 .. q*32+31 of each tile) and k-steps kk = part (mod kParts).
+// Lane group lane/4 is one (slot, channel), lane & 3 the capsule column d2:
+// the staged capsules were transposed in place, so the 8 bytes at offset
+// d2*8 are (d1 = 0..3) of column d2 -- two TMEM columns of the A operand.  The per-tile
+// addressing is computed once per work item (WLane) -- the tile tables are
+// large kernel parameters and must not be re-read per stage.
+constexpr int kWMaxTG = 8;
+struct WLane {
+    uint32_t base[kWMaxTG];   // staging byte offset of this lane's capsule row at window pixel 0 (minus plane start)
+    int kpl[kWMaxTG];         // staged plane index (-1: padding row)
+    int sp0[kWMaxTG];         // staged pixel (within its plane window) read for stage pixel 0
+    int ntl, np;
+    int minsh[4];
+};
+
+__device__ __forceinline__ void w_lane_setup(const WgradMma &P, int g, int q, int lane, WLane &L) {
     const uint32_t pxb = (uint32_t)P.CBI * 32u;
     const int row = q * 32 + lane;
     const int d1 = lane & 3;
-    const int nk = P.KP / 4;
-    for (int tt = 0; tt < P.TG; ++tt) {
-        const int mt = g * P.TG + tt;
-        if (mt >= P.n_mtiles) break;
-        const WTile &T = P.tile[mt];
-        // which slot / channel this lane's row belongs to
-        int j = -1;
-        for (int s2 = 0; s2 < T.nslots; ++s2)
-            if (row >= T.slot[s2].row0 && row < T.slot[s2].row0 + 4 * T.slot[s2].cn) j = s2;
-        uint32_t src = 0;
-        bool ok = false;
-        if (j >= 0) {
-            const WSlot &S = T.slot[j];
-            const int c = S.c0 + ((row - S.row0) >> 2);
-            int k = 0;
-            while (P.g_plane[g][k] != S.plane) ++k;
-            const int w0 = v0 + P.g_minsh[g][k];
-            const int off = w_off(P, w0) + (v0 + S.shift - w0);
-            const int cl = c - P.g_clo[g];
-            const int bx = cl / P.CBI, cc = cl - bx * P.CBI;
-            ok = c < P.C;
-            src = stg + k * P.stgI_plane + (uint32_t)bx * P.capI * pxb + (uint32_t)off * pxb + (uint32_t)(cc * 32 + d1 * 8);
-        }
-        for (int kk = half; kk < nk; kk += 2) {
-            uint32_t r[8];
+    L.ntl = min(P.TG, P.n_mtiles - g * P.TG);
+    L.np = P.g_np[g];
 #pragma unroll
-            for (int px = 0; px < 4; ++px) {
-                uint32_t lo = 0, hi = 0;
-                if (ok) {
-                    const uint32_t a = src + (uint32_t)(kk * 4 + px) * pxb;
-                    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(a));
-                }
-                transpose4x4(lo, hi, d1);
-                r[2 * px] = lo;
-                r[2 * px + 1] = hi;
+    for (int k = 0; k < 4; ++k) L.minsh[k] = k < L.np ? P.g_minsh[g][k] : 0;
+#pragma unroll
+    for (int tt = 0; tt < kWMaxTG; ++tt) {
+        L.kpl[tt] = -1;
+        L.base[tt] = 0;
+        L.sp0[tt] = 0;
+        if (tt >= L.ntl) continue;
+        const WTile &T = P.tile[g * P.TG + tt];
+        for (int j = 0; j < T.nslots; ++j) {
+            const WSlot &S = T.slot[j];
+            if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
+                const int c = S.c0 + ((row - S.row0) >> 2);
+                if (c >= P.C) break;
+                int k = 0;
+                while (P.g_plane[g][k] != S.plane) ++k;
+                const int cl = c - P.g_clo[g];
+                const int bx = cl / P.CBI, cc = cl - bx * P.CBI;
+                L.kpl[tt] = k;
+                L.sp0[tt] = S.shift - P.g_minsh[g][k];
+                L.base[tt] = k * P.stgI_plane + (uint32_t)bx * P.capI * pxb +
+                             (uint32_t)(S.shift - P.g_minsh[g][k]) * pxb + (uint32_t)(cc * 32 + d1 * 8);
             }
-            tmem_st8(tm_a + ((uint32_t)(q * 32) << 16) + (uint32_t)((tt * nk + kk) * 8), r);
+        }
+    }
+}
+
+__device__ __forceinline__ void w_load_A(const WgradMma &P, const WLane &L, int v0, uint32_t stg, uint32_t tm_a,
+                                         int q, int part) {
+    // Unconditional loads: padding rows read harmless staged data (their D
+    // rows are never stored) and the staging tail past the tensor end is zero.
+    constexpr int kParts = kWLoad / 128;
+    const uint32_t pxb = (uint32_t)P.CBI * 32u;
+    const int nk = P.KP / 4;
+    int wo[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int w0 = v0 + L.minsh[k];
+        wo[k] = (P.batch_mode || P.I_contig) ? 0 : w0 - floor_div(w0, P.Wg) * P.Wg;
+    }
+    const uint32_t lane_q = (uint32_t)(q * 32) << 16;
+#pragma unroll
+    for (int tt = 0; tt < kWMaxTG; ++tt) {
+        if (tt >= L.ntl) break;
+        const int k = L.kpl[tt] < 0 ? 0 : L.kpl[tt];
+        int wok = wo[0];
+#pragma unroll
+        for (int kx = 1; kx < 4; ++kx)
+            if (k == kx) wok = wo[kx];
+        const uint32_t src = stg + L.base[tt] + (uint32_t)wok * pxb;
+        const uint32_t dcol = tm_a + lane_q + (uint32_t)(tt * nk * 8);
+        for (int kk = part; kk < nk; kk += kParts) {
+            uint32_t r[8];
+            const uint32_t a = src + (uint32_t)(kk * 4) * pxb;
+#pragma unroll
+            for (int px = 0; px < 4; ++px)
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n"
+                             : "=r"(r[2 * px]), "=r"(r[2 * px + 1])
+                             : "r"(a + (uint32_t)px * pxb));
+            tmem_st8(dcol + (uint32_t)(kk * 8), r);
         }
     }
 }
@@ -290,44 +427,58 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
         if (lane == 0) {
             tma::prefetch_desc(&P.tm_I);
             tma::prefetch_desc(&P.tm_O);
-            int sb = 0;
-            uint32_t sph = 0;
-            for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-                int g, ks, p0, p1;
-                wdecode(P, item, g, ks, p0, p1);
-                for (int v0 = p0; v0 < p1; v0 += P.KP) {
-                    const int si = (v0 - p0) / P.KP;
-                    WTRACE(0, si, 0);
-                    mbar_wait(stg_empty + sb, sph ^ 1);
-                    WTRACE(0, si, 1);
-                    const uint32_t stg = stg0 + sb * P.stg_bytes;
-                    mbar_arrive_expect_tx(stg_full + sb, w_issue(P, g, v0, stg, 0, false));
-                    w_issue(P, g, v0, stg, smem_u32(stg_full + sb), true);
-                    WTRACE(0, si, 2);
-                    if (++sb == P.nstg) { sb = 0; sph ^= 1; }
+        }
+        int sb = 0;
+        uint32_t sph = 0;
+        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+            int g, ks, p0, p1;
+            wdecode(P, item, g, ks, p0, p1);
+            WGroup G;
+            w_group_setup(P, g, G);
+            for (int v0 = p0; v0 < p1; v0 += P.KP) {
+                const int si = (v0 - p0) / P.KP;
+                if (lane == 0) WTRACE(0, si, 0);
+                mbar_wait(stg_empty + sb, sph ^ 1);
+                if (lane == 0) WTRACE(0, si, 1);
+                const uint32_t stg = stg0 + sb * P.stg_bytes;
+                if (P.I_contig) {
+                    const int lo = v0 + G.minsh[0];
+                    const int valid = max(0, min(P.vtotal, lo + P.KP + G.span[0]) - lo);
+                    const uint32_t zb = (uint32_t)valid * P.C * 32u, ze = (uint32_t)P.capI * P.C * 32u;
+                    for (uint32_t z = zb + (uint32_t)lane * 16u; z < ze; z += 512u) st_shared_v4z(stg + z);
+                    __syncwarp();
                 }
+                if (lane == 0) mbar_arrive_expect_tx(stg_full + sb, w_issue(P, G, v0, stg, 0, false, 0));
+                __syncwarp();
+                w_issue(P, G, v0, stg, smem_u32(stg_full + sb), true, lane);
+                if (lane == 0) WTRACE(0, si, 2);
+                if (++sb == P.nstg) { sb = 0; sph ^= 1; }
             }
         }
     } else if (warp < kEpi0) {
         // ---------------------------------------------------------- loaders
         const int tid = threadIdx.x;
-        const int q = warp & 3, half = warp >> 2;
+        const int q = warp & 3, part = warp >> 2;
         int sb = 0, st = 0;
         uint32_t sph = 0, ph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             int g, ks, p0, p1;
             wdecode(P, item, g, ks, p0, p1);
+            WLane L;
+            w_lane_setup(P, g, q, lane, L);
             for (int v0 = p0; v0 < p1; v0 += P.KP) {
                 const int si = (v0 - p0) / P.KP;
                 if (tid == 0) WTRACE(1, si, 0);
                 mbar_wait(stg_full + sb, sph);
                 if (tid == 0) WTRACE(1, si, 1);
+                w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, tid);
+                named_bar_sync(1, kWLoad);
                 mbar_wait(op_empty + st, ph ^ 1);
                 fence_after_sync();
                 if (tid == 0) WTRACE(1, si, 2);
                 const uint32_t stg = stg0 + sb * P.stg_bytes;
                 w_load_B(P, v0, stg, op0 + st * P.b_bytes, tid);
-                w_load_A(P, g, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, half, lane);
+                w_load_A(P, L, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 fence_proxy_async_smem();
                 fence_before_sync();
@@ -492,6 +643,8 @@ WPlan make_wplan(const Problem &p) {
         pl.I_B = p.B; pl.I_H = p.H; pl.I_W = p.W; pl.I_C = p.C;
         pl.O_B = p.B; pl.O_H = p.Ho; pl.O_W = p.Wo; pl.O_C = p.Cout;
     }
+    P.I_contig = (!fc && s == 1 && P.C <= 16) ? 1 : 0;
+    P.Ho = (int)pl.O_H; P.Wo = (int)pl.O_W;
     const long long vt = (long long)P.Bn * P.Hg * P.Wg;
     if (vt * 4 >= (1ll << 31)) return pl;
     P.vtotal = (int)vt;
@@ -547,7 +700,7 @@ WPlan make_wplan(const Problem &p) {
     bool found = false;
     // tiles per CTA group: as many as TMEM holds (shared staged window), then
     // pixels per stage and pipeline depths that fit shared memory
-    for (int TG = std::min(P.n_mtiles, 8); TG >= 1 && !found; --TG) {
+    for (int TG = std::min(P.n_mtiles, kWMaxTG); TG >= 1 && !found; --TG) {
         if (force_tg && TG != force_tg) continue;
         const int ngroups = cdiv(P.n_mtiles, TG);
         // group unions
@@ -576,18 +729,23 @@ WPlan make_wplan(const Problem &p) {
         }
         P.CBI = std::min(16, gmax_ci);
         const int nbI = cdiv(gmax_ci, P.CBI);
-        for (int KP : {64, 32, 16}) {
+        static const int force_kp = getenv("CAPSCONV_WG_KP") ? atoi(getenv("CAPSCONV_WG_KP")) : 0;
+        for (int KP : {128, 96, 64, 32, 16}) {
+            if (force_kp ? KP != force_kp : KP > 64) continue;
             const uint32_t acc = (uint32_t)(TG * P.N_tile);
             const uint32_t abuf = (uint32_t)(2 * TG * KP);      // TG tiles x KP/4 k-steps x 8 columns
             int ns = 0;
             for (int n = 3; n >= 2; --n)
                 if (acc + n * abuf <= 512) { ns = n; break; }
             if (!ns) continue;
-            const int capI = P.batch_mode ? KP : ((KP + gmax_span - 1) / P.Wg + 2) * P.Wg;
-            const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wg;
+            const int capI = P.batch_mode ? KP
+                             : P.I_contig ? KP + gmax_span
+                                          : ((KP + gmax_span - 1) / P.Wg + 2) * P.Wg;
+            // dO: whole dO rows touched by the window
+            const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wo;
             const uint32_t stgI_plane = (uint32_t)nbI * capI * P.CBI * 32;
             const uint32_t stgI = (uint32_t)gmax_np * stgI_plane;
-            const uint32_t stgO = (uint32_t)nbO * capO * P.CBO * 32;
+            const uint32_t stgO = (uint32_t)capO * P.Cout * 32;
             const uint32_t stg = stgI + stgO;
             const uint32_t sbo = (uint32_t)KP * 64 + 16;
             const uint32_t bbytes = (uint32_t)(P.N_tile / 8) * sbo;
@@ -677,6 +835,9 @@ cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK
     if (!make_capsule_tmap(&P.tm_O, dO, pl.O_B, pl.O_H, pl.O_W, pl.O_C, P.CBO, boxw, 1, boxb, 1))
         return cudaErrorInvalidValue;
     P.part = P.ksplit > 1 ? static_cast<float *>(ws) : dK;
+    P.I_ptr = static_cast<const uint8_t *>(I);
+    P.O_ptr = static_cast<const uint8_t *>(dO);
+    P.dbg = getenv("CAPSCONV_WG_DBG") ? atoi(getenv("CAPSCONV_WG_DBG")) : 0;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmemLimit);

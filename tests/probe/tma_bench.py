@@ -7,9 +7,7 @@ subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-s
                 os.path.join(csrc, "tma.cpp"), "-lcuda"], check=True)
 L = ctypes.CDLL(lib)
 L.tma_bench.restype = ctypes.c_double
-L.tma_bench.argtypes = [ctypes.c_int] * 6
-for B in (2000, 8000):
-    for W, rows, nbox in [(24, 1, 7), (24, 1, 28)]:
-        for mode in (0, 1):
-            print("B=%d mode=%s W=%d rows/box=%d nbox=%d box=%d B: %.0f GB/s" % (B, ["tensor", "bulk"][mode], W, rows, nbox,
-                  W * 256 * rows, L.tma_bench(mode, nbox, 100, W, rows, B)), flush=True)
+L.tma_bench.argtypes = [ctypes.c_int] * 8
+for mode in (0, 2):
+    for nbox in (8, 16):
+        print("mode=%s nbox=%d: %.0f GB/s" % (["one map", "bulk", "two maps"][mode], nbox, L.tma_bench(mode, nbox, 100, 24, 1, 2000, 24, 32)), flush=True)
