@@ -68,7 +68,10 @@ class CapsStack:
         h, w = self.hw[-1]
         self.out = torch.empty((batch, h, w, last.Cout, D, D), dtype=self.dtype, device=self.device)
         self.grads = [torch.empty_like(a) for a in self.acts]           # dI of every layer
-        self.dK = [torch.empty(k.shape, dtype=torch.float32, device=self.device) for k in self.K]
+        # dK is fp32 for fp32/bf16 operands (libcapsconv's contract); wider
+        # operand types (test backends) keep their own precision
+        kdt = torch.float64 if self.dtype == torch.float64 else torch.float32
+        self.dK = [torch.empty(k.shape, dtype=kdt, device=self.device) for k in self.K]
         self.comm_stream = torch.cuda.Stream(self.device) if self.overlap else None
         self.events = [torch.cuda.Event() for _ in self.K] if self.overlap else None
 

@@ -186,3 +186,53 @@ def test_launch_counter_moves(cc):
     cc.fwd(capsinputs.make_input(L).to(DEV), capsinputs.make_kernel(L).to(DEV), 1)
     torch.cuda.synchronize()
     assert cc.launch_count() > n0
+
+
+def _stack_layers():
+    import oracle
+    return capsinputs.stack_layers(capsinputs.STACK_BATCH, oracle.output_dims)
+
+
+@pytest.mark.parametrize("li", [0, 1, 2, 3], ids=["L1", "L2", "L3", "FC"])
+def test_stack_layers_full_batch_exact(cc, oracle_mod, li):
+    """Each layer of the config-5 stack at global batch 1024 (the sizes bench.py
+    times), exact-integer inputs in {-1, 0, 1}: bitwise equal to the oracle."""
+    L = _stack_layers()[li]
+    dtype = torch.bfloat16
+    I = capsinputs.make_input(L, "int1", dtype, layer_idx=li)
+    K = capsinputs.make_kernel(L, "int1", dtype, layer_idx=li)
+    Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "int1", dtype, layer_idx=li)
+    O, dI, dK = run_all(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), L.stride)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
+    assert np.abs(rdK).max() < 2 ** 24
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
+
+
+def test_stack_step_small_batch(cc, oracle_mod):
+    """The product stack (CapsStack over libcapsconv) against the oracle stack
+    with bf16 rounding at the layer boundaries (reading R13), batch 6."""
+    from paper_2104_02621_b200.stack import CapsStack, LayerSpec
+    specs = [LayerSpec(*l) for l in capsinputs.STACK_LAYERS]
+    si = capsinputs.STACK_INPUT
+    B = 6
+    layers = capsinputs.stack_layers(B, oracle_mod.output_dims)
+    Ks = [capsinputs.make_kernel(L, dtype=torch.bfloat16, layer_idx=i) for i, L in enumerate(layers)]
+    X = capsinputs.make_input(layers[0], dtype=torch.bfloat16)
+    h, w = si["H"], si["W"]
+    for s in specs:
+        h, w = oracle_mod.output_dims(h, w, s.KH, s.KW, s.stride)
+    dY = capsinputs.make_grad_output((B, h, w, specs[-1].Cout, 4, 4), dtype=torch.bfloat16, layer_idx=len(specs))
+    st = CapsStack(specs, si["H"], si["W"], 4, B, Ks, DEV)
+    dKs = st.step(X.to(DEV), dY.to(DEV))
+    torch.cuda.synchronize()
+    acts, dX, rdKs, den = oracle_mod.stack_fwd_bwd(to_np(X), [to_np(k) for k in Ks], [s.stride for s in specs],
+                                                   to_np(dY), True)
+    assert_close(to_np(st.out), acts[-1], den["fwd"][-1], torch.bfloat16, "stack output")
+    assert_close(to_np(st.grads[0]), dX, den["dI"][0], torch.bfloat16, "stack dX")
+    for li in range(len(specs)):
+        assert_close(to_np(dKs[li]), rdKs[li], den["dK"][li], torch.bfloat16, "stack dK L%d" % (li + 1))
