@@ -99,6 +99,12 @@ struct WgradMma {
     // contiguous staging (1-D bulk copies): dO always; I when stride 1 (not FC)
     const uint8_t *I_ptr, *O_ptr;
     int I_contig;
+    // stride-2 input planes: whole contiguous input rows (both parities) are
+    // staged with one bulk copy; a per-stage table maps plane pixels to them
+    int I_rows;
+    int Hin, Win, Bin;
+    int TABW;                              // table entries per plane
+    uint32_t tab_off;                      // table offset from the dynamic smem base
     int Ho, Wo;                            // dO extents (rows per image, pixels per row)
 };
 #define WTRACE(role, idx, ev)                                                              \
@@ -164,6 +170,17 @@ __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint
                  : "memory");
 }
 
+// stride-2 rows mode: global input rows [rA, rB] covering every plane window
+// of the stage (virtual rows R = b*Hg + Y map to input rows b*H + 2Y + a)
+__device__ __forceinline__ void w_in_rows(const WgradMma &P, int wlo, int whi, int &rA, int &rB) {
+    const int Ra = wlo / P.Wg, Rb = whi / P.Wg;
+    const int bA = Ra / P.Hg, YA = Ra - bA * P.Hg;
+    const int bB = Rb / P.Hg, YB = Rb - bB * P.Hg;
+    rA = bA * P.Hin + 2 * YA;
+    rB = min(bB * P.Hin + 2 * YB + 1, P.Bin * P.Hin - 1);
+    if (rB < rA) rB = rA - 1;
+}
+
 struct WGroup {
     int np, nbI, clo;
     int minsh[4], span[4], ox[4], oy[4];
@@ -187,7 +204,20 @@ __device__ __forceinline__ uint32_t w_issue(const WgradMma &P, const WGroup &G, 
                                             bool issue, int lane) {
     uint32_t bytes = 0;
     int box_id = 0;
-    if (P.I_contig) {
+    if (P.I_rows) {
+        int wlo = 1 << 30, whi = -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < G.np) { wlo = min(wlo, v0 + G.minsh[k]); whi = max(whi, v0 + G.minsh[k] + P.KP + G.span[k] - 1); }
+        int rA, rB;
+        w_in_rows(P, wlo, min(whi, P.vtotal - 1), rA, rB);
+        if (rB >= rA) {
+            const uint32_t nb = (uint32_t)(rB - rA + 1) * P.Win * P.C * 32u;
+            if (issue && lane == 0) bulk_g2s_u32(stg, P.I_ptr + (size_t)rA * P.Win * P.C * 32, nb, (uint64_t *)0, mbar);
+            bytes += nb;
+        }
+        ++box_id;
+    } else if (P.I_contig) {
         // stride 1: the window of input pixels is contiguous in memory (one plane, all channels)
         const int lo = v0 + G.minsh[0];
         const int hi = min(v0 + P.KP + G.span[0] + G.minsh[0], P.vtotal);
@@ -312,6 +342,7 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
 // large kernel parameters and must not be re-read per stage.
 constexpr int kWMaxTG = 8;
 struct WLane {
+    uint32_t loff[kWMaxTG];   // lane offset inside a staged pixel: channel box + capsule column
     uint32_t base[kWMaxTG];   // staging byte offset of this lane's capsule row at window pixel 0 (minus plane start)
     int kpl[kWMaxTG];         // staged plane index (-1: padding row)
     int sp0[kWMaxTG];         // staged pixel (within its plane window) read for stage pixel 0
@@ -331,6 +362,7 @@ __device__ __forceinline__ void w_lane_setup(const WgradMma &P, int g, int q, in
     for (int tt = 0; tt < kWMaxTG; ++tt) {
         L.kpl[tt] = -1;
         L.base[tt] = 0;
+        L.loff[tt] = 0;
         L.sp0[tt] = 0;
         if (tt >= L.ntl) continue;
         const WTile &T = P.tile[g * P.TG + tt];
@@ -345,9 +377,66 @@ __device__ __forceinline__ void w_lane_setup(const WgradMma &P, int g, int q, in
                 const int bx = cl / P.CBI, cc = cl - bx * P.CBI;
                 L.kpl[tt] = k;
                 L.sp0[tt] = S.shift - P.g_minsh[g][k];
+                L.loff[tt] = (uint32_t)bx * P.capI * pxb + (uint32_t)(cc * 32 + d1 * 8);
                 L.base[tt] = k * P.stgI_plane + (uint32_t)bx * P.capI * pxb +
                              (uint32_t)(S.shift - P.g_minsh[g][k]) * pxb + (uint32_t)(cc * 32 + d1 * 8);
             }
+        }
+    }
+}
+
+// Rows mode: table[k][w] = staged pixel of plane k's window position w
+// (window of plane k starts at v0 + minsh_k), -1 outside the input.
+__device__ __forceinline__ void w_build_table(const WgradMma &P, const WGroup &G, int v0, uint32_t tab, int tid) {
+    int wlo = 1 << 30, whi = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (k < G.np) { wlo = min(wlo, v0 + G.minsh[k]); whi = max(whi, v0 + G.minsh[k] + P.KP + G.span[k] - 1); }
+    int rA, rB;
+    w_in_rows(P, wlo, min(whi, P.vtotal - 1), rA, rB);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    for (int e = tid; e < 4 * P.TABW; e += kWLoad) {
+        const int k = e / P.TABW, w = e - k * P.TABW;
+        int idx = -1;
+        if (k < G.np && w < P.KP + G.span[k]) {
+            const int v = v0 + G.minsh[k] + w;
+            if (v < P.vtotal) {
+                const uint32_t b = P.fd_HgWg.div((uint32_t)v);
+                const uint32_t rr = (uint32_t)v - b * HgWg;
+                const uint32_t Y = P.fd_Wg.div(rr);
+                const uint32_t X = rr - Y * (uint32_t)P.Wg;
+                const int y = 2 * (int)Y + G.oy[k], x = 2 * (int)X + G.ox[k];
+                if (y < P.Hin && x < P.Win) idx = ((int)b * P.Hin + y - rA) * P.Win + x;
+            }
+        }
+        asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(tab + (uint32_t)e * 4u), "r"(idx) : "memory");
+    }
+}
+
+__device__ __forceinline__ void w_load_A_rows(const WgradMma &P, const WLane &L, uint32_t stg, uint32_t tab,
+                                              uint32_t zero8, uint32_t tm_a, int q, int part) {
+    constexpr int kParts = kWLoad / 128;
+    const uint32_t pxb = (uint32_t)P.CBI * 32u;
+    const int nk = P.KP / 4;
+    const uint32_t lane_q = (uint32_t)(q * 32) << 16;
+#pragma unroll
+    for (int tt = 0; tt < kWMaxTG; ++tt) {
+        if (tt >= L.ntl) break;
+        const int k = L.kpl[tt] < 0 ? 0 : L.kpl[tt];
+        const uint32_t trow = tab + (uint32_t)(k * P.TABW + L.sp0[tt]) * 4u;
+        const uint32_t dcol = tm_a + lane_q + (uint32_t)(tt * nk * 8);
+        for (int kk = part; kk < nk; kk += kParts) {
+            int idx[4];
+#pragma unroll
+            for (int px = 0; px < 4; ++px)
+                asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx[px]) : "r"(trow + (uint32_t)(kk * 4 + px) * 4u));
+            uint32_t r[8];
+#pragma unroll
+            for (int px = 0; px < 4; ++px) {
+                const uint32_t a = idx[px] >= 0 ? stg + (uint32_t)idx[px] * pxb + L.loff[tt] : zero8;
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(r[2 * px]), "=r"(r[2 * px + 1]) : "r"(a));
+            }
+            tmem_st8(dcol + (uint32_t)(kk * 8), r);
         }
     }
 }
@@ -401,6 +490,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     constexpr int kEpi0 = kWLoad / 32, kMma = kEpi0 + kWEpi / 32, kTma = kMma + 1;
 
+    const uint32_t zero8 = smem_u32(smem_raw) + 768;   // 16 zero bytes (padding pixels)
+    if (threadIdx.x < 4) reinterpret_cast<uint32_t *>(smem_raw + 768)[threadIdx.x] = 0u;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(stg_full + i, 1);
@@ -466,11 +557,15 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             wdecode(P, item, g, ks, p0, p1);
             WLane L;
             w_lane_setup(P, g, q, lane, L);
+            WGroup G;
+            w_group_setup(P, g, G);
+            const uint32_t tab = smem_u32(smem_raw) + P.tab_off;
             for (int v0 = p0; v0 < p1; v0 += P.KP) {
                 const int si = (v0 - p0) / P.KP;
                 if (tid == 0) WTRACE(1, si, 0);
                 mbar_wait(stg_full + sb, sph);
                 if (tid == 0) WTRACE(1, si, 1);
+                if (P.I_rows) w_build_table(P, G, v0, tab, tid);
                 w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, tid);
                 named_bar_sync(1, kWLoad);
                 mbar_wait(op_empty + st, ph ^ 1);
@@ -478,7 +573,10 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 if (tid == 0) WTRACE(1, si, 2);
                 const uint32_t stg = stg0 + sb * P.stg_bytes;
                 w_load_B(P, v0, stg, op0 + st * P.b_bytes, tid);
-                w_load_A(P, L, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
+                if (P.I_rows)
+                    w_load_A_rows(P, L, stg, tab, zero8, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
+                else
+                    w_load_A(P, L, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 fence_proxy_async_smem();
                 fence_before_sync();
@@ -644,6 +742,8 @@ WPlan make_wplan(const Problem &p) {
         pl.O_B = p.B; pl.O_H = p.Ho; pl.O_W = p.Wo; pl.O_C = p.Cout;
     }
     P.I_contig = (!fc && s == 1 && P.C <= 16) ? 1 : 0;
+    P.I_rows = (!fc && s == 2 && P.C <= 16) ? 1 : 0;
+    P.Hin = (int)p.H; P.Win = (int)p.W; P.Bin = (int)p.B;
     P.Ho = (int)pl.O_H; P.Wo = (int)pl.O_W;
     const long long vt = (long long)P.Bn * P.Hg * P.Wg;
     if (vt * 4 >= (1ll << 31)) return pl;
@@ -704,7 +804,7 @@ WPlan make_wplan(const Problem &p) {
         if (force_tg && TG != force_tg) continue;
         const int ngroups = cdiv(P.n_mtiles, TG);
         // group unions
-        int gmax_np = 1, gmax_span = 0, gmax_ci = 0;
+        int gmax_np = 1, gmax_span = 0, gmax_ci = 0, gmax_msh = 0;
         for (int g = 0; g < ngroups; ++g) {
             int np = 0, plane[4], mn[4], mx[4], clo = 1 << 30, chi = 0;
             for (int mt = g * TG; mt < std::min(P.n_mtiles, (g + 1) * TG); ++mt) {
@@ -724,6 +824,11 @@ WPlan make_wplan(const Problem &p) {
                 gmax_span = std::max(gmax_span, mx[k] - mn[k]);
             }
             P.g_clo[g] = clo; P.g_chi[g] = chi;
+            {
+                int lo = 1 << 30, hi = -(1 << 30);
+                for (int k = 0; k < np; ++k) { lo = std::min(lo, mn[k]); hi = std::max(hi, mx[k]); }
+                gmax_msh = std::max(gmax_msh, hi - lo - 0);
+            }
             gmax_np = std::max(gmax_np, np);
             gmax_ci = std::max(gmax_ci, chi - clo);
         }
@@ -738,25 +843,32 @@ WPlan make_wplan(const Problem &p) {
             for (int n = 3; n >= 2; --n)
                 if (acc + n * abuf <= 512) { ns = n; break; }
             if (!ns) continue;
+            // rows mode: both parities of every virtual row the union window touches
+            const int rows_mode_cap = 2 * ((KP + gmax_span + gmax_msh - 1) / P.Wg + 2) * P.Win;
             const int capI = P.batch_mode ? KP
                              : P.I_contig ? KP + gmax_span
+                             : P.I_rows   ? rows_mode_cap
                                           : ((KP + gmax_span - 1) / P.Wg + 2) * P.Wg;
             // dO: whole dO rows touched by the window
             const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wo;
             const uint32_t stgI_plane = (uint32_t)nbI * capI * P.CBI * 32;
-            const uint32_t stgI = (uint32_t)gmax_np * stgI_plane;
+            const uint32_t stgI = P.I_rows ? stgI_plane : (uint32_t)gmax_np * stgI_plane;
+            const int TABW = KP + gmax_span;
             const uint32_t stgO = (uint32_t)capO * P.Cout * 32;
             const uint32_t stg = stgI + stgO;
             const uint32_t sbo = (uint32_t)KP * 64 + 16;
             const uint32_t bbytes = (uint32_t)(P.N_tile / 8) * sbo;
             for (int nstg = 3; nstg >= 2 && !found; --nstg) {
-                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes;
+                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes + (P.I_rows ? 16 * TABW : 0);
                 if (tot > kWSmemLimit) continue;
                 P.TG = TG; P.n_groups = ngroups;
                 P.KP = KP; P.capI = capI; P.capO = capO; P.stgI_plane = stgI_plane; P.stgI_bytes = stgI;
                 P.stgO_bytes = stgO; P.stg_bytes = stg; P.b_sbo = sbo; P.b_bytes = bbytes;
                 P.nstg = nstg; P.nstages = ns; P.smem_bytes = (uint32_t)tot;
                 P.acc_cols = acc; P.abuf_cols = abuf;
+                P.TABW = TABW;
+                P.tab_off = 1024 + nstg * stg + ns * bbytes;
+                if (P.I_rows) P.stgI_plane = 0;   // one staged region shared by all planes
                 found = true;
             }
             if (found) break;
@@ -765,7 +877,8 @@ WPlan make_wplan(const Problem &p) {
     if (!found) return pl;
     // ---- split of the pixel range so that items fill the machine
     const int nstage_total = cdiv(P.vtotal, P.KP);
-    int ks = std::max(1, std::min(nstage_total, cdiv(2 * nsm, P.n_groups)));
+    // one item per CTA: fewer fp32 partials for the finalize pass to read
+    int ks = std::max(1, std::min(nstage_total, nsm / std::max(1, P.n_groups)));
     const int stages_per = cdiv(nstage_total, ks);
     P.kpix = stages_per * P.KP;
     P.ksplit = cdiv(P.vtotal, P.kpix);
