@@ -57,6 +57,10 @@ struct ConvMma {
     uint32_t stg_plane_bytes;  // stg_cap_px * CC * 32
     uint32_t stg_bytes;        // npl * stg_plane_bytes
     int nstg;                  // staging buffers (1 or 2)
+    // stride-2 forward: whole input rows (both parities) staged with one bulk
+    // copy; a per-stage table maps each plane pixel of the window to them
+    int I_rows, Hin, Win, Bin;
+    uint32_t tab_off;          // table offset from the dynamic smem base (npl * win_px int32)
     // ---- tensors
     const __nv_bfloat16 *src;  // A source, natural capsule layout, pixel = CS*16 elements
     const uint8_t *wpack;      // prepacked B: [ntile][chunk][tap][kc][N_tile][16 B]

@@ -70,12 +70,35 @@ __device__ __forceinline__ int staging_off(const ConvMma &P, int v0) {
     return P.stg_batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
 }
 
+// rows mode: global input rows [rA, rB] covering the window [v0, v0 + win_px)
+// of every plane (virtual row R = b*Hg + Y -> input rows b*H + 2Y + a)
+__device__ __forceinline__ void conv_in_rows(const ConvMma &P, int v0, int &rA, int &rB) {
+    const int wlo = max(v0, 0), whi = min(v0 + P.win_px, P.Bn * P.Hg * P.Wg) - 1;
+    const int Ra = wlo / P.Wg, Rb = whi / P.Wg;
+    const int bA = Ra / P.Hg, YA = Ra - bA * P.Hg;
+    const int bB = Rb / P.Hg, YB = Rb - bB * P.Hg;
+    rA = bA * P.Hin + 2 * YA;
+    rB = min(bB * P.Hin + 2 * YB + 1, P.Bin * P.Hin - 1);
+    if (whi < wlo) rB = rA - 1;
+}
+
 // TMA thread: stage the natural-layout source pixels covering the window of
 // channel chunk `ch` for every plane.  Rows mode: one box per virtual row
 // (Wg pixels, every pl_s-th source pixel, rows/batches outside the tensor
 // read as zero).  Batch mode (Hg*Wg == 1): boxes of BB images.
 __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &it, int ch, uint32_t stg,
                                                   uint32_t mbar) {
+    if (P.I_rows) {
+        int rA, rB;
+        conv_in_rows(P, window_v0(P, it), rA, rB);
+        if (rB < rA) return 0;
+        const uint32_t nb = (uint32_t)(rB - rA + 1) * P.Win * P.CS * 32u;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         stg),
+                     "l"(reinterpret_cast<const uint8_t *>(P.src) + (size_t)rA * P.Win * P.CS * 32), "r"(nb), "r"(mbar)
+                     : "memory");
+        return nb;
+    }
     const int v0 = window_v0(P, it);
     const int len = P.win_px;
     const int c0 = ch * P.CC * 16;
@@ -103,6 +126,11 @@ __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &
 }
 
 __device__ __forceinline__ uint32_t staging_bytes(const ConvMma &P, const Item &it) {
+    if (P.I_rows) {
+        int rA, rB;
+        conv_in_rows(P, window_v0(P, it), rA, rB);
+        return rB >= rA ? (uint32_t)(rB - rA + 1) * P.Win * P.CS * 32u : 0u;
+    }
     const int v0 = window_v0(P, it);
     const uint32_t px_bytes = (uint32_t)P.CC * 32u;
     uint32_t per_plane;
@@ -119,6 +147,52 @@ __device__ __forceinline__ uint32_t staging_bytes(const ConvMma &P, const Item &
 // Producers: repack the staged natural layout [pixel][c][d1][d2] into the
 // K-major window rows (pixel, d1) x k-chunks (c pair, d2): each 16-byte unit
 // (c, rows 2i, 2i+1) becomes two 8-byte pieces (the D1 repack of SURVEY H1).
+// rows mode: tab[k*win_px + vl] = staged pixel of plane k, window pixel vl (-1: outside)
+__device__ __forceinline__ void build_table(const ConvMma &P, const Item &it, uint32_t tab, int tid) {
+    const int v0 = window_v0(P, it);
+    int rA, rB;
+    conv_in_rows(P, v0, rA, rB);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const int vtotal = P.Bn * P.Hg * P.Wg;
+    for (int e = tid; e < P.npl * P.win_px; e += kProducerThreads) {
+        int k = 0, vl = e;
+        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+        const int v = v0 + vl;
+        int idx = -1;
+        if (v >= 0 && v < vtotal) {
+            const uint32_t b = P.fd_HgWg.div((uint32_t)v);
+            const uint32_t rr = (uint32_t)v - b * HgWg;
+            const uint32_t Y = P.fd_Wg.div(rr);
+            const uint32_t X = rr - Y * (uint32_t)P.Wg;
+            const int y = 2 * (int)Y + P.pl_oy[k], x = 2 * (int)X + P.pl_ox[k];
+            if (y < P.Hin && x < P.Win) idx = ((int)b * P.Hin + y - rA) * P.Win + x;
+        }
+        asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(tab + (uint32_t)e * 4u), "r"(idx) : "memory");
+    }
+}
+
+__device__ __forceinline__ void repack_rows(const ConvMma &P, uint32_t stg, uint32_t tab, uint32_t a_stage, int tid) {
+    const int upp = 2 * P.CC;
+    const int total = P.npl * P.win_px * upp;
+    const uint32_t px_bytes = (uint32_t)P.CC * 32u;
+#pragma unroll 4
+    for (int L = tid; L < total; L += kProducerThreads) {
+        const int pix = (int)P.fd_units.div((uint32_t)L);      // k * win_px + vl
+        const int u2 = L - pix * upp;
+        const int c = u2 >> 1, i = u2 & 1;
+        int k = 0, vl = pix;
+        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+        int idx;
+        asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(tab + (uint32_t)pix * 4u));
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (idx >= 0) v = ld_shared_v4(stg + (uint32_t)idx * px_bytes + (uint32_t)u2 * 16u);
+        const uint32_t dst = a_stage + k * P.plane_bytes + (c >> 1) * P.a_lbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
+                             (c & 1) * 8u;
+        st_shared_v2(dst, v.x, v.y);
+        st_shared_v2(dst + 16u, v.z, v.w);
+    }
+}
+
 __device__ __forceinline__ void repack_window(const ConvMma &P, const Item &it, uint32_t stg, uint32_t a_stage,
                                               int tid) {
     const int upp = 2 * P.CC;
@@ -242,7 +316,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 }
                 mbar_wait(stg_full + sb, sphase);
                 if (tid == 0) TRACE(0, ii, 1);
-                if (!(P.dbg & 1)) repack_window(P, it, stg0 + sb * P.stg_bytes, a_stage, tid);
+                if (P.I_rows) {
+                    const uint32_t tab = smem_u32(smem_raw) + P.tab_off;
+                    build_table(P, it, tab, tid);
+                    asm volatile("bar.sync 1, %0;\n" ::"r"(kProducerThreads) : "memory");
+                    repack_rows(P, stg0 + sb * P.stg_bytes, tab, a_stage, tid);
+                    asm volatile("bar.sync 1, %0;\n" ::"r"(kProducerThreads) : "memory");   // table reuse
+                } else if (!(P.dbg & 1)) {
+                    repack_window(P, it, stg0 + sb * P.stg_bytes, a_stage, tid);
+                }
                 fence_proxy_async_smem();
                 mbar_arrive(a_full + stage);
                 mbar_arrive(stg_empty + sb);
@@ -619,27 +701,35 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const bool bres = (P.nog == 1 && nchunks == 1 && P.n_ntiles == 1);
             // staging of the natural layout (whole virtual rows, or BB-image boxes)
             const bool batch_mode = (P.Hg * P.Wg == 1);
-            if (!batch_mode && P.Wg * s > 256) continue;
+            const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1;
+            if (!batch_mode && !rows_mode && P.Wg * s > 256) continue;
             const int BB = std::min(win_px, 256);
-            const int cap = batch_mode ? ceil_div(win_px, BB) * BB : ((win_px - 1) / P.Wg + 2) * P.Wg;
+            const int cap = batch_mode ? ceil_div(win_px, BB) * BB
+                            : rows_mode ? 2 * ((win_px - 1) / P.Wg + 2) * (int)p.W
+                                        : ((win_px - 1) / P.Wg + 2) * P.Wg;
             const uint32_t stg_plane = (uint32_t)cap * cc * 32;
-            const uint32_t stg = (uint32_t)P.npl * stg_plane;
+            const uint32_t stg = rows_mode ? stg_plane : (uint32_t)P.npl * stg_plane;
+            const uint32_t tab_bytes = rows_mode ? (uint32_t)(P.npl * win_px * 4 + 15) & ~15u : 0u;
             int best_st = 0, best_nstg = 0;
             for (int nstg = 2; nstg >= 1 && !best_st; --nstg)
                 for (int st = std::min(kMaxStages, 4); st >= (nstg == 2 ? 2 : 3); --st) {
                     const uint64_t bytes = 1024 + (uint64_t)nstg * stg + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) +
-                                           (bres ? b_stage : 0);
+                                           (bres ? b_stage : 0) + tab_bytes;
                     if (bytes <= kSmemLimit) { best_st = st; best_nstg = nstg; break; }
                 }
             if (!best_st) continue;
             P.stg_batch_mode = batch_mode ? 1 : 0; P.BB = BB; P.stg_cap_px = cap;
             P.stg_plane_bytes = stg_plane; P.stg_bytes = stg; P.nstg = best_nstg;
+            P.I_rows = rows_mode ? 1 : 0;
+            P.Hin = (int)p.H; P.Win = (int)p.W; P.Bin = (int)p.B;
             if (a_lbo >= (1u << 18) || b_stage >= (1u << 20)) continue;
             P.CC = cc; P.nchunks = nchunks; P.ksplit = ksplit; P.G = G;
             P.win_px = win_px; P.a_lbo = a_lbo; P.plane_bytes = plane;
             P.a_stage_bytes = a_stage; P.b_stage_bytes = b_stage;
             P.b_resident = bres ? 1 : 0; P.nstages = best_st;
-            P.smem_bytes = 1024 + best_nstg * stg + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
+            P.smem_bytes = 1024 + best_nstg * stg + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0) +
+                           tab_bytes;
+            P.tab_off = 1024 + best_nstg * stg + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
             found = true;
             break;
         }
