@@ -680,13 +680,17 @@ Plan make_plan(const Problem &p, bool dgrad) {
     for (int cc = std::min(P.CSpad, 16); cc >= 4; cc -= 4)   // TMA box: cc*16 <= 256 elements
         if (P.CSpad % cc == 0) ccs.push_back(cc);
     bool found = false;
-    for (int cc : ccs) {
-        const int nchunks = P.CSpad / cc;
-        int ksplit = 1;
-        if (base_items < nsm && P.nog == 1) ksplit = std::min(nchunks, ceil_div(2 * nsm, base_items));
-        static const int force_g = getenv("CAPSCONV_FORCE_G") ? atoi(getenv("CAPSCONV_FORCE_G")) : 0;
-        for (int G : {8, 4, 2, 1}) {
-            if (force_g && G != force_g) continue;
+    ConvMma best;
+    long long best_score = -1;
+    static const int force_g = getenv("CAPSCONV_FORCE_G") ? atoi(getenv("CAPSCONV_FORCE_G")) : 0;
+    for (int G : {8, 4, 2, 1}) {
+        if (force_g && G != force_g) continue;
+        for (int cc : ccs) {
+            static const int force_cc = getenv("CAPSCONV_FORCE_CC") ? atoi(getenv("CAPSCONV_FORCE_CC")) : 0;
+            if (force_cc && cc != force_cc) continue;
+            const int nchunks = P.CSpad / cc;
+            int ksplit = 1;
+            if (base_items < nsm && P.nog == 1) ksplit = std::min(nchunks, ceil_div(2 * nsm, base_items));
             if (2 * G * P.N_tile > 512) continue;
             const long long items = (long long)P.nog * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
             if (G > 1 && items < 2 * nsm && !force_g) continue;
@@ -730,12 +734,19 @@ Plan make_plan(const Problem &p, bool dgrad) {
             P.smem_bytes = 1024 + best_nstg * stg + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0) +
                            tab_bytes;
             P.tab_off = 1024 + best_nstg * stg + best_st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0);
+            // measured on the stack layers (tests/probe/gcc_sweep.sh): time
+            // falls with G*CC (MMAs per staged window); at equal G*CC the
+            // larger G wins (fewer items), except for stride 2, where the
+            // wider chunk wins (fwd: whole-row staging needs one chunk;
+            // dI: s*s phase groups each restage the window per chunk)
+            const bool prefer_cc = s == 2 && !full_extent;
+            const long long score = (long long)G * cc * 64 + (prefer_cc ? cc : G);
+            if (!found || score > best_score) { best = P; best_score = score; }
             found = true;
-            break;
         }
-        if (found) break;
     }
     if (!found) return pl;
+    P = best;
     P.n_igroups = ceil_div(P.n_mtiles, P.G);
     P.n_items = P.nog * P.n_igroups * P.n_ntiles * P.ksplit;
     uint32_t cols = 32;
