@@ -95,7 +95,7 @@ struct WgradMma {
     int nstg, nstages;
     uint32_t smem_bytes, tmem_cols;
     unsigned long long *trace;             // debug: globaltimer stamps of CTA 0 [role][stage][4]
-    int dbg;                               // bench-only: 1 skip transpose, 2 skip TMEM stores, 4 skip B, 8 skip LDS
+    int dbg;                               // bench-only (wrong results): 1 skip transpose, 4 skip B, 16 skip A
     // contiguous staging (1-D bulk copies): dO always; I when stride 1 (not FC)
     const uint8_t *I_ptr, *O_ptr;
     int I_contig;
@@ -104,7 +104,14 @@ struct WgradMma {
     int I_rows;
     int Hin, Win, Bin;
     int TABW;                              // table entries per plane
-    uint32_t tab_off;                      // table offset from the dynamic smem base
+    uint32_t tab_off;                      // tables (per staging buffer) offset from the dynamic smem base
+    uint32_t tab_stride;                   // bytes of tables per staging buffer
+    uint32_t btab_off;                     // B source table offset inside a buffer's tables
+    // column shifts: B holds nq copies of the dO window,
+    // copy j read at virtual pixel u - j, side by side in N; D column block j
+    // of a slot for tap (p, q) is the gradient of tap (p, q + s*j)
+    int nq, KWv;
+    int b_pstep;                           // staged dO pixels per B-loader iteration (loader threads / (2*Cout))
     int Ho, Wo;                            // dO extents (rows per image, pixels per row)
 };
 #define WTRACE(role, idx, ev)                                                              \
@@ -155,13 +162,14 @@ __device__ __forceinline__ int w_off(const WgradMma &P, int v0) {
 }
 
 // dO rows [ra, rb) (global row index b*Ho + Y) covering virtual pixels [v0, v0 + KP)
+// (v0 >= 0 on the forward grid; FastDiv: no runtime integer division)
 __device__ __forceinline__ void w_dO_rows(const WgradMma &P, int v0, int &ra, int &rb) {
-    const int Ra = v0 / P.Wg;                       // virtual rows (v0 >= 0 for the forward grid)
-    const int Rb = (min(v0 + P.KP, P.vtotal) - 1) / P.Wg;
-    const int ba = Ra / P.Hg, ya = Ra - ba * P.Hg;
-    const int bb = Rb / P.Hg, yb = Rb - bb * P.Hg;
-    ra = ya < P.Ho ? ba * P.Ho + ya : (ba + 1) * P.Ho;
-    rb = yb < P.Ho ? bb * P.Ho + yb + 1 : (bb + 1) * P.Ho;
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const uint32_t va = (uint32_t)max(v0 - (P.nq - 1), 0), vb = (uint32_t)(min(v0 + P.KP, P.vtotal) - 1);
+    const uint32_t ba = P.fd_HgWg.div(va), bb = P.fd_HgWg.div(vb);
+    const int ya = (int)P.fd_Wg.div(va - ba * HgWg), yb = (int)P.fd_Wg.div(vb - bb * HgWg);
+    ra = ya < P.Ho ? (int)ba * P.Ho + ya : ((int)ba + 1) * P.Ho;
+    rb = yb < P.Ho ? (int)bb * P.Ho + yb + 1 : ((int)bb + 1) * P.Ho;
 }
 
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint32_t bytes, uint64_t *, uint32_t mbar) {
@@ -173,11 +181,11 @@ __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint
 // stride-2 rows mode: global input rows [rA, rB] covering every plane window
 // of the stage (virtual rows R = b*Hg + Y map to input rows b*H + 2Y + a)
 __device__ __forceinline__ void w_in_rows(const WgradMma &P, int wlo, int whi, int &rA, int &rB) {
-    const int Ra = wlo / P.Wg, Rb = whi / P.Wg;
-    const int bA = Ra / P.Hg, YA = Ra - bA * P.Hg;
-    const int bB = Rb / P.Hg, YB = Rb - bB * P.Hg;
-    rA = bA * P.Hin + 2 * YA;
-    rB = min(bB * P.Hin + 2 * YB + 1, P.Bin * P.Hin - 1);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const uint32_t bA = P.fd_HgWg.div((uint32_t)wlo), bB = P.fd_HgWg.div((uint32_t)whi);
+    const int YA = (int)P.fd_Wg.div((uint32_t)wlo - bA * HgWg), YB = (int)P.fd_Wg.div((uint32_t)whi - bB * HgWg);
+    rA = (int)bA * P.Hin + 2 * YA;
+    rB = min((int)bB * P.Hin + 2 * YB + 1, P.Bin * P.Hin - 1);
     if (rB < rA) rB = rA - 1;
 }
 
@@ -248,38 +256,66 @@ __device__ __forceinline__ uint32_t w_issue(const WgradMma &P, const WGroup &G, 
     return bytes;
 }
 
-// dO -> B: MN-major shared-memory operand, columns n = (c', d3) in groups of
-// 8 (c' pair), k-rows (v, d1) at 16 bytes; a capsule unit (c', d1 rows 2i,
-// 2i+1) becomes two 8-byte pieces (the D1 transpose).
-__device__ __forceinline__ void w_load_B(const WgradMma &P, int v0, uint32_t stg, uint32_t b, int tid) {
-    // staged dO = whole dO rows [ra, rb); virtual pixel (b, Y, X) is valid for
-    // Y < Ho, X < Wo and then sits at staged pixel (b*Ho + Y - ra)*Wo + X.
+// B source table: entry e (0 <= e < KP + nq - 1) = staged dO pixel of
+// virtual pixel v0 - (nq - 1) + e, or -1 (outside dO: a zero row of B)
+__device__ __forceinline__ void w_build_btab(const WgradMma &P, int v0, uint32_t btab, int tid) {
     int ra, rb;
     w_dO_rows(P, v0, ra, rb);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const int n = P.KP + P.nq - 1;
+    for (int e = tid; e < n; e += kWLoad) {
+        const int vv = v0 - (P.nq - 1) + e;
+        int idx = -1;
+        if (vv >= 0 && vv < P.vtotal) {
+            const uint32_t bq = P.fd_HgWg.div((uint32_t)vv);
+            const uint32_t rr = (uint32_t)vv - bq * HgWg;
+            const uint32_t Y = P.fd_Wg.div(rr);
+            const uint32_t X = rr - Y * (uint32_t)P.Wg;
+            if ((int)Y < P.Ho && (int)X < P.Wo) idx = ((int)bq * P.Ho + (int)Y - ra) * P.Wo + (int)X;
+        }
+        asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(btab + (uint32_t)e * 4u), "r"(idx) : "memory");
+    }
+}
+
+// dO -> B: MN-major shared-memory operand, columns n = (j, c', d3) in groups
+// of 8 (c' pair), k-rows (v, d1) at 16 bytes; a capsule unit (c', d1 rows
+// 2i, 2i+1) becomes two 8-byte pieces (the D1 transpose).  Copy j holds
+// dO[v - j]: each staged unit is loaded once and stored into every copy
+// whose local row falls inside the stage.
+constexpr int kWMaxNq = 4;
+__device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32_t btab, uint32_t b, int tid) {
+    // thread -> fixed unit (c', i) of a staged pixel; pixels advance by
+    // P.b_pstep per iteration (b_pstep * upp <= loader threads): no division
     const uint32_t base = stg + P.stgI_bytes;
     const int upp = 2 * P.Cout;
-    const int total = P.KP * upp;
+    const int pix0 = tid / upp;                 // once per stage
+    const int u = tid - pix0 * upp;
+    if (pix0 >= P.b_pstep) return;
+    const int c = u >> 1, i = u & 1;
     const uint32_t pxb = (uint32_t)P.Cout * 32u;
-    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const uint32_t src_off = (uint32_t)(c * 32 + i * 16);
+    const int npx = P.KP + P.nq - 1;
+    uint32_t dcol[kWMaxNq];                     // per copy: column-group offset of this unit
+#pragma unroll
+    for (int j = 0; j < kWMaxNq; ++j) {
+        const int col = j * P.Cout + c;
+        dcol[j] = b + (uint32_t)(col >> 1) * P.b_sbo + (uint32_t)(2 * i) * 16u + (col & 1) * 8u;
+    }
 #pragma unroll 4
-    for (int L = tid; L < total; L += kWLoad) {
-        const int vl = (int)P.fd_uppO.div((uint32_t)L);
-        const int u = L - vl * upp;
-        const int c = u >> 1, i = u & 1;
-        const int vv = v0 + vl;
-        const uint32_t bq = P.fd_HgWg.div((uint32_t)vv);
-        const uint32_t rr = (uint32_t)vv - bq * HgWg;
-        const uint32_t Y = P.fd_Wg.div(rr);
-        const uint32_t X = rr - Y * (uint32_t)P.Wg;
-        uint4 v4 = make_uint4(0, 0, 0, 0);
-        if (vv < P.vtotal && (int)Y < P.Ho && (int)X < P.Wo) {
-            const int sp = ((int)bq * P.Ho + (int)Y - ra) * P.Wo + (int)X;
-            v4 = ld_shared_v4(base + (uint32_t)sp * pxb + (uint32_t)(c * 32 + i * 16));
+    for (int e = pix0; e < npx; e += P.b_pstep) {
+        int idx;
+        asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(btab + (uint32_t)e * 4u));
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (idx >= 0) v = ld_shared_v4(base + (uint32_t)idx * pxb + src_off);
+#pragma unroll
+        for (int j = 0; j < kWMaxNq; ++j) {
+            const int l = e - (P.nq - 1) + j;     // local row of copy j
+            if (j < P.nq && l >= 0 && l < P.KP) {
+                const uint32_t dst = dcol[j] + (uint32_t)l * 64u;
+                st_shared_v2(dst, v.x, v.y);
+                st_shared_v2(dst + 16u, v.z, v.w);
+            }
         }
-        const uint4 v = v4;
-        const uint32_t dst = b + (uint32_t)(c >> 1) * P.b_sbo + (uint32_t)(vl * 4 + 2 * i) * 16u + (c & 1) * 8u;
-        st_shared_v2(dst, v.x, v.y);
-        st_shared_v2(dst + 16u, v.z, v.w);
     }
 }
 
@@ -307,15 +343,24 @@ __device__ __forceinline__ void transpose4x4(uint32_t &lo, uint32_t &hi, int r) 
 __device__ __forceinline__ void w_transpose_stage(uint32_t base, uint32_t bytes, int tid) {
     const int lane = tid & 31;
     const uint32_t n8 = bytes / 8;                      // 8-byte rows
-    const uint32_t step = (uint32_t)kWLoad;
+    constexpr uint32_t kStep = (uint32_t)kWLoad;
+    constexpr int kU = 4;                               // independent rows in flight per lane
     // all lanes of a warp iterate together (shuffles need the full warp)
-    for (uint32_t r0 = (uint32_t)(tid - lane); r0 < n8; r0 += step) {
-        const uint32_t r = r0 + (uint32_t)lane;
-        uint32_t lo = 0, hi = 0;
-        const uint32_t a = base + r * 8u;
-        if (r < n8) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(a));
-        transpose4x4(lo, hi, lane & 3);
-        if (r < n8) st_shared_v2(a, lo, hi);
+    for (uint32_t r0 = (uint32_t)(tid - lane); r0 < n8; r0 += kU * kStep) {
+        uint32_t lo[kU], hi[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t r = r0 + u * kStep + (uint32_t)lane;
+            lo[u] = 0; hi[u] = 0;
+            if (r < n8) asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(lo[u]), "=r"(hi[u]) : "r"(base + r * 8u));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) transpose4x4(lo[u], hi[u], lane & 3);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t r = r0 + u * kStep + (uint32_t)lane;
+            if (r < n8) st_shared_v2(base + r * 8u, lo[u], hi[u]);
+        }
     }
 }
 
@@ -347,6 +392,7 @@ struct WLane {
     int kpl[kWMaxTG];         // staged plane index (-1: padding row)
     int sp0[kWMaxTG];         // staged pixel (within its plane window) read for stage pixel 0
     int ntl, np;
+    uint32_t live;            // bit tt: some lane of this warp holds a real row of tile tt
     int minsh[4];
 };
 
@@ -383,6 +429,10 @@ __device__ __forceinline__ void w_lane_setup(const WgradMma &P, int g, int q, in
             }
         }
     }
+    L.live = 0;
+#pragma unroll
+    for (int tt = 0; tt < kWMaxTG; ++tt)
+        if (__any_sync(0xffffffffu, L.kpl[tt] >= 0)) L.live |= 1u << tt;
 }
 
 // Rows mode: table[k][w] = staged pixel of plane k's window position w
@@ -422,21 +472,29 @@ __device__ __forceinline__ void w_load_A_rows(const WgradMma &P, const WLane &L,
 #pragma unroll
     for (int tt = 0; tt < kWMaxTG; ++tt) {
         if (tt >= L.ntl) break;
+        if (!((L.live >> tt) & 1u)) continue;   // rows of this lane quarter are all padding: never stored
         const int k = L.kpl[tt] < 0 ? 0 : L.kpl[tt];
         const uint32_t trow = tab + (uint32_t)(k * P.TABW + L.sp0[tt]) * 4u;
         const uint32_t dcol = tm_a + lane_q + (uint32_t)(tt * nk * 8);
-        for (int kk = part; kk < nk; kk += kParts) {
-            int idx[4];
+        // two k-steps per batch (independent table and data loads in flight)
+        for (int kk = part; kk < nk; kk += 2 * kParts) {
+            const bool two = kk + kParts < nk;
+            const int kk2 = two ? kk + kParts : kk;
+            int idx[8];
 #pragma unroll
             for (int px = 0; px < 4; ++px)
                 asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx[px]) : "r"(trow + (uint32_t)(kk * 4 + px) * 4u));
-            uint32_t r[8];
 #pragma unroll
-            for (int px = 0; px < 4; ++px) {
+            for (int px = 0; px < 4; ++px)
+                asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx[4 + px]) : "r"(trow + (uint32_t)(kk2 * 4 + px) * 4u));
+            uint32_t r[16];
+#pragma unroll
+            for (int px = 0; px < 8; ++px) {
                 const uint32_t a = idx[px] >= 0 ? stg + (uint32_t)idx[px] * pxb + L.loff[tt] : zero8;
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n" : "=r"(r[2 * px]), "=r"(r[2 * px + 1]) : "r"(a));
             }
-            tmem_st8(dcol + (uint32_t)(kk * 8), r);
+            tmem_st8(dcol + (uint32_t)(kk * 8), *reinterpret_cast<const uint32_t(*)[8]>(r));
+            if (two) tmem_st8(dcol + (uint32_t)(kk2 * 8), *reinterpret_cast<const uint32_t(*)[8]>(r + 8));
         }
     }
 }
@@ -458,6 +516,7 @@ __device__ __forceinline__ void w_load_A(const WgradMma &P, const WLane &L, int 
 #pragma unroll
     for (int tt = 0; tt < kWMaxTG; ++tt) {
         if (tt >= L.ntl) break;
+        if (!((L.live >> tt) & 1u)) continue;   // rows of this lane quarter are all padding: never stored
         const int k = L.kpl[tt] < 0 ? 0 : L.kpl[tt];
         int wok = wo[0];
 #pragma unroll
@@ -465,15 +524,24 @@ __device__ __forceinline__ void w_load_A(const WgradMma &P, const WLane &L, int 
             if (k == kx) wok = wo[kx];
         const uint32_t src = stg + L.base[tt] + (uint32_t)wok * pxb;
         const uint32_t dcol = tm_a + lane_q + (uint32_t)(tt * nk * 8);
-        for (int kk = part; kk < nk; kk += kParts) {
-            uint32_t r[8];
+        // two k-steps per batch: 8 independent loads in flight before the TMEM stores
+        for (int kk = part; kk < nk; kk += 2 * kParts) {
+            const bool two = kk + kParts < nk;
+            uint32_t r[8], r2[8];
             const uint32_t a = src + (uint32_t)(kk * 4) * pxb;
+            const uint32_t a2 = two ? a + (uint32_t)(kParts * 4) * pxb : a;
 #pragma unroll
             for (int px = 0; px < 4; ++px)
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n"
                              : "=r"(r[2 * px]), "=r"(r[2 * px + 1])
                              : "r"(a + (uint32_t)px * pxb));
+#pragma unroll
+            for (int px = 0; px < 4; ++px)
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];\n"
+                             : "=r"(r2[2 * px]), "=r"(r2[2 * px + 1])
+                             : "r"(a2 + (uint32_t)px * pxb));
             tmem_st8(dcol + (uint32_t)(kk * 8), r);
+            if (two) tmem_st8(dcol + (uint32_t)((kk + kParts) * 8), r2);
         }
     }
 }
@@ -487,7 +555,9 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + 512);
     const uint32_t stg0 = smem_u32(smem_raw) + 1024;
     const uint32_t op0 = stg0 + P.nstg * P.stg_bytes;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // warp index broadcast from lane 0: the compiler then knows the role
+    // branches are warp-uniform and keeps the MMA operands in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
     constexpr int kEpi0 = kWLoad / 32, kMma = kEpi0 + kWEpi / 32, kTma = kMma + 1;
 
     const uint32_t zero8 = smem_u32(smem_raw) + 768;   // 16 zero bytes (padding pixels)
@@ -511,7 +581,11 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
-    const uint32_t tmem = *tmem_slot;
+    // all 512 columns belong to this CTA, so the allocation starts at lane 0,
+    // column 0.  Using the constant (not the value read back from shared
+    // memory) keeps every MMA operand in uniform registers -- no R2UR per MMA.
+    if (*tmem_slot != 0u) __trap();
+    constexpr uint32_t tmem = 0u;
     const int nk = P.KP / 4;
 
     if (warp == kTma) {
@@ -539,9 +613,48 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                     for (uint32_t z = zb + (uint32_t)lane * 16u; z < ze; z += 512u) st_shared_v4z(stg + z);
                     __syncwarp();
                 }
-                if (lane == 0) mbar_arrive_expect_tx(stg_full + sb, w_issue(P, G, v0, stg, 0, false, 0));
-                __syncwarp();
-                w_issue(P, G, v0, stg, smem_u32(stg_full + sb), true, lane);
+                if (P.I_contig || P.I_rows) {
+                    // at most two bulk copies: computed once, issued by lane 0
+                    if (lane == 0) {
+                        const uint32_t mb = smem_u32(stg_full + sb);
+                        const uint8_t *srcI = nullptr;
+                        uint32_t nbI = 0;
+                        if (P.I_rows) {
+                            int wlo = 1 << 30, whi = -1;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (k < G.np) {
+                                    wlo = min(wlo, v0 + G.minsh[k]);
+                                    whi = max(whi, v0 + G.minsh[k] + P.KP + G.span[k] - 1);
+                                }
+                            int rA, rB;
+                            w_in_rows(P, wlo, min(whi, P.vtotal - 1), rA, rB);
+                            if (rB >= rA) {
+                                nbI = (uint32_t)(rB - rA + 1) * P.Win * P.C * 32u;
+                                srcI = P.I_ptr + (size_t)rA * P.Win * P.C * 32;
+                            }
+                        } else {
+                            const int lo = v0 + G.minsh[0];
+                            const int hi = min(v0 + P.KP + G.span[0] + G.minsh[0], P.vtotal);
+                            if (hi > lo) {
+                                nbI = (uint32_t)(hi - lo) * P.C * 32u;
+                                srcI = P.I_ptr + (size_t)lo * P.C * 32;
+                            }
+                        }
+                        int ra, rb;
+                        w_dO_rows(P, v0, ra, rb);
+                        const uint32_t nbO = rb > ra ? (uint32_t)(rb - ra) * P.Wo * P.Cout * 32u : 0u;
+                        mbar_arrive_expect_tx(stg_full + sb, nbI + nbO);
+                        if (nbI) bulk_g2s_u32(stg, srcI, nbI, nullptr, mb);
+                        if (nbO)
+                            bulk_g2s_u32(stg + P.stgI_bytes, P.O_ptr + (size_t)ra * P.Wo * P.Cout * 32, nbO, nullptr, mb);
+                    }
+                    __syncwarp();
+                } else {
+                    if (lane == 0) mbar_arrive_expect_tx(stg_full + sb, w_issue(P, G, v0, stg, 0, false, 0));
+                    __syncwarp();
+                    w_issue(P, G, v0, stg, smem_u32(stg_full + sb), true, lane);
+                }
                 if (lane == 0) WTRACE(0, si, 2);
                 if (++sb == P.nstg) { sb = 0; sph ^= 1; }
             }
@@ -559,21 +672,26 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             w_lane_setup(P, g, q, lane, L);
             WGroup G;
             w_group_setup(P, g, G);
-            const uint32_t tab = smem_u32(smem_raw) + P.tab_off;
             for (int v0 = p0; v0 < p1; v0 += P.KP) {
+                // tables per staging buffer: a buffer is refilled (and its
+                // tables rewritten) only after every loader thread released it
+                const uint32_t tab = smem_u32(smem_raw) + P.tab_off + (uint32_t)sb * P.tab_stride;
+                const uint32_t btab = tab + P.btab_off;
                 const int si = (v0 - p0) / P.KP;
                 if (tid == 0) WTRACE(1, si, 0);
                 mbar_wait(stg_full + sb, sph);
                 if (tid == 0) WTRACE(1, si, 1);
                 if (P.I_rows) w_build_table(P, G, v0, tab, tid);
-                w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, tid);
+                w_build_btab(P, v0, btab, tid);
+                if (!(P.dbg & 1)) w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, tid);
                 named_bar_sync(1, kWLoad);
                 mbar_wait(op_empty + st, ph ^ 1);
                 fence_after_sync();
                 if (tid == 0) WTRACE(1, si, 2);
                 const uint32_t stg = stg0 + sb * P.stg_bytes;
-                w_load_B(P, v0, stg, op0 + st * P.b_bytes, tid);
-                if (P.I_rows)
+                if (!(P.dbg & 4)) w_load_B(P, stg, btab, op0 + st * P.b_bytes, tid);
+                if (P.dbg & 16) {
+                } else if (P.I_rows)
                     w_load_A_rows(P, L, stg, tab, zero8, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
                 else
                     w_load_A(P, L, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
@@ -606,19 +724,26 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 fence_after_sync();
                 const uint64_t bd0 = smem_desc(op0 + st * P.b_bytes, 128, P.b_sbo);
                 const uint32_t a0 = tmem + P.acc_cols + (uint32_t)st * P.abuf_cols;
-                if (elect_one()) {
-                    for (int tt = 0; tt < ntl; ++tt) {
-                        const uint32_t d = tmem + (uint32_t)(tt * P.N_tile);
-                        for (int kk = 0; kk < nk; ++kk) {
-                            asm volatile(
-                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
-                                "r"(a0 + (uint32_t)((tt * nk + kk) * 8)), "l"(bd0 + (uint64_t)(kk * 16)), "r"(idesc),
-                                "r"((first && kk == 0) ? 0u : 1u));
+                // the warp stays converged; one elected lane issues 4 MMAs at a
+                // time (a long divergent single-lane loop issues far slower)
+                for (int tt = 0; tt < ntl; ++tt) {
+                    const uint32_t d = tmem + (uint32_t)(tt * P.N_tile);
+                    for (int k4 = 0; k4 < nk; k4 += 4) {
+                        if (elect_one()) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int kk = k4 + u;
+                                asm volatile(
+                                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                    "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+                                    "r"(a0 + (uint32_t)((tt * nk + kk) * 8)), "l"(bd0 + (uint64_t)(kk * 16)),
+                                    "r"(idesc), "r"((first && kk == 0) ? 0u : 1u));
+                            }
                         }
+                        __syncwarp();
                     }
-                    mma_commit(op_empty + st);
                 }
+                if (elect_one()) mma_commit(op_empty + st);
                 __syncwarp();
                 first = false;
                 if (++st == P.nstages) { st = 0; ph ^= 1; }
@@ -651,6 +776,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                         c = S.c0 + ((row - S.row0) >> 2);
                     }
                 }
+                // column n = (j, c', d3): block j is tap (p, q + s*j) of the slot's tap (p, q)
+                const int q0 = tap < 0 ? 0 : tap % P.KWv;
                 float *dst = P.part + (size_t)ks * nkel + (((size_t)(tap < 0 ? 0 : tap) * P.C + c) * P.Cout) * 16 + d2 * 4;
                 const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(tt * P.N_tile);
                 for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
@@ -660,9 +787,10 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                     if (tap >= 0 && c < P.C) {
 #pragma unroll
                         for (int jj = 0; jj < 4; ++jj) {
-                            const int co = n0 / 4 + jj;
-                            if (co < P.Cout)
-                                *reinterpret_cast<float4 *>(dst + (size_t)co * 16) =
+                            const int cn = n0 / 4 + jj;           // capsule column j*Cout + c'
+                            const int j = cn / P.Cout, co = cn - j * P.Cout;
+                            if (j < P.nq && q0 + P.s * j < P.KWv)
+                                *reinterpret_cast<float4 *>(dst + ((size_t)P.s * j * P.C * P.Cout + co) * 16) =
                                     make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
                         }
                     }
@@ -748,26 +876,41 @@ WPlan make_wplan(const Problem &p) {
     const long long vt = (long long)P.Bn * P.Hg * P.Wg;
     if (vt * 4 >= (1ll << 31)) return pl;
     P.vtotal = (int)vt;
-    P.N_tile = cdiv(P.Cout * 4, 16) * 16;
+    // ---- column shifts: taps (p, q) with q >= s are served by B copy j = q / s
+    // of the slot for tap (p, q mod s) -- fewer, wider MMAs and 1/nq of the A
+    // operand to build.  Only while N = nq*4*Cout fits one MMA.
+    static const int force_nq1 = getenv("CAPSCONV_WG_NQ1") ? 1 : 0;
+    P.KWv = fc ? 1 : (int)p.KW;
+    P.nq = 1;
+    if (!fc && !force_nq1) {
+        const int nq = cdiv(p.KW, s);
+        if (nq > 1 && nq <= kWMaxNq && cdiv(nq * P.Cout * 4, 16) * 16 <= 256) P.nq = nq;
+    }
+    std::vector<int> stap;   // taps that own A slots
+    for (int t = 0; t < P.ntaps; ++t)
+        if (P.nq == 1 || t % P.KWv < s) stap.push_back(t);
+    const int nst = (int)stap.size();
+    P.N_tile = cdiv(P.nq * P.Cout * 4, 16) * 16;
     if (P.N_tile > 256) return pl;
     // ---- M tiles: slots (tap, channel range); channels in pairs (C odd -> padded slot rows)
     const int cpad = (P.C + 1) & ~1;
     std::vector<WTile> tiles;
     if (4 * cpad <= 128) {
         const int per = 128 / (4 * cpad);
-        for (int t0 = 0; t0 < P.ntaps; t0 += per) {
+        for (int t0 = 0; t0 < nst; t0 += per) {
             WTile T{};
-            T.nslots = std::min(per, P.ntaps - t0);
+            T.nslots = std::min(per, nst - t0);
             if (T.nslots > kWMaxSlots) return pl;
             T.c_lo = 0; T.c_hi = P.C;
             for (int j = 0; j < T.nslots; ++j) {
-                T.slot[j] = WSlot{t0 + j, tplane[t0 + j], tshift[t0 + j], 0, cpad, j * 4 * cpad, {}};
+                const int t = stap[t0 + j];
+                T.slot[j] = WSlot{t, tplane[t], tshift[t], 0, cpad, j * 4 * cpad, {}};
                 T.slot[j].fd_upp.init((uint32_t)(2 * cpad));
             }
             tiles.push_back(T);
         }
     } else {
-        for (int t = 0; t < P.ntaps; ++t)
+        for (int t : stap)
             for (int c0 = 0; c0 < P.C; c0 += 32) {
                 WTile T{};
                 T.nslots = 1;
@@ -839,10 +982,6 @@ WPlan make_wplan(const Problem &p) {
             if (force_kp ? KP != force_kp : KP > 64) continue;
             const uint32_t acc = (uint32_t)(TG * P.N_tile);
             const uint32_t abuf = (uint32_t)(2 * TG * KP);      // TG tiles x KP/4 k-steps x 8 columns
-            int ns = 0;
-            for (int n = 3; n >= 2; --n)
-                if (acc + n * abuf <= 512) { ns = n; break; }
-            if (!ns) continue;
             // rows mode: both parities of every virtual row the union window touches
             const int rows_mode_cap = 2 * ((KP + gmax_span + gmax_msh - 1) / P.Wg + 2) * P.Win;
             const int capI = P.batch_mode ? KP
@@ -850,7 +989,7 @@ WPlan make_wplan(const Problem &p) {
                              : P.I_rows   ? rows_mode_cap
                                           : ((KP + gmax_span - 1) / P.Wg + 2) * P.Wg;
             // dO: whole dO rows touched by the window
-            const int capO = P.batch_mode ? KP : ((KP - 1) / P.Wg + 2) * P.Wo;
+            const int capO = P.batch_mode ? KP : ((KP + P.nq - 2) / P.Wg + 2) * P.Wo;
             const uint32_t stgI_plane = (uint32_t)nbI * capI * P.CBI * 32;
             const uint32_t stgI = P.I_rows ? stgI_plane : (uint32_t)gmax_np * stgI_plane;
             const int TABW = KP + gmax_span;
@@ -858,8 +997,12 @@ WPlan make_wplan(const Problem &p) {
             const uint32_t stg = stgI + stgO;
             const uint32_t sbo = (uint32_t)KP * 64 + 16;
             const uint32_t bbytes = (uint32_t)(P.N_tile / 8) * sbo;
+            const uint32_t btab_off = P.I_rows ? 16u * TABW : 0u;
+            const uint32_t tab_stride = btab_off + (((uint32_t)(KP + P.nq) * 4u + 15u) & ~15u);
+            for (int ns = 3; ns >= 2 && !found; --ns)
             for (int nstg = 3; nstg >= 2 && !found; --nstg) {
-                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes + (P.I_rows ? 16 * TABW : 0);
+                if (acc + ns * abuf > 512) continue;   // TMEM: accumulators + ns A buffers
+                const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes + (uint64_t)nstg * tab_stride;
                 if (tot > kWSmemLimit) continue;
                 P.TG = TG; P.n_groups = ngroups;
                 P.KP = KP; P.capI = capI; P.capO = capO; P.stgI_plane = stgI_plane; P.stgI_bytes = stgI;
@@ -868,6 +1011,7 @@ WPlan make_wplan(const Problem &p) {
                 P.acc_cols = acc; P.abuf_cols = abuf;
                 P.TABW = TABW;
                 P.tab_off = 1024 + nstg * stg + ns * bbytes;
+                P.tab_stride = tab_stride; P.btab_off = btab_off;
                 if (P.I_rows) P.stgI_plane = 0;   // one staged region shared by all planes
                 found = true;
             }
@@ -887,6 +1031,8 @@ WPlan make_wplan(const Problem &p) {
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_uppO.init((uint32_t)(2 * P.Cout));
+    P.b_pstep = kWLoad / (2 * P.Cout);
+    if (P.b_pstep < 1) return WPlan{};
     const size_t nk = (size_t)P.ntaps * P.C * P.Cout * 16;
     pl.part_bytes = P.ksplit > 1 ? ((size_t)P.ksplit * nk * 4 + 255) & ~(size_t)255 : 0;
     pl.ok = true;
@@ -920,9 +1066,9 @@ const WPlan &cached_wplan(const Problem &p) {
         const WgradMma &P = pl.P;
         fprintf(stderr,
                 "[capsconv] wgrad plan: C=%d Cout=%d Hg=%d Wg=%d taps=%d mtiles=%d TG=%d groups=%d N_tile=%d KP=%d "
-                "ksplit=%d items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u acc=%u abuf=%u\n",
+                "ksplit=%d items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u acc=%u abuf=%u nq=%d\n",
                 P.C, P.Cout, P.Hg, P.Wg, P.ntaps, P.n_mtiles, P.TG, P.n_groups, P.N_tile, P.KP, P.ksplit, P.n_items,
-                P.capI, P.capO, P.nstg, P.nstages, P.smem_bytes, P.acc_cols, P.abuf_cols);
+                P.capI, P.capO, P.nstg, P.nstages, P.smem_bytes, P.acc_cols, P.abuf_cols, P.nq);
     }
     return pl;
 }

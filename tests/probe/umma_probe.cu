@@ -269,3 +269,71 @@ extern "C" int umma_probe_ts(const void *A, const void *B, float *D, int N, int 
     probe_ts<<<1, 128, 65536>>>((const __nv_bfloat16 *)A, (const __nv_bfloat16 *)B, D, N, K);
     return (int)cudaDeviceSynchronize();
 }
+
+// Variant of bench_kernel with wgrad's operand forms: B MN-major (LBO 128,
+// SBO = 8 k-rows... see wgrad.cu) or K-major, A from TMEM walking `a_step`
+// columns per MMA over 8 k-steps.  Returns cycles per MMA (CTA 0).
+__global__ void bench2_kernel(int N, int iters, int b_mn, int a_step, unsigned long long *cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar, done;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 65536 / 4; i += blockDim.x) ((uint32_t *)smem)[i] = 0x3c003c00u;
+    if (tid < 32) tmem_alloc<512>(&tmem_base);
+    if (tid == 0) { mbar_init(&bar, 1); mbar_init(&done, 1); mbar_fence_init(); }
+    fence_proxy_async_smem();
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tm = tmem_base;
+    if (tid >= 32) {
+        mbar_wait(&done, 0);   // spinning waiters (as the idle roles of a warp-specialised kernel)
+    } else {
+        const uint32_t idesc = idesc_bf16(128, N, 0, b_mn);
+        const uint32_t sb = smem_u32(smem);
+        // MN-major: n-groups of 8 at SBO = 128 * (k rows per stage = 128) ... use K=128 rows of 16 B per n-group
+        const uint64_t bd = b_mn ? smem_desc(sb, 128, 128 * 16) : smem_desc(sb, 256 * 16, 128);
+        unsigned long long t0 = clock64();
+        // a_step: 0 -> one A block; 8 -> 8 blocks; -1 -> 24 blocks, 3 accumulators (wgrad);
+        // -2 -> 24 blocks, one accumulator; -3 -> 8 blocks, 3 accumulators.  Constant offsets.
+        for (int it = 0; it < iters; it += 24) {
+            if (elect_one()) {
+#pragma unroll
+                for (int u = 0; u < 24; ++u) {
+                    uint32_t acol, dcol;
+                    if (a_step >= 0) { acol = 256 + (u % 8) * a_step; dcol = 0; }
+                    else if (a_step == -1) { acol = 128 + u * 8; dcol = (u / 8) * N; }
+                    else if (a_step == -2) { acol = 128 + u * 8; dcol = 0; }
+                    else { acol = 256 + (u % 8) * 8; dcol = (u / 8) * N; }
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tm + dcol),
+                        "r"(tm + acol), "l"(bd + (uint64_t)(b_mn ? (u % 8) * 16 : (u % 8) * 2)), "r"(idesc), "r"(1));
+                }
+            }
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(&bar);
+        __syncwarp();
+        mbar_wait(&bar, 0);
+        unsigned long long t1 = clock64();
+        if (blockIdx.x == 0 && tid == 0) *cycles = (t1 - t0);
+        if (tid == 0) mbar_arrive(&done);
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc<512>(tm);
+}
+
+extern "C" double umma_bench2(int N, int iters, int b_mn, int a_step, int nblocks, int nthreads) {
+    unsigned long long *d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(bench2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 32768);
+    bench2_kernel<<<nblocks, nthreads, 65536 + 32768>>>(N, iters, b_mn, a_step, d);
+    unsigned long long h = 0;
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return -1.0;
+    return (double)h / iters;
+}
