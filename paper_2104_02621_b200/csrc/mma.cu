@@ -260,7 +260,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
     const uint32_t stage_stride = P.a_stage_bytes + (P.b_resident ? 0u : P.b_stage_bytes);
     const uint32_t bres_addr = stage0 + P.nstages * stage_stride;
 
-    const int warp = threadIdx.x / 32;
+    // warp index broadcast from lane 0: role branches are then known to be
+    // warp-uniform and the MMA operands stay in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
     const int lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
@@ -283,11 +285,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
     constexpr int kEpiWarp0 = kProducerThreads / 32;
     constexpr int kMmaWarp = kEpiWarp0 + kEpilogueThreads / 32;
     constexpr int kTmaWarp = kMmaWarp + 1;
-    if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, P.tmem_cols);
+    // all 512 columns (one CTA per SM): the allocation then starts at column 0
+    if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, 512);
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
-    const uint32_t tmem = *tmem_slot;
+    if (*tmem_slot != 0u) __trap();
+    constexpr uint32_t tmem = 0u;   // constant base: no R2UR per MMA
 
     if (warp < kEpiWarp0) {
         // ================================================= producers
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
     __syncthreads();
     if (warp == kMmaWarp) {
         fence_after_sync();
-        tmem_dealloc_dyn(tmem, P.tmem_cols);
+        tmem_dealloc_dyn(tmem, 512);
     }
 }
 
