@@ -30,6 +30,7 @@ using namespace umma;
 namespace {
 
 constexpr int kMaxStages = 8;
+constexpr int kMaxStg = 4;     // staging buffers
 
 
 struct Item {
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
     uint64_t *acc_empty = acc_full + 2;
     uint64_t *b_res = acc_empty + 2;
     uint64_t *stg_full = b_res + 1;
-    uint64_t *stg_empty = stg_full + 2;
+    uint64_t *stg_empty = stg_full + kMaxStg;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem_raw + 512);
     const uint32_t stg0 = smem_u32(smem_raw) + 1024;
     const uint32_t stage0 = stg0 + P.nstg * P.stg_bytes;
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             mbar_init(acc_empty + i, kEpilogueThreads / 32);
         }
         mbar_init(b_res, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kMaxStg; ++i) {
             mbar_init(stg_full + i, 1);
             mbar_init(stg_empty + i, kProducerThreads);
         }
@@ -694,7 +695,17 @@ Plan make_plan(const Problem &p, bool dgrad) {
             if (force_cc && cc != force_cc) continue;
             const int nchunks = P.CSpad / cc;
             int ksplit = 1;
-            if (base_items < nsm && P.nog == 1) ksplit = std::min(nchunks, ceil_div(2 * nsm, base_items));
+            if (base_items < nsm && P.nog == 1) {
+                // split-K: at least ~2 items per SM, then the factor (up to 2x
+                // that) whose items fill the last wave best; ties -> fewer partials
+                const int ks0 = std::min(nchunks, ceil_div(2 * nsm, base_items));
+                double best_eff = -1.0;
+                for (int k = ks0; k <= std::min(nchunks, 2 * ks0); ++k) {
+                    const long long it = base_items * k;
+                    const double eff = (double)it / (double)(ceil_div(it, nsm) * nsm);
+                    if (eff > best_eff + 1e-9) { best_eff = eff; ksplit = k; }
+                }
+            }
             if (2 * G * P.N_tile > 512) continue;
             const long long items = (long long)P.nog * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
             if (G > 1 && items < 2 * nsm && !force_g) continue;
@@ -719,8 +730,11 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const uint32_t stg = rows_mode ? stg_plane : (uint32_t)P.npl * stg_plane;
             const uint32_t tab_bytes = rows_mode ? (uint32_t)(P.npl * win_px * 4 + 15) & ~15u : 0u;
             int best_st = 0, best_nstg = 0;
-            for (int nstg = 2; nstg >= 1 && !best_st; --nstg)
-                for (int st = std::min(kMaxStages, 4); st >= (nstg == 2 ? 2 : 3); --st) {
+            // batch mode (fully-connected view) is a streaming GEMM: deeper
+            // staging keeps more HBM bytes in flight per SM
+            const int max_nstg = batch_mode ? kMaxStg : 2;
+            for (int nstg = max_nstg; nstg >= 1 && !best_st; --nstg)
+                for (int st = std::min(kMaxStages, 4); st >= (nstg >= 2 ? 2 : 3); --st) {
                     const uint64_t bytes = 1024 + (uint64_t)nstg * stg + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) +
                                            (bres ? b_stage : 0) + tab_bytes;
                     if (bytes <= kSmemLimit) { best_st = st; best_nstg = nstg; break; }

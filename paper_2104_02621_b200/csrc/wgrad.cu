@@ -122,8 +122,11 @@ struct WgradMma {
 __device__ __forceinline__ void wdecode(const WgradMma &P, int item, int &mt, int &ks, int &p0, int &p1) {
     ks = item % P.ksplit;
     mt = item / P.ksplit;                  // group index
-    p0 = ks * P.kpix;
-    p1 = min(P.vtotal, p0 + P.kpix);
+    // balanced split of the nst = ceil(vtotal / KP) stages: split ks owns
+    // stages [ks*nst/ksplit, (ks+1)*nst/ksplit)
+    const int nst = (P.vtotal + P.KP - 1) / P.KP;
+    p0 = (int)((long long)ks * nst / P.ksplit) * P.KP;
+    p1 = min(P.vtotal, (int)((long long)(ks + 1) * nst / P.ksplit) * P.KP);
 }
 
 // Rows mode: the window [v0, v0 + len) as whole virtual rows; returns the
@@ -1023,9 +1026,8 @@ WPlan make_wplan(const Problem &p) {
     const int nstage_total = cdiv(P.vtotal, P.KP);
     // one item per CTA: fewer fp32 partials for the finalize pass to read
     int ks = std::max(1, std::min(nstage_total, nsm / std::max(1, P.n_groups)));
-    const int stages_per = cdiv(nstage_total, ks);
-    P.kpix = stages_per * P.KP;
-    P.ksplit = cdiv(P.vtotal, P.kpix);
+    P.kpix = cdiv(nstage_total, ks) * P.KP;   // longest split (informational)
+    P.ksplit = ks;
     P.n_items = P.n_groups * P.ksplit;
     P.tmem_cols = 512;
     P.fd_Wg.init((uint32_t)P.Wg);
