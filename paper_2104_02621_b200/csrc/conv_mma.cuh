@@ -84,6 +84,8 @@ struct ConvMma {
     int og_t0[4], og_t1[4];
     int og_oy[4], og_ox[4];
     int og_offmin[4];          // min tap shift of the group
+    int gpi;                   // output groups per work item (1, or nog: one staged window for all phases)
+    int ib_offmin[4];          // window offset of the item block starting at group g (min shift over its groups)
     int out_H, out_W, NCH;
     // ---- tiling
     int N_tile, n_ntiles;

@@ -45,7 +45,7 @@ __device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
     it.ks = r % P.ksplit; r /= P.ksplit;
     it.nt = r % P.n_ntiles; r /= P.n_ntiles;
     it.ig = r % P.n_igroups;
-    it.g = r / P.n_igroups;
+    it.g = (r / P.n_igroups) * P.gpi;   // first output group of the item
     it.tile0 = it.ig * P.G;
     it.ntl = min(P.G, P.n_mtiles - it.tile0);
     it.c_begin = it.ks * P.nchunks / P.ksplit;
@@ -65,7 +65,7 @@ __device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
 // Window of virtual pixels [v0, v0 + len) of the current item; with the
 // staging layout of whole virtual rows the window starts `off` pixels in.
 __device__ __forceinline__ int window_v0(const ConvMma &P, const Item &it) {
-    return it.tile0 * kTilePix + P.og_offmin[it.g];
+    return it.tile0 * kTilePix + P.ib_offmin[it.g];
 }
 __device__ __forceinline__ int staging_off(const ConvMma &P, int v0) {
     return P.stg_batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
@@ -210,8 +210,8 @@ __device__ __forceinline__ void repack_window(const ConvMma &P, const Item &it, 
         const uint4 v = ld_shared_v4(stg + k * P.stg_plane_bytes + (uint32_t)(vl + off) * px_bytes + (uint32_t)u2 * 16u);
         const uint32_t dst = a_stage + k * P.plane_bytes + (c >> 1) * P.a_lbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
                              (c & 1) * 8u;
-        st_shared_v2(dst, v.x, v.y);          // row d1 = 2i
-        st_shared_v2(dst + 16u, v.z, v.w);    // row d1 = 2i + 1
+        st_shared_v2(dst, v.x, v.y);
+        st_shared_v2(dst + 16u, v.z, v.w);
     }
 }
 
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         // ================================================= producers
         const int tid = threadIdx.x;
         if (P.b_resident && tid == 0) {
-            const uint32_t bytes = (uint32_t)(P.og_t1[0] - P.og_t0[0]) * (P.CC / 2) * P.N_tile * 16;
+            const uint32_t bytes = (uint32_t)(P.og_t1[P.gpi - 1] - P.og_t0[0]) * (P.CC / 2) * P.N_tile * 16;
             mbar_arrive_expect_tx(b_res, bytes);
             bulk_g2s_u32(bres_addr, P.wpack, bytes, b_res);
         }
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 mbar_wait(a_empty + stage, phase ^ 1);
                 const uint32_t a_stage = stage0 + stage * stage_stride;
                 if (!P.b_resident && tid == 0) {
-                    const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
+                    const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g + P.gpi - 1];
                     const size_t blk = (size_t)(P.CC / 2) * P.N_tile * 16;
                     const size_t off = (((size_t)it.nt * P.nchunks + ch) * P.ntaps + t0) * blk;
                     const uint32_t bytes = (uint32_t)((t1 - t0) * blk);
@@ -354,7 +354,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             mbar_wait(acc_full + abuf, aphase);
             if (row == 0) TRACE(2, ii, 1);
             fence_after_sync();
-            for (int gi = ehalf; gi < ((P.dbg & 32) ? 0 : it.ntl); gi += 2) {
+            const int nq_epi = (P.dbg & 32) ? 0 : P.gpi * it.ntl;
+            for (int qi = ehalf; qi < nq_epi; qi += 2) {
+                const int gg = qi / it.ntl, gi = qi - gg * it.ntl;   // output group, tile
+                const int g = it.g + gg;
                 const int u = (it.tile0 + gi) * kTilePix + (row >> 2);
                 const int d1 = row & 3;
                 bool valid = u < vtotal;
@@ -364,12 +367,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     const uint32_t rr = (uint32_t)u - b * HgWg;
                     const uint32_t Y = P.fd_Wg.div(rr);
                     const uint32_t X = rr - Y * (uint32_t)P.Wg;
-                    const int oy = P.og_s * (int)Y + P.og_oy[it.g];
-                    const int ox = P.og_s * (int)X + P.og_ox[it.g];
+                    const int oy = P.og_s * (int)Y + P.og_oy[g];
+                    const int ox = P.og_s * (int)X + P.og_ox[g];
                     valid = oy < P.out_H && ox < P.out_W;
                     opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
                 }
-                const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)((abuf * P.G + gi) * P.N_tile);
+                const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(((abuf * P.gpi + gg) * P.G + gi) * P.N_tile);
                 for (int n0 = 0; n0 < P.N_tile; n0 += 32) {
                     float va[16], vb[16];
                     const bool two = n0 + 16 < P.N_tile;
@@ -433,8 +436,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             mbar_wait(acc_empty + abuf, aphase ^ 1);
             if (lane == 0) TRACE(1, ii, 1);
             fence_after_sync();
-            const int t0 = P.og_t0[it.g], t1 = P.og_t1[it.g];
-            const int offmin = P.og_offmin[it.g];
+            const int T0 = P.og_t0[it.g];
+            const int offmin = P.ib_offmin[it.g];
             for (int ch = it.c_begin; ch < it.c_end; ++ch) {
                 mbar_wait(a_full + stage, phase);
                 if (!P.b_resident) mbar_wait(b_full + stage, phase);
@@ -447,18 +450,20 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 // bits, so a byte offset is added as (offset >> 4).
                 const uint64_t a_desc0 = smem_desc(a_stage, P.a_lbo, 128);
                 const uint64_t b_desc0 = smem_desc(b_base, b_lbo, 128);
-                const uint32_t d0 = tmem + (uint32_t)(abuf * P.G * P.N_tile);
                 const int ksteps = P.CC / 4;
                 if (elect_one()) {
                     if (!(P.dbg & 2))
-                    for (int t = t0; t < t1; ++t) {
+                    for (int gg = 0; gg < P.gpi; ++gg) {
+                    const int g = it.g + gg;
+                    const uint32_t d0 = tmem + (uint32_t)((abuf * P.gpi + gg) * P.G * P.N_tile);
+                    for (int t = P.og_t0[g]; t < P.og_t1[g]; ++t) {
                         const uint64_t a_tap = a_desc0 + ((P.tap_plane[t] * P.plane_bytes +
                                                            (uint32_t)(P.tap_shift[t] - offmin) * 64u) >> 4);
-                        const uint64_t b_tap = b_desc0 + (((t - t0) * (P.CC / 2) * b_lbo) >> 4);
+                        const uint64_t b_tap = b_desc0 + (((t - T0) * (P.CC / 2) * b_lbo) >> 4);
                         for (int j = 0; j < ksteps; ++j) {
                             const uint64_t bd = b_tap + ((2u * j * b_lbo) >> 4);
                             const uint64_t aj = a_tap + ((2u * j * P.a_lbo) >> 4);
-                            const uint32_t acc = (ch != it.c_begin || t != t0 || j != 0) ? 1u : 0u;
+                            const uint32_t acc = (ch != it.c_begin || t != P.og_t0[g] || j != 0) ? 1u : 0u;
                             uint32_t d = d0;
                             uint64_t ad = aj;
                             for (int gi = 0; gi < it.ntl; ++gi) {
@@ -467,6 +472,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                                 ad += (kTilePix * 64) >> 4;
                             }
                         }
+                    }
                     }
                     mma_commit(a_empty + stage);
                 }
@@ -669,6 +675,15 @@ Plan make_plan(const Problem &p, bool dgrad) {
         max_taps_g = std::max(max_taps_g, t1 - t0);
         max_span = std::max(max_span, mx - mn);
     }
+    // all output groups in one item (stride-2 dI): one staged window covering
+    // every group's taps, nog accumulator sets
+    int span_all = 0, offmin_all = 1 << 30;
+    {
+        int mx = -(1 << 30);
+        for (int t = 0; t < P.ntaps; ++t) { offmin_all = std::min(offmin_all, tshift[t]); mx = std::max(mx, tshift[t]); }
+        span_all = mx - offmin_all;
+    }
+    static const int no_merge = getenv("CAPSCONV_NO_MERGE") ? 1 : 0;
     const long long vtotal = (long long)P.Bn * P.Hg * P.Wg;
     if (vtotal * 4 >= (1ll << 31) || (long long)P.src_H * P.src_W * P.Bn >= (1ll << 31)) return pl;
 
@@ -688,6 +703,10 @@ Plan make_plan(const Problem &p, bool dgrad) {
     ConvMma best;
     long long best_score = -1;
     static const int force_g = getenv("CAPSCONV_FORCE_G") ? atoi(getenv("CAPSCONV_FORCE_G")) : 0;
+    const int gpis[2] = {P.nog, 1};
+    for (int gq = (P.nog > 1 && !no_merge) ? 0 : 1; gq < 2; ++gq) {
+    const int gpi = gpis[gq];
+    if (gq == 1 && found) break;   // merged plan found: keep it
     for (int G : {8, 4, 2, 1}) {
         if (force_g && G != force_g) continue;
         for (int cc : ccs) {
@@ -706,18 +725,19 @@ Plan make_plan(const Problem &p, bool dgrad) {
                     if (eff > best_eff + 1e-9) { best_eff = eff; ksplit = k; }
                 }
             }
-            if (2 * G * P.N_tile > 512) continue;
-            const long long items = (long long)P.nog * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
+            if (2 * gpi * G * P.N_tile > 512) continue;
+            const long long items = (long long)(P.nog / gpi) * P.n_ntiles * ceil_div(P.n_mtiles, G) * ksplit;
             if (G > 1 && items < 2 * nsm && !force_g) continue;
-            const int win_px = ((G * kTilePix + max_span) + 1) & ~1;
+            const int span = gpi > 1 ? span_all : max_span;
+            const int win_px = ((G * kTilePix + span) + 1) & ~1;
             // k-chunk planes staggered by 16 bytes mod 128: the repack's 8-byte
             // stores of a warp (lanes = (pixel, c, i) units) then hit every
             // bank exactly twice -- two wavefronts, the minimum for 256 bytes
             const uint32_t a_lbo = (uint32_t)win_px * 64 + 16;
             const uint32_t plane = (uint32_t)(cc / 2) * a_lbo;
             const uint32_t a_stage = (uint32_t)P.npl * plane;
-            const uint32_t b_stage = (uint32_t)max_taps_g * (cc / 2) * P.N_tile * 16;
-            const bool bres = (P.nog == 1 && nchunks == 1 && P.n_ntiles == 1);
+            const uint32_t b_stage = (uint32_t)(gpi > 1 ? P.ntaps : max_taps_g) * (cc / 2) * P.N_tile * 16;
+            const bool bres = (gpi == P.nog && nchunks == 1 && P.n_ntiles == 1);
             // staging of the natural layout (whole virtual rows, or BB-image boxes)
             const bool batch_mode = (P.Hg * P.Wg == 1);
             const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1;
@@ -745,7 +765,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
             P.I_rows = rows_mode ? 1 : 0;
             P.Hin = (int)p.H; P.Win = (int)p.W; P.Bin = (int)p.B;
             if (a_lbo >= (1u << 18) || b_stage >= (1u << 20)) continue;
-            P.CC = cc; P.nchunks = nchunks; P.ksplit = ksplit; P.G = G;
+            P.CC = cc; P.nchunks = nchunks; P.ksplit = ksplit; P.G = G; P.gpi = gpi;
             P.win_px = win_px; P.a_lbo = a_lbo; P.plane_bytes = plane;
             P.a_stage_bytes = a_stage; P.b_stage_bytes = b_stage;
             P.b_resident = bres ? 1 : 0; P.nstages = best_st;
@@ -763,12 +783,14 @@ Plan make_plan(const Problem &p, bool dgrad) {
             found = true;
         }
     }
+    }
     if (!found) return pl;
     P = best;
+    for (int g = 0; g < P.nog; ++g) P.ib_offmin[g] = P.gpi > 1 ? offmin_all : P.og_offmin[g];
     P.n_igroups = ceil_div(P.n_mtiles, P.G);
-    P.n_items = P.nog * P.n_igroups * P.n_ntiles * P.ksplit;
+    P.n_items = (P.nog / P.gpi) * P.n_igroups * P.n_ntiles * P.ksplit;
     uint32_t cols = 32;
-    while (cols < (uint32_t)(2 * P.G * P.N_tile)) cols <<= 1;
+    while (cols < (uint32_t)(2 * P.gpi * P.G * P.N_tile)) cols <<= 1;
     P.tmem_cols = cols;
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
@@ -874,10 +896,10 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
         fprintf(stderr,
                 "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
                 "nchunks=%d ksplit=%d G=%d mtiles=%d items=%d win_px=%d stages=%d bres=%d smem=%u tmem=%u nstg=%d "
-                "stg_cap=%d batch=%d\n",
+                "stg_cap=%d batch=%d gpi=%d\n",
                 dgrad ? "dgrad" : "fwd", P.CS, P.NCH, P.Hg, P.Wg, P.npl, P.nog, P.ntaps, P.N_tile, P.n_ntiles, P.CC,
                 P.nchunks, P.ksplit, P.G, P.n_mtiles, P.n_items, P.win_px, P.nstages, P.b_resident, P.smem_bytes,
-                P.tmem_cols, P.nstg, P.stg_cap_px, P.stg_batch_mode);
+                P.tmem_cols, P.nstg, P.stg_cap_px, P.stg_batch_mode, P.gpi);
     }
     return pl;
 }
