@@ -814,13 +814,27 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     }
 }
 
+// Split-K partials -> dK, deterministic: a block of 256 threads is E = 256/nsl
+// elements x nsl slices of the split range (nsl in {1, 2, 4, 8}, more slices
+// for longer splits); each thread sums its slice in order, the slice sums are
+// then added in slice order (a fixed summation tree for every launch).
 __global__ void __launch_bounds__(256) w_finalize(const float *__restrict__ part, float *__restrict__ dK, int64_t n,
-                                                  int ksplit) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                                                  int ksplit, int nsl) {
+    __shared__ float red[256];
+    const int E = 256 / nsl;
+    const int el = threadIdx.x % E, sl = threadIdx.x / E;
+    const int64_t i = (int64_t)blockIdx.x * E + el;
+    const int k0 = sl * ksplit / nsl, k1 = (sl + 1) * ksplit / nsl;
     float acc = 0.f;
-    for (int k = 0; k < ksplit; ++k) acc += part[(int64_t)k * n + i];
-    dK[i] = acc;
+    if (i < n)
+        for (int k = k0; k < k1; ++k) acc += part[(int64_t)k * n + i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (sl == 0 && i < n) {
+        float t = red[el];
+        for (int j = 1; j < nsl; ++j) t += red[j * E + el];
+        dK[i] = t;
+    }
 }
 
 // ------------------------------------------------------------------ planning
@@ -1133,7 +1147,9 @@ cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK
     }
     if (P.ksplit > 1) {
         const int64_t n = (int64_t)P.ntaps * P.C * P.Cout * 16;
-        w_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P.part, dK, n, P.ksplit);
+        const int nsl = P.ksplit >= 64 ? 8 : P.ksplit >= 32 ? 4 : P.ksplit >= 16 ? 2 : 1;
+        const int64_t E = 256 / nsl;
+        w_finalize<<<(unsigned)((n + E - 1) / E), 256, 0, st>>>(P.part, dK, n, P.ksplit, nsl);
         note_launches(1);
     }
     return cudaGetLastError();
