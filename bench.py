@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce on the compute stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
     return ap.parse_args()
 
 
@@ -151,6 +152,34 @@ class CallTimer:
             out.setdefault(key, []).append(a.elapsed_time(b))
         self.pending = []
         return out
+
+
+class GraphCallTimer:
+    """The same per-call events, recorded while the step is captured into a
+    CUDA graph (external events become event-record nodes, so every replay
+    re-records them); collect() reads the last replay's durations."""
+
+    def __init__(self):
+        self.ev = {}
+        self.order = []
+
+    def _pair(self, key):
+        if key not in self.ev:
+            self.ev[key] = (torch.cuda.Event(enable_timing=True, external=True),
+                            torch.cuda.Event(enable_timing=True, external=True))
+            self.order.append(key)
+        return self.ev[key]
+
+    def begin(self, li, kind):
+        self._pair((li, kind))[0].record()
+
+    def end(self, li, kind):
+        self._pair((li, kind))[1].record()
+
+    def collect_into(self, out):
+        for key in self.order:
+            a, b = self.ev[key]
+            out.setdefault(key, []).append(a.elapsed_time(b))
 
 
 def pass_bytes(st, li, kind, elem):
@@ -295,6 +324,28 @@ def main():
         st.step(X, dY)
     torch.cuda.synchronize()
 
+    # The timed step is one CUDA-graph replay of the whole step (every kernel
+    # of every pass; the graph removes host launch gaps between them).  The
+    # per-call events are captured with it; launches are counted at capture.
+    use_graph = not args.eager
+    gtimer = GraphCallTimer() if use_graph else None
+    launches_per_step = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        cap_stream = torch.cuda.Stream(dev)
+        cap_stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cap_stream):
+            st.step(X, dY)                      # warm the capture stream's workspace
+        torch.cuda.synchronize()
+        c0 = pkg.launch_count()
+        with torch.cuda.graph(graph, stream=cap_stream):
+            st.step(X, dY, timer=gtimer)
+        launches_per_step = pkg.launch_count() - c0
+        torch.cuda.synchronize()
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+
     timer = CallTimer()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -302,16 +353,23 @@ def main():
     torch.cuda.synchronize()
     n0 = pkg.launch_count()
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        gcalls = {}
         for i in range(args.steps):
             flush.zero_()
             starts[i].record()
-            st.step(X, dY, timer=timer)
+            if use_graph:
+                graph.replay()
+            else:
+                st.step(X, dY, timer=timer)
             ends[i].record()
+            if use_graph:                       # read this replay's per-call events
+                torch.cuda.synchronize()
+                gtimer.collect_into(gcalls)
         torch.cuda.synchronize()
         barrier()
-    launches = pkg.launch_count() - n0
+    launches = launches_per_step * args.steps if use_graph else pkg.launch_count() - n0
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
-    calls = timer.collect()
+    calls = gcalls if use_graph else timer.collect()
     ms = sum(step_ms) / len(step_ms)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -437,7 +495,9 @@ def main():
                        "layers": ["%dx%d s%d %d->%d" % (s.KH, s.KW, s.stride, s.C, s.Cout) for s in specs],
                        "input": "%dx%dx%d capsules %dx%d" % (H, W, specs[0].C, D, D),
                        "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
-                       "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None},
+                       "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None,
+                       "launch": ("one CUDA-graph replay of the captured step (%d libcapsconv kernels)" % launches_per_step)
+                       if use_graph else "eager launches"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

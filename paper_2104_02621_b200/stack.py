@@ -61,9 +61,12 @@ class CapsStack:
         for sp in self.specs:
             h, w = self.hw[-1]
             self.hw.append(ops.output_dims(h, w, sp.KH, sp.KW, sp.stride))
-        # static buffers (stable pointers: the step can be captured in a CUDA graph)
+        # static buffers (stable pointers: the step can be captured in a CUDA graph).
+        # acts[0] is the caller's input itself when it already has the layer-0
+        # layout (no copy); the static buffer is only used otherwise.
         self.acts = [torch.empty((batch, h, w, sp.C, D, D), dtype=self.dtype, device=self.device)
                      for (h, w), sp in zip(self.hw[:-1], self.specs)]
+        self._acts0 = self.acts[0]
         last = self.specs[-1]
         h, w = self.hw[-1]
         self.out = torch.empty((batch, h, w, last.Cout, D, D), dtype=self.dtype, device=self.device)
@@ -87,8 +90,16 @@ class CapsStack:
         return 3 * sum(self.layer_flops(i, batch) for i in range(len(self.specs)))
 
     # ------------------------------------------------------------ one step
+    def _bind_input(self, x: torch.Tensor):
+        a0 = self._acts0
+        if x.device == a0.device and x.dtype == a0.dtype and x.shape == a0.shape and x.is_contiguous():
+            self.acts[0] = x            # read in place (forward input and layer-0 dK operand)
+        else:
+            a0.copy_(x)
+            self.acts[0] = a0
+
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        self.acts[0].copy_(x)
+        self._bind_input(x)
         for li, sp in enumerate(self.specs):
             dst = self.acts[li + 1] if li + 1 < len(self.specs) else self.out
             self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst)
@@ -123,7 +134,7 @@ class CapsStack:
         if timer is None:
             self.forward(x)
             return self.backward(dy)
-        self.acts[0].copy_(x)
+        self._bind_input(x)
         for li, sp in enumerate(self.specs):
             dst = self.acts[li + 1] if li + 1 < len(self.specs) else self.out
             timer.begin(li, "fwd")
