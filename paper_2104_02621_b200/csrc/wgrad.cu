@@ -112,6 +112,9 @@ struct WgradMma {
     // of a slot for tap (p, q) is the gradient of tap (p, q + s*j)
     int nq, KWv;
     int b_pstep;                           // staged dO pixels per B-loader iteration (loader threads / (2*Cout))
+    // bdesc: B holds ONE dO copy over KP + nq - 1 pixels; copy j is the same
+    // buffer at descriptor offset (nq-1-j) pixels (64 B), one N = 4*Cout MMA per copy
+    int bdesc;
     int Ho, Wo;                            // dO extents (rows per image, pixels per row)
 };
 #define WTRACE(role, idx, ev)                                                              \
@@ -303,6 +306,19 @@ __device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32
     for (int j = 0; j < kWMaxNq; ++j) {
         const int col = j * P.Cout + c;
         dcol[j] = b + (uint32_t)(col >> 1) * P.b_sbo + (uint32_t)(2 * i) * 16u + (col & 1) * 8u;
+    }
+    if (P.bdesc) {
+#pragma unroll 4
+        for (int e = pix0; e < npx; e += P.b_pstep) {
+            int idx;
+            asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(btab + (uint32_t)e * 4u));
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (idx >= 0) v = ld_shared_v4(base + (uint32_t)idx * pxb + src_off);
+            const uint32_t dst = dcol[0] + (uint32_t)e * 64u;
+            st_shared_v2(dst, v.x, v.y);
+            st_shared_v2(dst + 16u, v.z, v.w);
+        }
+        return;
     }
 #pragma unroll 4
     for (int e = pix0; e < npx; e += P.b_pstep) {
@@ -710,6 +726,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
         }
     } else if (warp == kMma) {
         const uint32_t idesc = idesc_bf16(128, P.N_tile, 0, 1);
+        const uint32_t idesc_sub = idesc_bf16(128, P.Cout * 4, 0, 1);
         int st = 0, abuf = 0;
         uint32_t ph = 0, aph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
@@ -727,8 +744,35 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 fence_after_sync();
                 const uint64_t bd0 = smem_desc(op0 + st * P.b_bytes, 128, P.b_sbo);
                 const uint32_t a0 = tmem + P.acc_cols + (uint32_t)st * P.abuf_cols;
-                // the warp stays converged; one elected lane issues 4 MMAs at a
-                // time (a long divergent single-lane loop issues far slower)
+                // the warp stays converged; one elected lane issues 4 k-steps at
+                // a time (a long divergent single-lane loop issues far slower)
+                if (P.bdesc) {
+                    const int nsub = P.Cout * 4;
+                    for (int tt = 0; tt < ntl; ++tt) {
+                        const uint32_t d = tmem + (uint32_t)(tt * P.N_tile);
+                        for (int k4 = 0; k4 < nk; k4 += 4) {
+                            if (elect_one()) {
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int kk = k4 + u;
+#pragma unroll
+                                    for (int j = 0; j < kWMaxNq; ++j) {
+                                        if (j < P.nq) {
+                                            asm volatile(
+                                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(
+                                                    d + (uint32_t)(j * nsub)),
+                                                "r"(a0 + (uint32_t)((tt * nk + kk) * 8)),
+                                                "l"(bd0 + (uint64_t)((P.nq - 1 - j) * 4 + kk * 16)), "r"(idesc_sub),
+                                                "r"((first && kk == 0) ? 0u : 1u));
+                                        }
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    }
+                } else
                 for (int tt = 0; tt < ntl; ++tt) {
                     const uint32_t d = tmem + (uint32_t)(tt * P.N_tile);
                     for (int k4 = 0; k4 < nk; k4 += 4) {
@@ -849,7 +893,7 @@ struct WPlan {
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 constexpr uint32_t kWSmemLimit = 227 * 1024;
 
-WPlan make_wplan(const Problem &p) {
+WPlan make_wplan(const Problem &p, bool allow_nq) {
     WPlan pl;
     WgradMma &P = pl.P;
     if (p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return pl;
@@ -895,20 +939,29 @@ WPlan make_wplan(const Problem &p) {
     P.vtotal = (int)vt;
     // ---- column shifts: taps (p, q) with q >= s are served by B copy j = q / s
     // of the slot for tap (p, q mod s) -- fewer, wider MMAs and 1/nq of the A
-    // operand to build.  Only while N = nq*4*Cout fits one MMA.
+    // operand to build.  bdesc: one B copy, the shifts are
+    // descriptor offsets and each copy is its own N = 4*Cout MMA (the
+    // accumulators, nq*4*Cout columns per tile, only have to fit TMEM);
+    // otherwise the copies are materialised side by side in one N <= 256 MMA.
     static const int force_nq1 = getenv("CAPSCONV_WG_NQ1") ? 1 : 0;
+    static const int bdesc_env = getenv("CAPSCONV_WG_BDESC") ? atoi(getenv("CAPSCONV_WG_BDESC")) : -1;
     P.KWv = fc ? 1 : (int)p.KW;
     P.nq = 1;
-    if (!fc && !force_nq1) {
+    P.bdesc = 0;
+    if (!fc && !force_nq1 && allow_nq) {
         const int nq = cdiv(p.KW, s);
-        if (nq > 1 && nq <= kWMaxNq && cdiv(nq * P.Cout * 4, 16) * 16 <= 256) P.nq = nq;
+        const bool bd = (P.Cout * 4) % 16 == 0 && P.Cout * 4 <= 256 && bdesc_env != 0;
+        if (nq > 1 && nq <= kWMaxNq && (bd ? nq * P.Cout * 4 <= 384 : cdiv(nq * P.Cout * 4, 16) * 16 <= 256)) {
+            P.nq = nq;
+            P.bdesc = bd ? 1 : 0;
+        }
     }
     std::vector<int> stap;   // taps that own A slots
     for (int t = 0; t < P.ntaps; ++t)
         if (P.nq == 1 || t % P.KWv < s) stap.push_back(t);
     const int nst = (int)stap.size();
     P.N_tile = cdiv(P.nq * P.Cout * 4, 16) * 16;
-    if (P.N_tile > 256) return pl;
+    if (P.N_tile > (P.bdesc ? 384 : 256)) return pl;
     // ---- M tiles: slots (tap, channel range); channels in pairs (C odd -> padded slot rows)
     const int cpad = (P.C + 1) & ~1;
     std::vector<WTile> tiles;
@@ -1012,8 +1065,8 @@ WPlan make_wplan(const Problem &p) {
             const int TABW = KP + gmax_span;
             const uint32_t stgO = (uint32_t)capO * P.Cout * 32;
             const uint32_t stg = stgI + stgO;
-            const uint32_t sbo = (uint32_t)KP * 64 + 16;
-            const uint32_t bbytes = (uint32_t)(P.N_tile / 8) * sbo;
+            const uint32_t sbo = (uint32_t)(P.bdesc ? KP + P.nq - 1 : KP) * 64 + 16;
+            const uint32_t bbytes = (uint32_t)((P.bdesc ? P.Cout * 4 : P.N_tile) / 8) * sbo;
             const uint32_t btab_off = P.I_rows ? 16u * TABW : 0u;
             const uint32_t tab_stride = btab_off + (((uint32_t)(KP + P.nq) * 4u + 15u) & ~15u);
             for (int ns = 3; ns >= 2 && !found; --ns)
@@ -1076,15 +1129,17 @@ const WPlan &cached_wplan(const Problem &p) {
     for (auto &kv : cache)
         if (kv.first == k) return kv.second;
     if (cache.size() > 256) cache.clear();
-    cache.emplace_back(k, make_wplan(p));
+    WPlan w = make_wplan(p, true);
+    if (!w.ok) w = make_wplan(p, false);   // column shifts do not fit TMEM/smem: one tap per slot
+    cache.emplace_back(k, w);
     const WPlan &pl = cache.back().second;
     if (getenv("CAPSCONV_DEBUG") && pl.ok) {
         const WgradMma &P = pl.P;
         fprintf(stderr,
                 "[capsconv] wgrad plan: C=%d Cout=%d Hg=%d Wg=%d taps=%d mtiles=%d TG=%d groups=%d N_tile=%d KP=%d "
-                "ksplit=%d items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u acc=%u abuf=%u nq=%d\n",
+                "ksplit=%d items=%d capI=%d capO=%d nstg=%d stages=%d smem=%u acc=%u abuf=%u nq=%d bdesc=%d\n",
                 P.C, P.Cout, P.Hg, P.Wg, P.ntaps, P.n_mtiles, P.TG, P.n_groups, P.N_tile, P.KP, P.ksplit, P.n_items,
-                P.capI, P.capO, P.nstg, P.nstages, P.smem_bytes, P.acc_cols, P.abuf_cols, P.nq);
+                P.capI, P.capO, P.nstg, P.nstages, P.smem_bytes, P.acc_cols, P.abuf_cols, P.nq, P.bdesc);
     }
     return pl;
 }
