@@ -115,6 +115,10 @@ struct WgradMma {
     // bdesc: B holds ONE dO copy over KP + nq - 1 pixels; copy j is the same
     // buffer at descriptor offset (nq-1-j) pixels (64 B), one N = 4*Cout MMA per copy
     int bdesc;
+    // loader groups: stage s is built by group s % lgroups (lgroups divides nstg
+    // and nstages, so every buffer always belongs to one group); the groups
+    // work on different stages concurrently
+    int lgroups;
     int Ho, Wo;                            // dO extents (rows per image, pixels per row)
 };
 #define WTRACE(role, idx, ev)                                                              \
@@ -264,12 +268,12 @@ __device__ __forceinline__ uint32_t w_issue(const WgradMma &P, const WGroup &G, 
 
 // B source table: entry e (0 <= e < KP + nq - 1) = staged dO pixel of
 // virtual pixel v0 - (nq - 1) + e, or -1 (outside dO: a zero row of B)
-__device__ __forceinline__ void w_build_btab(const WgradMma &P, int v0, uint32_t btab, int tid) {
+__device__ __forceinline__ void w_build_btab(const WgradMma &P, int v0, uint32_t btab, int tid, int nthr) {
     int ra, rb;
     w_dO_rows(P, v0, ra, rb);
     const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
     const int n = P.KP + P.nq - 1;
-    for (int e = tid; e < n; e += kWLoad) {
+    for (int e = tid; e < n; e += nthr) {
         const int vv = v0 - (P.nq - 1) + e;
         int idx = -1;
         if (vv >= 0 && vv < P.vtotal) {
@@ -359,10 +363,10 @@ __device__ __forceinline__ void transpose4x4(uint32_t &lo, uint32_t &hi, int r) 
 // Transpose every staged input capsule in place (rows d1 -> columns d2), once
 // per stage, so the per-slot loads below are plain 8-byte reads of a column.
 // Lane groups of 4 own one 32-byte capsule.
-__device__ __forceinline__ void w_transpose_stage(uint32_t base, uint32_t bytes, int tid) {
+__device__ __forceinline__ void w_transpose_stage(uint32_t base, uint32_t bytes, int tid, int nthr) {
     const int lane = tid & 31;
     const uint32_t n8 = bytes / 8;                      // 8-byte rows
-    constexpr uint32_t kStep = (uint32_t)kWLoad;
+    const uint32_t kStep = (uint32_t)nthr;
     constexpr int kU = 4;                               // independent rows in flight per lane
     // all lanes of a warp iterate together (shuffles need the full warp)
     for (uint32_t r0 = (uint32_t)(tid - lane); r0 < n8; r0 += kU * kStep) {
@@ -456,7 +460,8 @@ __device__ __forceinline__ void w_lane_setup(const WgradMma &P, int g, int q, in
 
 // Rows mode: table[k][w] = staged pixel of plane k's window position w
 // (window of plane k starts at v0 + minsh_k), -1 outside the input.
-__device__ __forceinline__ void w_build_table(const WgradMma &P, const WGroup &G, int v0, uint32_t tab, int tid) {
+__device__ __forceinline__ void w_build_table(const WgradMma &P, const WGroup &G, int v0, uint32_t tab, int tid,
+                                              int nthr) {
     int wlo = 1 << 30, whi = -1;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -464,7 +469,7 @@ __device__ __forceinline__ void w_build_table(const WgradMma &P, const WGroup &G
     int rA, rB;
     w_in_rows(P, wlo, min(whi, P.vtotal - 1), rA, rB);
     const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
-    for (int e = tid; e < 4 * P.TABW; e += kWLoad) {
+    for (int e = tid; e < 4 * P.TABW; e += nthr) {
         const int k = e / P.TABW, w = e - k * P.TABW;
         int idx = -1;
         if (k < G.np && w < P.KP + G.span[k]) {
@@ -483,8 +488,7 @@ __device__ __forceinline__ void w_build_table(const WgradMma &P, const WGroup &G
 }
 
 __device__ __forceinline__ void w_load_A_rows(const WgradMma &P, const WLane &L, uint32_t stg, uint32_t tab,
-                                              uint32_t zero8, uint32_t tm_a, int q, int part) {
-    constexpr int kParts = kWLoad / 128;
+                                              uint32_t zero8, uint32_t tm_a, int q, int part, int kParts) {
     const uint32_t pxb = (uint32_t)P.CBI * 32u;
     const int nk = P.KP / 4;
     const uint32_t lane_q = (uint32_t)(q * 32) << 16;
@@ -519,10 +523,9 @@ __device__ __forceinline__ void w_load_A_rows(const WgradMma &P, const WLane &L,
 }
 
 __device__ __forceinline__ void w_load_A(const WgradMma &P, const WLane &L, int v0, uint32_t stg, uint32_t tm_a,
-                                         int q, int part) {
+                                         int q, int part, int kParts) {
     // Unconditional loads: padding rows read harmless staged data (their D
     // rows are never stored) and the staging tail past the tensor end is zero.
-    constexpr int kParts = kWLoad / 128;
     const uint32_t pxb = (uint32_t)P.CBI * 32u;
     const int nk = P.KP / 4;
     int wo[4];
@@ -584,14 +587,14 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(stg_full + i, 1);
-            mbar_init(stg_empty + i, kWLoad);
+            mbar_init(stg_empty + i, kWLoad / P.lgroups);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(acc_full + i, 1);
             mbar_init(acc_empty + i, kWEpi / 32);
         }
         for (int s = 0; s < P.nstages; ++s) {
-            mbar_init(op_full + s, kWLoad);
+            mbar_init(op_full + s, kWLoad / P.lgroups);
             mbar_init(op_empty + s, 1);
         }
         mbar_fence_init();
@@ -681,9 +684,16 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     } else if (warp < kEpi0) {
         // ---------------------------------------------------------- loaders
         const int tid = threadIdx.x;
-        const int q = warp & 3, part = warp >> 2;
-        int sb = 0, st = 0;
-        uint32_t sph = 0, ph = 0;
+        // group lg = tid / gsize owns the stages s with s % lgroups == lg; the
+        // warps of a group cover all four TMEM lane quarters (quarter = warp % 4)
+        const int NG = P.lgroups;
+        const int gsize = kWLoad / NG, gwarps = gsize / 32;
+        const int lg = tid / gsize, gtid = tid - lg * gsize;
+        const int q = warp & 3;
+        int part = 0, nparts = 0;
+        for (int w = lg * gwarps; w < (lg + 1) * gwarps; ++w)
+            if ((w & 3) == q) { if (w < warp) ++part; ++nparts; }
+        int s_glob = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             int g, ks, p0, p1;
             wdecode(P, item, g, ks, p0, p1);
@@ -691,7 +701,10 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             w_lane_setup(P, g, q, lane, L);
             WGroup G;
             w_group_setup(P, g, G);
-            for (int v0 = p0; v0 < p1; v0 += P.KP) {
+            for (int v0 = p0; v0 < p1; v0 += P.KP, ++s_glob) {
+                if (s_glob % NG != lg) continue;
+                const int sb = s_glob % P.nstg, st = s_glob % P.nstages;
+                const uint32_t sph = (uint32_t)(s_glob / P.nstg) & 1u, ph = (uint32_t)(s_glob / P.nstages) & 1u;
                 // tables per staging buffer: a buffer is refilled (and its
                 // tables rewritten) only after every loader thread released it
                 const uint32_t tab = smem_u32(smem_raw) + P.tab_off + (uint32_t)sb * P.tab_stride;
@@ -700,28 +713,27 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 if (tid == 0) WTRACE(1, si, 0);
                 mbar_wait(stg_full + sb, sph);
                 if (tid == 0) WTRACE(1, si, 1);
-                if (P.I_rows) w_build_table(P, G, v0, tab, tid);
-                w_build_btab(P, v0, btab, tid);
-                if (!(P.dbg & 1)) w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, tid);
-                named_bar_sync(1, kWLoad);
+                if (P.I_rows) w_build_table(P, G, v0, tab, gtid, gsize);
+                w_build_btab(P, v0, btab, gtid, gsize);
+                if (!(P.dbg & 1)) w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, gtid, gsize);
+                named_bar_sync(1 + lg, gsize);
                 mbar_wait(op_empty + st, ph ^ 1);
                 fence_after_sync();
                 if (tid == 0) WTRACE(1, si, 2);
                 const uint32_t stg = stg0 + sb * P.stg_bytes;
-                if (!(P.dbg & 4)) w_load_B(P, stg, btab, op0 + st * P.b_bytes, tid);
+                if (!(P.dbg & 4)) w_load_B(P, stg, btab, op0 + st * P.b_bytes, gtid);
                 if (P.dbg & 16) {
                 } else if (P.I_rows)
-                    w_load_A_rows(P, L, stg, tab, zero8, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
+                    w_load_A_rows(P, L, stg, tab, zero8, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part,
+                                  nparts);
                 else
-                    w_load_A(P, L, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part);
+                    w_load_A(P, L, v0, stg, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part, nparts);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 fence_proxy_async_smem();
                 fence_before_sync();
                 if (tid == 0) WTRACE(1, si, 3);
                 mbar_arrive(op_full + st);
                 mbar_arrive(stg_empty + sb);
-                if (++sb == P.nstg) { sb = 0; sph ^= 1; }
-                if (++st == P.nstages) { st = 0; ph ^= 1; }
             }
         }
     } else if (warp == kMma) {
@@ -747,29 +759,27 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 // the warp stays converged; one elected lane issues 4 k-steps at
                 // a time (a long divergent single-lane loop issues far slower)
                 if (P.bdesc) {
+                    // copy-major: each accumulator block takes its k-steps back
+                    // to back (switching the accumulator every MMA is slower)
                     const int nsub = P.Cout * 4;
                     for (int tt = 0; tt < ntl; ++tt) {
-                        const uint32_t d = tmem + (uint32_t)(tt * P.N_tile);
-                        for (int k4 = 0; k4 < nk; k4 += 4) {
-                            if (elect_one()) {
+                        for (int j = 0; j < P.nq; ++j) {
+                            const uint32_t d = tmem + (uint32_t)(tt * P.N_tile + j * nsub);
+                            const uint64_t bj = bd0 + (uint64_t)((P.nq - 1 - j) * 4);
+                            for (int k4 = 0; k4 < nk; k4 += 4) {
+                                if (elect_one()) {
 #pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const int kk = k4 + u;
-#pragma unroll
-                                    for (int j = 0; j < kWMaxNq; ++j) {
-                                        if (j < P.nq) {
-                                            asm volatile(
-                                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(
-                                                    d + (uint32_t)(j * nsub)),
-                                                "r"(a0 + (uint32_t)((tt * nk + kk) * 8)),
-                                                "l"(bd0 + (uint64_t)((P.nq - 1 - j) * 4 + kk * 16)), "r"(idesc_sub),
-                                                "r"((first && kk == 0) ? 0u : 1u));
-                                        }
+                                    for (int u = 0; u < 4; ++u) {
+                                        const int kk = k4 + u;
+                                        asm volatile(
+                                            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+                                            "r"(a0 + (uint32_t)((tt * nk + kk) * 8)), "l"(bj + (uint64_t)(kk * 16)),
+                                            "r"(idesc_sub), "r"((first && kk == 0) ? 0u : 1u));
                                     }
                                 }
+                                __syncwarp();
                             }
-                            __syncwarp();
                         }
                     }
                 } else
@@ -1069,8 +1079,11 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             const uint32_t bbytes = (uint32_t)((P.bdesc ? P.Cout * 4 : P.N_tile) / 8) * sbo;
             const uint32_t btab_off = P.I_rows ? 16u * TABW : 0u;
             const uint32_t tab_stride = btab_off + (((uint32_t)(KP + P.nq) * 4u + 15u) & ~15u);
-            for (int ns = 3; ns >= 2 && !found; --ns)
-            for (int nstg = 3; nstg >= 2 && !found; --nstg) {
+            // (A buffers, staging buffers): equal counts first, so that the
+            // loader can run that many stage groups concurrently
+            static const int combos[4][2] = {{3, 3}, {2, 2}, {2, 3}, {3, 2}};
+            for (int ci = 0; ci < 4 && !found; ++ci) {
+                const int ns = combos[ci][0], nstg = combos[ci][1];
                 if (acc + ns * abuf > 512) continue;   // TMEM: accumulators + ns A buffers
                 const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes + (uint64_t)nstg * tab_stride;
                 if (tot > kWSmemLimit) continue;
@@ -1100,7 +1113,13 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_uppO.init((uint32_t)(2 * P.Cout));
-    P.b_pstep = kWLoad / (2 * P.Cout);
+    static const int lg_env = getenv("CAPSCONV_WG_LG") ? atoi(getenv("CAPSCONV_WG_LG")) : 0;
+    P.lgroups = 1;
+    for (int ng : {3, 2}) {
+        if (lg_env && ng != lg_env) continue;
+        if (P.nstg % ng == 0 && P.nstages % ng == 0 && (kWLoad / ng) / (2 * P.Cout) >= 1) { P.lgroups = ng; break; }
+    }
+    P.b_pstep = (kWLoad / P.lgroups) / (2 * P.Cout);
     if (P.b_pstep < 1) return WPlan{};
     const size_t nk = (size_t)P.ntaps * P.C * P.Cout * 16;
     pl.part_bytes = P.ksplit > 1 ? ((size_t)P.ksplit * nk * 4 + 255) & ~(size_t)255 : 0;
