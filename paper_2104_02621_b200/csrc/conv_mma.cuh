@@ -60,6 +60,10 @@ struct ConvMma {
     // stride-2 forward: whole input rows (both parities) staged with one bulk
     // copy; a per-stage table maps each plane pixel of the window to them
     int I_rows, Hin, Win, Bin;
+    // tall-box staging (unit-stride source planes, not batch mode): per image
+    // segment of the window, boxes of h_box source rows x src_W pixels; a
+    // per-item table maps window pixels to staged pixels (-1: zero)
+    int stg_tall, h_box;
     uint32_t tab_off;          // table offset from the dynamic smem base (npl * win_px int32)
     // ---- tensors
     const __nv_bfloat16 *src;  // A source, natural capsule layout, pixel = CS*16 elements

@@ -83,12 +83,88 @@ __device__ __forceinline__ void conv_in_rows(const ConvMma &P, int v0, int &rA, 
     if (whi < wlo) rB = rA - 1;
 }
 
+// Tall-box staging: the window's source rows, image by image.  Segment of
+// image b = rows [yfirst, yhi] (yfirst pulled up so the last box never runs
+// past yhi; a segment occupies max(rows, h_box) staged rows), staged at row
+// offset rowbase.  Every thread walks the same (<= 4) segments.
+struct TallSegs {
+    int n;
+    int b[4], yfirst[4], yhi[4], rowbase[4];
+};
+__device__ __forceinline__ void tall_segments(const ConvMma &P, int v0, TallSegs &S) {
+    S.n = 0;
+    const int vtot = P.Bn * P.Hg * P.Wg;
+    const int vlo = max(v0, 0), vhi = min(v0 + P.win_px, vtot) - 1;
+    if (vhi < vlo) return;
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const int ba = (int)P.fd_HgWg.div((uint32_t)vlo), bb = (int)P.fd_HgWg.div((uint32_t)vhi);
+    const int ya = (int)P.fd_Wg.div((uint32_t)vlo - (uint32_t)ba * HgWg);
+    const int yb = (int)P.fd_Wg.div((uint32_t)vhi - (uint32_t)bb * HgWg);
+    int rowbase = 0;
+    for (int b = ba; b <= bb && S.n < 4; ++b) {
+        const int ylo = b == ba ? ya : 0;
+        const int yhi = min(b == bb ? yb : P.Hg - 1, P.src_H - 1);
+        if (yhi < ylo) continue;   // only zero-padding rows of this image
+        const int yfirst = max(0, min(ylo, yhi - P.h_box + 1));
+        S.b[S.n] = b; S.yfirst[S.n] = yfirst; S.yhi[S.n] = yhi; S.rowbase[S.n] = rowbase;
+        ++S.n;
+        rowbase += max(yhi - yfirst + 1, P.h_box);
+    }
+}
+__device__ __forceinline__ int tall_nbox(const ConvMma &P, const TallSegs &S, int k) {
+    return max(1, (S.yhi[k] - S.yfirst[k] + P.h_box) / P.h_box);
+}
+__device__ __forceinline__ uint32_t tall_issue(const ConvMma &P, int v0, int ch, uint32_t stg, uint32_t mbar, bool issue) {
+    TallSegs S;
+    tall_segments(P, v0, S);
+    const uint32_t px_bytes = (uint32_t)P.CC * 32u;
+    const uint32_t box_bytes = (uint32_t)P.h_box * P.src_W * px_bytes;
+    const int c0 = ch * P.CC * 16;
+    uint32_t bytes = 0;
+    for (int k = 0; k < S.n; ++k) {
+        const int nb = tall_nbox(P, S, k);
+        for (int j = 0; j < nb; ++j) {
+            const int ys = j == nb - 1 ? max(S.yfirst[k], S.yhi[k] - P.h_box + 1) : S.yfirst[k] + j * P.h_box;
+            if (issue)
+                tma::load4d(stg + (uint32_t)((S.rowbase[k] + ys - S.yfirst[k]) * P.src_W) * px_bytes, &P.tmap, c0, 0,
+                            ys, S.b[k], mbar);
+            bytes += box_bytes;
+        }
+    }
+    return bytes;
+}
+// table of the window: tab[vl] = staged pixel of window pixel vl, -1 = zero
+__device__ __forceinline__ void build_table_tall(const ConvMma &P, const Item &it, uint32_t tab, int tid) {
+    const int v0 = window_v0(P, it);
+    TallSegs S;
+    tall_segments(P, v0, S);
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const int vtotal = P.Bn * P.Hg * P.Wg;
+    for (int e = tid; e < P.win_px; e += kProducerThreads) {
+        const int v = v0 + e;
+        int idx = -1;
+        if (v >= 0 && v < vtotal) {
+            const uint32_t b = P.fd_HgWg.div((uint32_t)v);
+            const uint32_t rr = (uint32_t)v - b * HgWg;
+            const int Y = (int)P.fd_Wg.div(rr);
+            const int X = (int)rr - Y * P.Wg;
+            if (Y < P.src_H && X < P.src_W) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < S.n && S.b[k] == (int)b) idx = (S.rowbase[k] + Y - S.yfirst[k]) * P.src_W + X;
+            }
+        }
+        asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(tab + (uint32_t)e * 4u), "r"(idx) : "memory");
+    }
+}
+
 // TMA thread: stage the natural-layout source pixels covering the window of
 // channel chunk `ch` for every plane.  Rows mode: one box per virtual row
 // (Wg pixels, every pl_s-th source pixel, rows/batches outside the tensor
 // read as zero).  Batch mode (Hg*Wg == 1): boxes of BB images.
 __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &it, int ch, uint32_t stg,
                                                   uint32_t mbar) {
+    if (P.stg_tall) return tall_issue(P, window_v0(P, it), ch, stg, mbar, true);
     if (P.I_rows) {
         int rA, rB;
         conv_in_rows(P, window_v0(P, it), rA, rB);
@@ -127,6 +203,7 @@ __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &
 }
 
 __device__ __forceinline__ uint32_t staging_bytes(const ConvMma &P, const Item &it) {
+    if (P.stg_tall) return tall_issue(P, window_v0(P, it), 0, 0, 0, false);
     if (P.I_rows) {
         int rA, rB;
         conv_in_rows(P, window_v0(P, it), rA, rB);
@@ -321,9 +398,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 }
                 mbar_wait(stg_full + sb, sphase);
                 if (tid == 0) TRACE(0, ii, 1);
-                if (P.I_rows) {
+                if (P.I_rows || P.stg_tall) {
                     const uint32_t tab = smem_u32(smem_raw) + P.tab_off;
-                    build_table(P, it, tab, tid);
+                    if (P.stg_tall) build_table_tall(P, it, tab, tid);
+                    else build_table(P, it, tab, tid);
                     asm volatile("bar.sync 1, %0;\n" ::"r"(kProducerThreads) : "memory");
                     repack_rows(P, stg0 + sb * P.stg_bytes, tab, a_stage, tid);
                     asm volatile("bar.sync 1, %0;\n" ::"r"(kProducerThreads) : "memory");   // table reuse
@@ -743,23 +821,43 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1;
             if (!batch_mode && !rows_mode && P.Wg * s > 256) continue;
             const int BB = std::min(win_px, 256);
-            const int cap = batch_mode ? ceil_div(win_px, BB) * BB
-                            : rows_mode ? 2 * ((win_px - 1) / P.Wg + 2) * (int)p.W
-                                        : ((win_px - 1) / P.Wg + 2) * P.Wg;
-            const uint32_t stg_plane = (uint32_t)cap * cc * 32;
-            const uint32_t stg = rows_mode ? stg_plane : (uint32_t)P.npl * stg_plane;
-            const uint32_t tab_bytes = rows_mode ? (uint32_t)(P.npl * win_px * 4 + 15) & ~15u : 0u;
-            int best_st = 0, best_nstg = 0;
+            // tall boxes: unit-stride source planes outside batch/rows mode
+            static const int no_tall = getenv("CAPSCONV_NO_TALL") ? 1 : 0;
+            // (only when a virtual-row box is small: <= 2.5 KB per TMA op is
+            // op-rate bound, measured: L3 dI 146 -> 99 us; 3 KB rows are not)
+            const bool tall_ok = !batch_mode && !rows_mode && P.pl_s == 1 && !no_tall && P.src_W <= 256 &&
+                                 P.Wg * cc * 32 <= 2560;
+            const int nrows = (win_px - 1) / P.Wg + 2;
+            const int nseg = (nrows - 1) / P.Hg + 2;
+            int best_st = 0, best_nstg = 0, cap = 0, hbox = 0;
+            uint32_t stg_plane = 0, stg = 0, tab_bytes = 0;
             // batch mode (fully-connected view) is a streaming GEMM: deeper
             // staging keeps more HBM bytes in flight per SM
             const int max_nstg = batch_mode ? kMaxStg : 2;
-            for (int nstg = max_nstg; nstg >= 1 && !best_st; --nstg)
-                for (int st = std::min(kMaxStages, 4); st >= (nstg >= 2 ? 2 : 3); --st) {
-                    const uint64_t bytes = 1024 + (uint64_t)nstg * stg + (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) +
-                                           (bres ? b_stage : 0) + tab_bytes;
-                    if (bytes <= kSmemLimit) { best_st = st; best_nstg = nstg; break; }
-                }
+            static const int force_h = getenv("CAPSCONV_TALL_H") ? atoi(getenv("CAPSCONV_TALL_H")) : -1;
+            for (int h : {8, 4, 2, 1, 0}) {            // h = 0: one virtual row per box
+                if (force_h >= 0 && h != force_h) continue;
+                if (h > 0 && (!tall_ok || h > P.src_H || nseg > 4)) continue;
+                if (h == 0 && tall_ok && best_st) break;
+                cap = batch_mode ? ceil_div(win_px, BB) * BB
+                      : rows_mode ? 2 * ((win_px - 1) / P.Wg + 2) * (int)p.W
+                      : h > 0 ? (nrows + nseg * h) * P.src_W
+                              : ((win_px - 1) / P.Wg + 2) * P.Wg;
+                stg_plane = (uint32_t)cap * cc * 32;
+                stg = rows_mode ? stg_plane : (uint32_t)P.npl * stg_plane;
+                tab_bytes = (rows_mode || h > 0) ? (uint32_t)(P.npl * win_px * 4 + 15) & ~15u : 0u;
+                best_st = 0; best_nstg = 0;
+                for (int nstg = max_nstg; nstg >= (h > 0 ? 2 : 1) && !best_st; --nstg)
+                    for (int st = std::min(kMaxStages, 4); st >= (nstg >= 2 ? 2 : 3); --st) {
+                        const uint64_t bytes = 1024 + (uint64_t)nstg * stg +
+                                               (uint64_t)st * (a_stage + (bres ? 0 : b_stage)) + (bres ? b_stage : 0) +
+                                               tab_bytes;
+                        if (bytes <= kSmemLimit) { best_st = st; best_nstg = nstg; break; }
+                    }
+                if (best_st) { hbox = h; break; }
+            }
             if (!best_st) continue;
+            P.stg_tall = hbox > 0 ? 1 : 0; P.h_box = hbox;
             P.stg_batch_mode = batch_mode ? 1 : 0; P.BB = BB; P.stg_cap_px = cap;
             P.stg_plane_bytes = stg_plane; P.stg_bytes = stg; P.nstg = best_nstg;
             P.I_rows = rows_mode ? 1 : 0;
@@ -816,7 +914,8 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
     P.dbg = dbg_bits;
     uint8_t *w = static_cast<uint8_t *>(ws);
     P.src = static_cast<const __nv_bfloat16 *>(src);
-    if (!make_capsule_tmap(&P.tmap, src, P.Bn, P.src_H, P.src_W, P.CS, P.CC, P.stg_batch_mode ? 1 : P.Wg, 1,
+    if (!make_capsule_tmap(&P.tmap, src, P.Bn, P.src_H, P.src_W, P.CS, P.CC,
+                           P.stg_batch_mode ? 1 : P.stg_tall ? P.src_W : P.Wg, P.stg_tall ? P.h_box : 1,
                            P.stg_batch_mode ? P.BB : 1, P.stg_batch_mode ? 1 : P.pl_s))
         return cudaErrorInvalidValue;
     P.wpack = w;
@@ -896,10 +995,10 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
         fprintf(stderr,
                 "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
                 "nchunks=%d ksplit=%d G=%d mtiles=%d items=%d win_px=%d stages=%d bres=%d smem=%u tmem=%u nstg=%d "
-                "stg_cap=%d batch=%d gpi=%d\n",
+                "stg_cap=%d batch=%d gpi=%d h_box=%d\n",
                 dgrad ? "dgrad" : "fwd", P.CS, P.NCH, P.Hg, P.Wg, P.npl, P.nog, P.ntaps, P.N_tile, P.n_ntiles, P.CC,
                 P.nchunks, P.ksplit, P.G, P.n_mtiles, P.n_items, P.win_px, P.nstages, P.b_resident, P.smem_bytes,
-                P.tmem_cols, P.nstg, P.stg_cap_px, P.stg_batch_mode, P.gpi);
+                P.tmem_cols, P.nstg, P.stg_cap_px, P.stg_batch_mode, P.gpi, P.stg_tall ? P.h_box : 0);
     }
     return pl;
 }
