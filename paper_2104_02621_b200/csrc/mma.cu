@@ -432,26 +432,37 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             mbar_wait(acc_full + abuf, aphase);
             if (row == 0) TRACE(2, ii, 1);
             fence_after_sync();
-            const int nq_epi = (P.dbg & 32) ? 0 : P.gpi * it.ntl;
-            for (int qi = ehalf; qi < nq_epi; qi += 2) {
-                const int gg = qi / it.ntl, gi = qi - gg * it.ntl;   // output group, tile
-                const int g = it.g + gg;
-                const int u = (it.tile0 + gi) * kTilePix + (row >> 2);
-                const int d1 = row & 3;
-                bool valid = u < vtotal;
-                size_t opix = 0;
-                if (valid) {
-                    const uint32_t b = P.fd_HgWg.div((uint32_t)u);
-                    const uint32_t rr = (uint32_t)u - b * HgWg;
-                    const uint32_t Y = P.fd_Wg.div(rr);
-                    const uint32_t X = rr - Y * (uint32_t)P.Wg;
-                    const int oy = P.og_s * (int)Y + P.og_oy[g];
-                    const int ox = P.og_s * (int)X + P.og_ox[g];
-                    valid = oy < P.out_H && ox < P.out_W;
-                    opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
+            // work units (output group, tile, 32-column chunk) alternate between
+            // the two warps of this lane quarter -- both stay busy even for
+            // one tile per item (G = 1)
+            const int nch = (P.N_tile + 31) / 32;
+            const int nunits = (P.dbg & 32) ? 0 : P.gpi * it.ntl * nch;
+            int cur_t = -1;
+            int u = 0, d1 = row & 3;
+            bool valid = false;
+            size_t opix = 0;
+            for (int w = ehalf; w < nunits; w += 2) {
+                const int t = w / nch, n0 = (w - t * nch) * 32;
+                const int gg = t / it.ntl, gi = t - gg * it.ntl;   // output group, tile
+                if (t != cur_t) {
+                    cur_t = t;
+                    const int g = it.g + gg;
+                    u = (it.tile0 + gi) * kTilePix + (row >> 2);
+                    valid = u < vtotal;
+                    opix = 0;
+                    if (valid) {
+                        const uint32_t b = P.fd_HgWg.div((uint32_t)u);
+                        const uint32_t rr = (uint32_t)u - b * HgWg;
+                        const uint32_t Y = P.fd_Wg.div(rr);
+                        const uint32_t X = rr - Y * (uint32_t)P.Wg;
+                        const int oy = P.og_s * (int)Y + P.og_oy[g];
+                        const int ox = P.og_s * (int)X + P.og_ox[g];
+                        valid = oy < P.out_H && ox < P.out_W;
+                        opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
+                    }
                 }
                 const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(((abuf * P.gpi + gg) * P.G + gi) * P.N_tile);
-                for (int n0 = 0; n0 < P.N_tile; n0 += 32) {
+                {
                     float va[16], vb[16];
                     const bool two = n0 + 16 < P.N_tile;
                     if (!(P.dbg & 16)) {

@@ -115,6 +115,8 @@ struct WgradMma {
     // bdesc: B holds ONE dO copy over KP + nq - 1 pixels; copy j is the same
     // buffer at descriptor offset (nq-1-j) pixels (64 B), one N = 4*Cout MMA per copy
     int bdesc;
+    int bmat;      // bdesc: materialised copies F_a[e] = F_0[e + a], a < bmat, side by side in N;
+                   // accumulator block bi (columns bi*4*Cout) is shift j = nq-1-bi
     // loader groups: stage s is built by group s % lgroups (lgroups divides nstg
     // and nstages, so every buffer always belongs to one group); the groups
     // work on different stages concurrently
@@ -321,6 +323,11 @@ __device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32
             const uint32_t dst = dcol[0] + (uint32_t)e * 64u;
             st_shared_v2(dst, v.x, v.y);
             st_shared_v2(dst + 16u, v.z, v.w);
+            if (P.bmat > 1 && e >= 1) {          // F_1[e - 1] = F_0[e]
+                const uint32_t d1 = dcol[1] + (uint32_t)(e - 1) * 64u;
+                st_shared_v2(d1, v.x, v.y);
+                st_shared_v2(d1 + 16u, v.z, v.w);
+            }
         }
         return;
     }
@@ -739,6 +746,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     } else if (warp == kMma) {
         const uint32_t idesc = idesc_bf16(128, P.N_tile, 0, 1);
         const uint32_t idesc_sub = idesc_bf16(128, P.Cout * 4, 0, 1);
+        const uint32_t idesc_sub2 = idesc_bf16(128, (P.bmat > 1 ? 2 : 1) * P.Cout * 4, 0, 1);
         int st = 0, abuf = 0;
         uint32_t ph = 0, aph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
@@ -759,13 +767,17 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 // the warp stays converged; one elected lane issues 4 k-steps at
                 // a time (a long divergent single-lane loop issues far slower)
                 if (P.bdesc) {
-                    // copy-major: each accumulator block takes its k-steps back
-                    // to back (switching the accumulator every MMA is slower)
+                    // accumulator block bi = shift j = nq-1-bi reads F_0 from
+                    // pixel bi (descriptor offset); one MMA covers bmat adjacent
+                    // blocks through the materialised copies.  Block-major order:
+                    // each accumulator takes its k-steps back to back.
                     const int nsub = P.Cout * 4;
                     for (int tt = 0; tt < ntl; ++tt) {
-                        for (int j = 0; j < P.nq; ++j) {
-                            const uint32_t d = tmem + (uint32_t)(tt * P.N_tile + j * nsub);
-                            const uint64_t bj = bd0 + (uint64_t)((P.nq - 1 - j) * 4);
+                        for (int b0 = 0; b0 < P.nq; b0 += P.bmat) {
+                            const bool two = P.bmat > 1 && b0 + 1 < P.nq;
+                            const uint32_t d = tmem + (uint32_t)(tt * P.N_tile + b0 * nsub);
+                            const uint64_t bj = bd0 + (uint64_t)(b0 * 4);
+                            const uint32_t idx = two ? idesc_sub2 : idesc_sub;
                             for (int k4 = 0; k4 < nk; k4 += 4) {
                                 if (elect_one()) {
 #pragma unroll
@@ -775,7 +787,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                                             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                                             "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
                                             "r"(a0 + (uint32_t)((tt * nk + kk) * 8)), "l"(bj + (uint64_t)(kk * 16)),
-                                            "r"(idesc_sub), "r"((first && kk == 0) ? 0u : 1u));
+                                            "r"(idx), "r"((first && kk == 0) ? 0u : 1u));
                                     }
                                 }
                                 __syncwarp();
@@ -845,8 +857,9 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
 #pragma unroll
                         for (int jj = 0; jj < 4; ++jj) {
                             const int cn = n0 / 4 + jj;           // capsule column j*Cout + c'
-                            const int j = cn / P.Cout, co = cn - j * P.Cout;
-                            if (j < P.nq && q0 + P.s * j < P.KWv)
+                            const int bi = cn / P.Cout, co = cn - bi * P.Cout;
+                            const int j = P.bdesc ? P.nq - 1 - bi : bi;   // shift of this block
+                            if (bi < P.nq && q0 + P.s * j < P.KWv)
                                 *reinterpret_cast<float4 *>(dst + ((size_t)P.s * j * P.C * P.Cout + co) * 16) =
                                     make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
                         }
@@ -966,6 +979,14 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             P.bdesc = bd ? 1 : 0;
         }
     }
+    {
+        static const int bmat_env = getenv("CAPSCONV_WG_BMAT") ? atoi(getenv("CAPSCONV_WG_BMAT")) : 0;
+        P.bmat = 1;
+        // measured (tests/probe/ab.sh CAPSCONV_WG_BMAT 2 1): two copies are
+        // slower on every stack layer (the bigger B costs pipeline depth), so
+        // one copy is the default; 2 stays selectable
+        if (P.bdesc && 2 * P.Cout * 4 <= 256 && bmat_env == 2) P.bmat = 2;
+    }
     std::vector<int> stap;   // taps that own A slots
     for (int t = 0; t < P.ntaps; ++t)
         if (P.nq == 1 || t % P.KWv < s) stap.push_back(t);
@@ -1076,7 +1097,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             const uint32_t stgO = (uint32_t)capO * P.Cout * 32;
             const uint32_t stg = stgI + stgO;
             const uint32_t sbo = (uint32_t)(P.bdesc ? KP + P.nq - 1 : KP) * 64 + 16;
-            const uint32_t bbytes = (uint32_t)((P.bdesc ? P.Cout * 4 : P.N_tile) / 8) * sbo;
+            const uint32_t bbytes = (uint32_t)((P.bdesc ? P.bmat * P.Cout * 4 : P.N_tile) / 8) * sbo;
             const uint32_t btab_off = P.I_rows ? 16u * TABW : 0u;
             const uint32_t tab_stride = btab_off + (((uint32_t)(KP + P.nq) * 4u + 15u) & ~15u);
             // (A buffers, staging buffers): equal counts first, so that the
