@@ -250,24 +250,30 @@ __device__ __forceinline__ void build_table(const ConvMma &P, const Item &it, ui
 }
 
 __device__ __forceinline__ void repack_rows(const ConvMma &P, uint32_t stg, uint32_t tab, uint32_t a_stage, int tid) {
+    // thread -> fixed unit (c, i); pixels advance by pstep = threads / units
+    // with incremental (plane, pixel) counters: no division, no plane loop
     const int upp = 2 * P.CC;
-    const int total = P.npl * P.win_px * upp;
+    const int pstep = kProducerThreads / upp;
+    const int p0 = tid / upp, u2 = tid - p0 * upp;
+    if (p0 >= pstep) return;
+    const int c = u2 >> 1, i = u2 & 1;
     const uint32_t px_bytes = (uint32_t)P.CC * 32u;
-#pragma unroll 4
-    for (int L = tid; L < total; L += kProducerThreads) {
-        const int pix = (int)P.fd_units.div((uint32_t)L);      // k * win_px + vl
-        const int u2 = L - pix * upp;
-        const int c = u2 >> 1, i = u2 & 1;
-        int k = 0, vl = pix;
-        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+    const uint32_t soff = (uint32_t)u2 * 16u;
+    const uint32_t dcol = a_stage + (c >> 1) * P.a_lbo + (uint32_t)(2 * i) * 16u + (c & 1) * 8u;
+    const int total = P.npl * P.win_px;
+    int k = 0, vl = p0;
+    while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+#pragma unroll 2
+    for (int pix = p0; pix < total; pix += pstep) {
         int idx;
         asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(tab + (uint32_t)pix * 4u));
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (idx >= 0) v = ld_shared_v4(stg + (uint32_t)idx * px_bytes + (uint32_t)u2 * 16u);
-        const uint32_t dst = a_stage + k * P.plane_bytes + (c >> 1) * P.a_lbo + (uint32_t)(vl * 4 + 2 * i) * 16u +
-                             (c & 1) * 8u;
+        if (idx >= 0) v = ld_shared_v4(stg + (uint32_t)idx * px_bytes + soff);
+        const uint32_t dst = dcol + k * P.plane_bytes + (uint32_t)vl * 64u;
         st_shared_v2(dst, v.x, v.y);
         st_shared_v2(dst + 16u, v.z, v.w);
+        vl += pstep;
+        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
     }
 }
 
