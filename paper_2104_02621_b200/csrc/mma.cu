@@ -279,9 +279,33 @@ __device__ __forceinline__ void repack_rows(const ConvMma &P, uint32_t stg, uint
 
 __device__ __forceinline__ void repack_window(const ConvMma &P, const Item &it, uint32_t stg, uint32_t a_stage,
                                               int tid) {
+    const int off = staging_off(P, window_v0(P, it));
+    if (!P.stg_batch_mode) {
+        // thread -> fixed unit (c, i), incremental (plane, pixel) counters
+        // (measured: 2% faster for row staging, 8% slower for FC batch boxes)
+        const int upp = 2 * P.CC;
+        const int pstep = kProducerThreads / upp;
+        const int p0 = tid / upp, u2 = tid - p0 * upp;
+        if (p0 >= pstep) return;
+        const int c = u2 >> 1, i = u2 & 1;
+        const uint32_t px_bytes = (uint32_t)P.CC * 32u;
+        const uint32_t src0 = stg + (uint32_t)off * px_bytes + (uint32_t)u2 * 16u;
+        const uint32_t dcol = a_stage + (c >> 1) * P.a_lbo + (uint32_t)(2 * i) * 16u + (c & 1) * 8u;
+        int k = 0, vl = p0;
+        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+#pragma unroll 2
+        for (; k < P.npl;) {
+            const uint4 v = ld_shared_v4(src0 + k * P.stg_plane_bytes + (uint32_t)vl * px_bytes);
+            const uint32_t dst = dcol + k * P.plane_bytes + (uint32_t)vl * 64u;
+            st_shared_v2(dst, v.x, v.y);
+            st_shared_v2(dst + 16u, v.z, v.w);
+            vl += pstep;
+            while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+        }
+        return;
+    }
     const int upp = 2 * P.CC;
     const int total = P.npl * P.win_px * upp;
-    const int off = staging_off(P, window_v0(P, it));
     const uint32_t px_bytes = (uint32_t)P.CC * 32u;
 #pragma unroll 4
     for (int L = tid; L < total; L += kProducerThreads) {
