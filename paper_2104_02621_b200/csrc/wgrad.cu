@@ -47,7 +47,10 @@ using namespace umma;
 
 namespace {
 
-constexpr int kWLoad = 384, kWEpi = 128;   // three loader warps per TMEM lane quarter
+// 16 loader warps (four per TMEM lane quarter); they also run the epilogue
+// at the end of each work item (a CTA holds ~one item, so dedicated epilogue
+// warps would idle through the whole main loop)
+constexpr int kWLoad = 512, kWEpi = 0;
 constexpr int kWThreads = kWLoad + kWEpi + 64;
 constexpr int kWMaxTiles = 96;
 constexpr int kWMaxSlots = 4;
@@ -120,7 +123,7 @@ struct WgradMma {
     // loader groups: stage s is built by group s % lgroups (lgroups divides nstg
     // and nstages, so every buffer always belongs to one group); the groups
     // work on different stages concurrently
-    int lgroups;
+    int lgroups;   // stage s is built by group s % lgroups
     int Ho, Wo;                            // dO extents (rows per image, pixels per row)
 };
 #define WTRACE(role, idx, ev)                                                              \
@@ -295,14 +298,18 @@ __device__ __forceinline__ void w_build_btab(const WgradMma &P, int v0, uint32_t
 // dO[v - j]: each staged unit is loaded once and stored into every copy
 // whose local row falls inside the stage.
 constexpr int kWMaxNq = 4;
-__device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32_t btab, uint32_t b, int tid) {
+// loader group lg of NG: warps [lg*16/NG, (lg+1)*16/NG) (sizes differ by at most one warp)
+__host__ __device__ __forceinline__ int w_group_w0(int lg, int ng) { return lg * (kWLoad / 32) / ng; }
+
+__device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32_t btab, uint32_t b, int tid,
+                                         int pstep) {
     // thread -> fixed unit (c', i) of a staged pixel; pixels advance by
     // P.b_pstep per iteration (b_pstep * upp <= loader threads): no division
     const uint32_t base = stg + P.stgI_bytes;
     const int upp = 2 * P.Cout;
     const int pix0 = tid / upp;                 // once per stage
     const int u = tid - pix0 * upp;
-    if (pix0 >= P.b_pstep) return;
+    if (pix0 >= pstep) return;
     const int c = u >> 1, i = u & 1;
     const uint32_t pxb = (uint32_t)P.Cout * 32u;
     const uint32_t src_off = (uint32_t)(c * 32 + i * 16);
@@ -315,7 +322,7 @@ __device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32
     }
     if (P.bdesc) {
 #pragma unroll 4
-        for (int e = pix0; e < npx; e += P.b_pstep) {
+        for (int e = pix0; e < npx; e += pstep) {
             int idx;
             asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(btab + (uint32_t)e * 4u));
             uint4 v = make_uint4(0, 0, 0, 0);
@@ -332,7 +339,7 @@ __device__ __forceinline__ void w_load_B(const WgradMma &P, uint32_t stg, uint32
         return;
     }
 #pragma unroll 4
-    for (int e = pix0; e < npx; e += P.b_pstep) {
+    for (int e = pix0; e < npx; e += pstep) {
         int idx;
         asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(btab + (uint32_t)e * 4u));
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -594,14 +601,14 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(stg_full + i, 1);
-            mbar_init(stg_empty + i, kWLoad / P.lgroups);
+            mbar_init(stg_empty + i, 32 * (w_group_w0(i % P.lgroups + 1, P.lgroups) - w_group_w0(i % P.lgroups, P.lgroups)));
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(acc_full + i, 1);
-            mbar_init(acc_empty + i, kWEpi / 32);
+            mbar_init(acc_empty + i, kWLoad / 32);
         }
         for (int s = 0; s < P.nstages; ++s) {
-            mbar_init(op_full + s, kWLoad / P.lgroups);
+            mbar_init(op_full + s, 32 * (w_group_w0(s % P.lgroups + 1, P.lgroups) - w_group_w0(s % P.lgroups, P.lgroups)));
             mbar_init(op_empty + s, 1);
         }
         mbar_fence_init();
@@ -694,13 +701,17 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
         // group lg = tid / gsize owns the stages s with s % lgroups == lg; the
         // warps of a group cover all four TMEM lane quarters (quarter = warp % 4)
         const int NG = P.lgroups;
-        const int gsize = kWLoad / NG, gwarps = gsize / 32;
-        const int lg = tid / gsize, gtid = tid - lg * gsize;
+        int lg = 0;
+        while (lg + 1 < NG && warp >= w_group_w0(lg + 1, NG)) ++lg;
+        const int gw0 = w_group_w0(lg, NG), gw1 = w_group_w0(lg + 1, NG);
+        const int gsize = 32 * (gw1 - gw0), gtid = tid - 32 * gw0;
+        const int bpstep = gsize / (2 * P.Cout);
         const int q = warp & 3;
         int part = 0, nparts = 0;
-        for (int w = lg * gwarps; w < (lg + 1) * gwarps; ++w)
+        for (int w = gw0; w < gw1; ++w)
             if ((w & 3) == q) { if (w < warp) ++part; ++nparts; }
         int s_glob = 0;
+        uint32_t e_aph = 0;   // accumulator phase (one accumulator set)
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             int g, ks, p0, p1;
             wdecode(P, item, g, ks, p0, p1);
@@ -728,7 +739,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 fence_after_sync();
                 if (tid == 0) WTRACE(1, si, 2);
                 const uint32_t stg = stg0 + sb * P.stg_bytes;
-                if (!(P.dbg & 4)) w_load_B(P, stg, btab, op0 + st * P.b_bytes, gtid);
+                if (!(P.dbg & 4)) w_load_B(P, stg, btab, op0 + st * P.b_bytes, gtid, bpstep);
                 if (P.dbg & 16) {
                 } else if (P.I_rows)
                     w_load_A_rows(P, L, stg, tab, zero8, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part,
@@ -741,6 +752,58 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 if (tid == 0) WTRACE(1, si, 3);
                 mbar_arrive(op_full + st);
                 mbar_arrive(stg_empty + sb);
+            }
+            // ------------------------------------------------ epilogue of the item
+            // units (tile, 16 columns) are spread over the four warps of this
+            // warp's lane quarter
+            {
+                const int wq = q, wi = warp >> 2;
+                const int row = wq * 32 + lane;
+                const size_t nkel = (size_t)P.ntaps * P.C * P.Cout * 16;
+                const int ntl = min(P.TG, P.n_mtiles - g * P.TG);
+                const int nch = P.N_tile / 16;
+                mbar_wait(acc_full + 0, e_aph);
+                fence_after_sync();
+                int cur_tt = -1, tap = -1, c = 0, q0 = 0;
+                float *dst = nullptr;
+                const int d2 = row & 3;
+                for (int unit = wi; unit < ntl * nch; unit += 4) {
+                    const int tt = unit / nch, n0 = (unit - tt * nch) * 16;
+                    if (tt != cur_tt) {
+                        cur_tt = tt;
+                        const WTile &T = P.tile[g * P.TG + tt];
+                        tap = -1; c = 0;
+                        for (int j = 0; j < T.nslots; ++j) {
+                            const WSlot &S = T.slot[j];
+                            if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
+                                tap = S.tap;
+                                c = S.c0 + ((row - S.row0) >> 2);
+                            }
+                        }
+                        // column n = (block, c', d3); block bi is shift j of the slot's tap (p, q)
+                        q0 = tap < 0 ? 0 : tap % P.KWv;
+                        dst = P.part + (size_t)ks * nkel + (((size_t)(tap < 0 ? 0 : tap) * P.C + c) * P.Cout) * 16 + d2 * 4;
+                    }
+                    const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(tt * P.N_tile);
+                    float v[16];
+                    tmem_ld16(tcol + n0, v);
+                    tmem_wait_ld();
+                    if (tap >= 0 && c < P.C) {
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int cn = n0 / 4 + jj;           // capsule column bi*Cout + c'
+                            const int bi = cn / P.Cout, co = cn - bi * P.Cout;
+                            const int j = P.bdesc ? P.nq - 1 - bi : bi;   // shift of this block
+                            if (bi < P.nq && q0 + P.s * j < P.KWv)
+                                *reinterpret_cast<float4 *>(dst + ((size_t)P.s * j * P.C * P.Cout + co) * 16) =
+                                    make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+                        }
+                    }
+                }
+                fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty + 0);
+                e_aph ^= 1;
             }
         }
     } else if (warp == kMma) {
@@ -820,56 +883,6 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
             if (elect_one()) mma_commit(acc_full + abuf);
             __syncwarp();
             aph ^= 1;   // one accumulator set (abuf stays 0)
-        }
-    } else {
-        // ---------------------------------------------------------- epilogue
-        const int wq = warp & 3;
-        const int row = wq * 32 + lane;
-        const size_t nkel = (size_t)P.ntaps * P.C * P.Cout * 16;
-        int abuf = 0;
-        uint32_t aph = 0;
-        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-            int g, ks, p0, p1;
-            wdecode(P, item, g, ks, p0, p1);
-            const int ntl = min(P.TG, P.n_mtiles - g * P.TG);
-            mbar_wait(acc_full + abuf, aph);
-            fence_after_sync();
-            for (int tt = 0; tt < ntl; ++tt) {
-                const WTile &T = P.tile[g * P.TG + tt];
-                int tap = -1, c = 0;
-                const int d2 = row & 3;
-                for (int j = 0; j < T.nslots; ++j) {
-                    const WSlot &S = T.slot[j];
-                    if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
-                        tap = S.tap;
-                        c = S.c0 + ((row - S.row0) >> 2);
-                    }
-                }
-                // column n = (j, c', d3): block j is tap (p, q + s*j) of the slot's tap (p, q)
-                const int q0 = tap < 0 ? 0 : tap % P.KWv;
-                float *dst = P.part + (size_t)ks * nkel + (((size_t)(tap < 0 ? 0 : tap) * P.C + c) * P.Cout) * 16 + d2 * 4;
-                const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(tt * P.N_tile);
-                for (int n0 = 0; n0 < P.N_tile; n0 += 16) {
-                    float v[16];
-                    tmem_ld16(tcol + n0, v);
-                    tmem_wait_ld();
-                    if (tap >= 0 && c < P.C) {
-#pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) {
-                            const int cn = n0 / 4 + jj;           // capsule column j*Cout + c'
-                            const int bi = cn / P.Cout, co = cn - bi * P.Cout;
-                            const int j = P.bdesc ? P.nq - 1 - bi : bi;   // shift of this block
-                            if (bi < P.nq && q0 + P.s * j < P.KWv)
-                                *reinterpret_cast<float4 *>(dst + ((size_t)P.s * j * P.C * P.Cout + co) * 16) =
-                                    make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
-                        }
-                    }
-                }
-            }
-            fence_before_sync();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty + abuf);
-            aph ^= 1;
         }
     }
 
@@ -1102,8 +1115,16 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             const uint32_t tab_stride = btab_off + (((uint32_t)(KP + P.nq) * 4u + 15u) & ~15u);
             // (A buffers, staging buffers): equal counts first, so that the
             // loader can run that many stage groups concurrently
-            static const int combos[4][2] = {{3, 3}, {2, 2}, {2, 3}, {3, 2}};
-            for (int ci = 0; ci < 4 && !found; ++ci) {
+            static const int cmode = getenv("CAPSCONV_WG_CMODE") ? atoi(getenv("CAPSCONV_WG_CMODE")) : 0;
+            // (A buffers, staging buffers): equal counts first, so that the
+            // loader runs that many stage groups concurrently; 3/3 (three
+            // groups of 5-6 warps) measured best where it fits (L1 dK 152 ->
+            // 130 us vs 2/2)
+            static const int combos_t[3][5][2] = {{{3, 3}, {2, 2}, {2, 3}, {3, 2}, {0, 0}},
+                                                  {{2, 2}, {3, 3}, {2, 3}, {3, 2}, {0, 0}},
+                                                  {{4, 4}, {2, 2}, {3, 3}, {2, 3}, {3, 2}}};
+            const int (*combos)[2] = combos_t[cmode];
+            for (int ci = 0; ci < 5 && combos[ci][0] && !found; ++ci) {
                 const int ns = combos[ci][0], nstg = combos[ci][1];
                 if (acc + ns * abuf > 512) continue;   // TMEM: accumulators + ns A buffers
                 const uint64_t tot = 1024 + (uint64_t)nstg * stg + (uint64_t)ns * bbytes + (uint64_t)nstg * tab_stride;
@@ -1136,11 +1157,17 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     P.fd_uppO.init((uint32_t)(2 * P.Cout));
     static const int lg_env = getenv("CAPSCONV_WG_LG") ? atoi(getenv("CAPSCONV_WG_LG")) : 0;
     P.lgroups = 1;
-    for (int ng : {3, 2}) {
+    // groups of 4 or 8 warps (every group covers the four lane quarters).
+    // NG must divide both buffer counts: then a buffer is always used by the
+    // same group, whose previous wait on it was the phase just before --
+    // otherwise a group running ahead could wait two phases ahead and the
+    // mbarrier parity test would pass falsely (observed: a hang).
+    for (int ng : {4, 3, 2}) {
         if (lg_env && ng != lg_env) continue;
-        if (P.nstg % ng == 0 && P.nstages % ng == 0 && (kWLoad / ng) / (2 * P.Cout) >= 1) { P.lgroups = ng; break; }
+        const int min_threads = 32 * w_group_w0(1, ng);   // the smallest group is the first
+        if (P.nstg % ng == 0 && P.nstages % ng == 0 && min_threads / (2 * P.Cout) >= 1) { P.lgroups = ng; break; }
     }
-    P.b_pstep = (kWLoad / P.lgroups) / (2 * P.Cout);
+    P.b_pstep = 32 * w_group_w0(1, P.lgroups) / (2 * P.Cout);   // smallest group's (informational)
     if (P.b_pstep < 1) return WPlan{};
     const size_t nk = (size_t)P.ntaps * P.C * P.Cout * 16;
     pl.part_bytes = P.ksplit > 1 ? ((size_t)P.ksplit * nk * 4 + 255) & ~(size_t)255 : 0;
