@@ -877,7 +877,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const int max_nstg = batch_mode ? kMaxStg : 2;
             static const int force_h = getenv("CAPSCONV_TALL_H") ? atoi(getenv("CAPSCONV_TALL_H")) : -1;
             for (int h : {8, 4, 2, 1, 0}) {            // h = 0: one virtual row per box
-                if (force_h >= 0 && h != force_h) continue;
+                if (force_h >= 0 && h > 0 && h != force_h) continue;   // (row boxes stay the fallback)
                 if (h > 0 && (!tall_ok || h > P.src_H || nseg > 4)) continue;
                 if (h == 0 && tall_ok && best_st) break;
                 cap = batch_mode ? ceil_div(win_px, BB) * BB
