@@ -327,7 +327,9 @@ def main():
     # The timed step is one CUDA-graph replay of the whole step (every kernel
     # of every pass; the graph removes host launch gaps between them).  The
     # per-call events are captured with it; launches are counted at capture.
-    use_graph = not args.eager
+    # (N > 1: eager -- the per-layer NCCL all-reduces on the side stream are
+    # not captured into the graph; that path is only exercised on CPU/gloo here)
+    use_graph = not args.eager and world == 1
     gtimer = GraphCallTimer() if use_graph else None
     launches_per_step = None
     if use_graph:

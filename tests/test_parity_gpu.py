@@ -208,6 +208,9 @@ def test_stack_layers_full_batch_exact(cc, oracle_mod, li):
     rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
     rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
     assert np.abs(rdK).max() < 2 ** 24
+    # the benchmarked configuration runs on the tensor-core path, every pass
+    ext = (L.B, L.H, L.W, L.C, L.Cout, L.KH, L.KW, L.D1, L.D2, L.D3, L.stride)
+    assert [cc.select_path(op, dtype, ext) for op in (0, 1, 2)] == [cc.PATH_MMA] * 3
     np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
     np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
     np.testing.assert_array_equal(to_np(dK), rdK)
