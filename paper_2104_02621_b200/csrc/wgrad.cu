@@ -809,6 +809,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
     } else if (warp == kMma) {
         const uint32_t idesc = idesc_bf16(128, P.N_tile, 0, 1);
         const uint32_t idesc_sub = idesc_bf16(128, P.Cout * 4, 0, 1);
+        // 8 k-steps per elected region when possible (measured: L1 dK 130 -> 126 us)
+        const bool unr8 = true;
         const uint32_t idesc_sub2 = idesc_bf16(128, (P.bmat > 1 ? 2 : 1) * P.Cout * 4, 0, 1);
         int st = 0, abuf = 0;
         uint32_t ph = 0, aph = 0;
@@ -841,6 +843,22 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                             const uint32_t d = tmem + (uint32_t)(tt * P.N_tile + b0 * nsub);
                             const uint64_t bj = bd0 + (uint64_t)(b0 * 4);
                             const uint32_t idx = two ? idesc_sub2 : idesc_sub;
+                            if (unr8 && (nk & 7) == 0) {
+                                for (int k8 = 0; k8 < nk; k8 += 8) {
+                                    if (elect_one()) {
+#pragma unroll
+                                        for (int u = 0; u < 8; ++u) {
+                                            const int kk = k8 + u;
+                                            asm volatile(
+                                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+                                                "r"(a0 + (uint32_t)((tt * nk + kk) * 8)), "l"(bj + (uint64_t)(kk * 16)),
+                                                "r"(idx), "r"((first && kk == 0) ? 0u : 1u));
+                                        }
+                                    }
+                                    __syncwarp();
+                                }
+                            } else
                             for (int k4 = 0; k4 < nk; k4 += 4) {
                                 if (elect_one()) {
 #pragma unroll
