@@ -570,31 +570,36 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 const uint64_t a_desc0 = smem_desc(a_stage, P.a_lbo, 128);
                 const uint64_t b_desc0 = smem_desc(b_base, b_lbo, 128);
                 const int ksteps = P.CC / 4;
-                if (elect_one()) {
-                    if (!(P.dbg & 2))
-                    for (int gg = 0; gg < P.gpi; ++gg) {
+                // warp-converged tap loop; one elected lane issues the tap's
+                // (k-step x tile) MMAs
+                if (!(P.dbg & 2))
+                for (int gg = 0; gg < P.gpi; ++gg) {
                     const int g = it.g + gg;
                     const uint32_t d0 = tmem + (uint32_t)((abuf * P.gpi + gg) * P.G * P.N_tile);
                     for (int t = P.og_t0[g]; t < P.og_t1[g]; ++t) {
                         const uint64_t a_tap = a_desc0 + ((P.tap_plane[t] * P.plane_bytes +
                                                            (uint32_t)(P.tap_shift[t] - offmin) * 64u) >> 4);
                         const uint64_t b_tap = b_desc0 + (((t - T0) * (P.CC / 2) * b_lbo) >> 4);
-                        for (int j = 0; j < ksteps; ++j) {
-                            const uint64_t bd = b_tap + ((2u * j * b_lbo) >> 4);
-                            const uint64_t aj = a_tap + ((2u * j * P.a_lbo) >> 4);
-                            const uint32_t acc = (ch != it.c_begin || t != P.og_t0[g] || j != 0) ? 1u : 0u;
-                            uint32_t d = d0;
-                            uint64_t ad = aj;
-                            for (int gi = 0; gi < it.ntl; ++gi) {
-                                mma_bf16_ss(d, ad, bd, idesc, acc);
-                                d += (uint32_t)P.N_tile;
-                                ad += (kTilePix * 64) >> 4;
+                        const bool first_tap = (ch == it.c_begin && t == P.og_t0[g]);
+                        if (elect_one()) {
+                            for (int j = 0; j < ksteps; ++j) {
+                                const uint64_t bd = b_tap + ((2u * j * b_lbo) >> 4);
+                                const uint64_t aj = a_tap + ((2u * j * P.a_lbo) >> 4);
+                                const uint32_t acc = (first_tap && j == 0) ? 0u : 1u;
+                                uint32_t d = d0;
+                                uint64_t ad = aj;
+                                for (int gi = 0; gi < it.ntl; ++gi) {
+                                    mma_bf16_ss(d, ad, bd, idesc, acc);
+                                    d += (uint32_t)P.N_tile;
+                                    ad += (kTilePix * 64) >> 4;
+                                }
                             }
                         }
+                        __syncwarp();
                     }
-                    }
-                    mma_commit(a_empty + stage);
                 }
+                if (elect_one()) mma_commit(a_empty + stage);
+
                 __syncwarp();
                 if (++stage == P.nstages) { stage = 0; phase ^= 1; }
             }
