@@ -221,3 +221,138 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------
+ * Zero padding (SPEC.md:48-53 symmetric zero padding -- the
+ * paper itself has no padding term).  The definition with
+ * the input read through a zero-padded view: I_pad(h, w) = I(h - pad, w - pad)
+ * inside the input, 0 outside.  Shape law H' = floor((H + 2 pad - KH)/s) + 1.
+ * Written out separately so the unpadded functions above (and their pins)
+ * are untouched.
+ * ------------------------------------------------------------------------ */
+int oracle_output_dims_pad(int64_t H, int64_t W, int64_t KH, int64_t KW,
+                           int64_t stride, int64_t pad, int64_t *Ho, int64_t *Wo)
+{
+    if (pad < 0) return OR_ERR_SHAPE;
+    return oracle_output_dims(H + 2 * pad, W + 2 * pad, KH, KW, stride, Ho, Wo);
+}
+
+int oracle_fwd_pad(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                   int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                   int64_t stride, int64_t pad, const double *I, const double *K,
+                   double *O, double *Oabs)
+{
+    int64_t Ho, Wo;
+    int rc = oracle_output_dims_pad(H, W, KH, KW, stride, pad, &Ho, &Wo);
+    if (rc) return rc;
+    if (B < 1 || C < 1 || Cout < 1 || D1 < 1 || D2 < 1 || D3 < 1) return OR_ERR_SHAPE;
+    const int64_t n_out = B * Ho * Wo * Cout * D1 * D3;
+#pragma omp parallel for schedule(static)
+    for (int64_t o = 0; o < n_out; ++o) {
+        int64_t r = o;
+        const int64_t d3 = r % D3; r /= D3;
+        const int64_t d1 = r % D1; r /= D1;
+        const int64_t co = r % Cout; r /= Cout;
+        const int64_t y = r % Wo; r /= Wo;
+        const int64_t x = r % Ho; r /= Ho;
+        const int64_t b = r;
+        double acc = 0.0, aabs = 0.0;
+        for (int64_t p = 0; p < KH; ++p)
+            for (int64_t q = 0; q < KW; ++q) {
+                const int64_t h = x * stride + p - pad, w = y * stride + q - pad;
+                if (h < 0 || h >= H || w < 0 || w >= W) continue;   /* a zero of the padding */
+                for (int64_t c = 0; c < C; ++c)
+                    for (int64_t d2 = 0; d2 < D2; ++d2) {
+                        const double t = I[IDX_I(b, h, w, c, d1, d2)] * K[IDX_K(p, q, c, co, d2, d3)];
+                        acc += t;
+                        aabs += fabs(t);
+                    }
+            }
+        O[o] = acc;
+        if (Oabs) Oabs[o] = aabs;
+    }
+    return OR_OK;
+}
+
+/* dI of the padded convolution: the adjoint restricted to real input pixels
+ * (h + pad = x*s + p). */
+int oracle_bwd_data_pad(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                        int64_t stride, int64_t pad, const double *dO, const double *K,
+                        double *dI, double *dIabs)
+{
+    int64_t Ho, Wo;
+    int rc = oracle_output_dims_pad(H, W, KH, KW, stride, pad, &Ho, &Wo);
+    if (rc) return rc;
+    if (B < 1 || C < 1 || Cout < 1 || D1 < 1 || D2 < 1 || D3 < 1) return OR_ERR_SHAPE;
+    const int64_t n_in = B * H * W * C * D1 * D2;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_in; ++e) {
+        int64_t r = e;
+        const int64_t d2 = r % D2; r /= D2;
+        const int64_t d1 = r % D1; r /= D1;
+        const int64_t c = r % C; r /= C;
+        const int64_t w = r % W; r /= W;
+        const int64_t h = r % H; r /= H;
+        const int64_t b = r;
+        double acc = 0.0, aabs = 0.0;
+        for (int64_t p = 0; p < KH; ++p) {
+            const int64_t hx = h + pad - p;
+            if (hx < 0 || hx % stride != 0) continue;
+            const int64_t x = hx / stride;
+            if (x >= Ho) continue;
+            for (int64_t q = 0; q < KW; ++q) {
+                const int64_t wy = w + pad - q;
+                if (wy < 0 || wy % stride != 0) continue;
+                const int64_t y = wy / stride;
+                if (y >= Wo) continue;
+                for (int64_t co = 0; co < Cout; ++co)
+                    for (int64_t d3 = 0; d3 < D3; ++d3) {
+                        const double t = dO[IDX_O(b, x, y, co, d1, d3)] * K[IDX_K(p, q, c, co, d2, d3)];
+                        acc += t;
+                        aabs += fabs(t);
+                    }
+            }
+        }
+        dI[e] = acc;
+        if (dIabs) dIabs[e] = aabs;
+    }
+    return OR_OK;
+}
+
+int oracle_bwd_kernel_pad(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                          int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                          int64_t stride, int64_t pad, const double *I, const double *dO,
+                          double *dK, double *dKabs)
+{
+    int64_t Ho, Wo;
+    int rc = oracle_output_dims_pad(H, W, KH, KW, stride, pad, &Ho, &Wo);
+    if (rc) return rc;
+    if (B < 1 || C < 1 || Cout < 1 || D1 < 1 || D2 < 1 || D3 < 1) return OR_ERR_SHAPE;
+    const int64_t n_k = KH * KW * C * Cout * D2 * D3;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_k; ++e) {
+        int64_t r = e;
+        const int64_t d3 = r % D3; r /= D3;
+        const int64_t d2 = r % D2; r /= D2;
+        const int64_t co = r % Cout; r /= Cout;
+        const int64_t c = r % C; r /= C;
+        const int64_t q = r % KW; r /= KW;
+        const int64_t p = r;
+        double acc = 0.0, aabs = 0.0;
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t x = 0; x < Ho; ++x)
+                for (int64_t y = 0; y < Wo; ++y) {
+                    const int64_t h = x * stride + p - pad, w = y * stride + q - pad;
+                    if (h < 0 || h >= H || w < 0 || w >= W) continue;
+                    for (int64_t d1 = 0; d1 < D1; ++d1) {
+                        const double t = I[IDX_I(b, h, w, c, d1, d2)] * dO[IDX_O(b, x, y, co, d1, d3)];
+                        acc += t;
+                        aabs += fabs(t);
+                    }
+                }
+        dK[e] = acc;
+        if (dKabs) dKabs[e] = aabs;
+    }
+    return OR_OK;
+}

@@ -56,6 +56,11 @@ def _load():
                 fn = getattr(lib, name)
                 fn.argtypes = [i64] * 11 + [dp] * 4
                 fn.restype = ctypes.c_int
+                fp = getattr(lib, name + "_pad")
+                fp.argtypes = [i64] * 12 + [dp] * 4
+                fp.restype = ctypes.c_int
+            lib.oracle_output_dims_pad.argtypes = [i64] * 6 + [ctypes.POINTER(i64)] * 2
+            lib.oracle_output_dims_pad.restype = ctypes.c_int
             lib.oracle_round_bf16_array.argtypes = [dp, i64]
             lib.oracle_round_bf16_array.restype = None
             lib.oracle_num_threads.argtypes = []
@@ -77,63 +82,79 @@ def num_threads() -> int:
     return int(_load().oracle_num_threads())
 
 
-def output_dims(H, W, KH, KW, stride):
+def output_dims(H, W, KH, KW, stride, pad=0):
     lib = _load()
     ho, wo = ctypes.c_int64(), ctypes.c_int64()
-    rc = lib.oracle_output_dims(H, W, KH, KW, stride, ctypes.byref(ho), ctypes.byref(wo))
+    if pad:
+        rc = lib.oracle_output_dims_pad(H, W, KH, KW, stride, pad, ctypes.byref(ho), ctypes.byref(wo))
+    else:
+        rc = lib.oracle_output_dims(H, W, KH, KW, stride, ctypes.byref(ho), ctypes.byref(wo))
     if rc:
         raise OracleError("oracle_output_dims: status %d" % rc)
     return ho.value, wo.value
 
 
-def fwd(I, K, stride):
-    """O = I (*) K  (Algorithm 2)."""
+def fwd(I, K, stride, pad=0):
+    """O = I (*) K  (Algorithm 2); pad > 0: symmetric zero
+    padding (oracle_fwd_pad)."""
     I, K = _f64(I), _f64(K)
     B, H, W, C, D1, D2 = I.shape
     KH, KW, C2, Cout, D2b, D3 = K.shape
     if C2 != C or D2b != D2:
         raise OracleError("channel / inner capsule dims disagree")
-    Ho, Wo = output_dims(H, W, KH, KW, stride)
+    Ho, Wo = output_dims(H, W, KH, KW, stride, pad)
     O = np.empty((B, Ho, Wo, Cout, D1, D3))
     A = np.empty_like(O)
-    rc = _load().oracle_fwd(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride,
-                            _ptr(I), _ptr(K), _ptr(O), _ptr(A))
+    if pad:
+        rc = _load().oracle_fwd_pad(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad,
+                                    _ptr(I), _ptr(K), _ptr(O), _ptr(A))
+    else:
+        rc = _load().oracle_fwd(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride,
+                                _ptr(I), _ptr(K), _ptr(O), _ptr(A))
     if rc:
         raise OracleError("oracle_fwd: status %d" % rc)
     return O, A
 
 
-def bwd_data(dO, K, stride, H, W):
+def bwd_data(dO, K, stride, H, W, pad=0):
     """dI, the adjoint of fwd in I (Algorithm 4 read as in R10/R11)."""
     dO, K = _f64(dO), _f64(K)
     B, Ho, Wo, Cout, D1, D3 = dO.shape
     KH, KW, C, Cout2, D2, D3b = K.shape
     if Cout2 != Cout or D3b != D3:
         raise OracleError("output channel / capsule dims disagree")
-    if output_dims(H, W, KH, KW, stride) != (Ho, Wo):
+    if output_dims(H, W, KH, KW, stride, pad) != (Ho, Wo):
         raise OracleError("dO spatial shape does not follow the shape law")
     dI = np.empty((B, H, W, C, D1, D2))
     A = np.empty_like(dI)
-    rc = _load().oracle_bwd_data(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride,
-                                 _ptr(dO), _ptr(K), _ptr(dI), _ptr(A))
+    if pad:
+        rc = _load().oracle_bwd_data_pad(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad,
+                                         _ptr(dO), _ptr(K), _ptr(dI), _ptr(A))
+    else:
+        rc = _load().oracle_bwd_data(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride,
+                                     _ptr(dO), _ptr(K), _ptr(dI), _ptr(A))
     if rc:
         raise OracleError("oracle_bwd_data: status %d" % rc)
     return dI, A
 
 
-def bwd_kernel(I, dO, stride, KH, KW):
+def bwd_kernel(I, dO, stride, KH, KW, pad=0):
     """dK, the adjoint of fwd in K (Algorithm 4 read as in R10/R11)."""
     I, dO = _f64(I), _f64(dO)
     B, H, W, C, D1, D2 = I.shape
     B2, Ho, Wo, Cout, D1b, D3 = dO.shape
     if B2 != B or D1b != D1:
         raise OracleError("batch / D1 disagree")
-    if output_dims(H, W, KH, KW, stride) != (Ho, Wo):
+    if output_dims(H, W, KH, KW, stride, pad) != (Ho, Wo):
         raise OracleError("dO spatial shape does not follow the shape law")
     dK = np.empty((KH, KW, C, Cout, D2, D3))
     A = np.empty_like(dK)
-    rc = _load().oracle_bwd_kernel(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride,
-                                   _ptr(I), _ptr(dO), _ptr(dK), _ptr(A))
+    if pad:
+        rc = _load().oracle_bwd_kernel_pad(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad,
+                                           _ptr(I), _ptr(dO), _ptr(dK), _ptr(A))
+    else:
+        rc = _load().oracle_bwd_kernel(B, H, W, C, Cout, KH, KW, D1, D2, D3, stride,
+                                       _ptr(I), _ptr(dO), _ptr(dK), _ptr(A))
     if rc:
         raise OracleError("oracle_bwd_kernel: status %d" % rc)
     return dK, A

@@ -401,3 +401,69 @@ def test_stack_depth1_and_fd(oracle_mod):
         Km[idx] -= h
         fd = (loss(I, Kp, K2) - loss(I, Km, K2)) / (2 * h)
         assert abs(fd - dKs[0][idx]) <= 1e-6 * max(1.0, abs(fd))
+
+
+# ---------------------------------------------------------------- zero padding
+# Pinned to the (already pinned) unpadded oracle run on an explicitly
+# zero-padded input -- numpy's pad, not the oracle's own index arithmetic --
+# plus the adjoint identities of the padded linear map.
+PAD_CASES = [
+    # B, H, W, C, Cout, KH, KW, D1, D2, D3, s, pad
+    (2, 5, 6, 2, 3, 3, 3, 2, 3, 2, 1, 1),
+    (1, 7, 7, 3, 2, 3, 3, 4, 4, 4, 2, 1),
+    (2, 4, 5, 1, 2, 2, 3, 3, 2, 4, 1, 2),
+    (1, 6, 6, 2, 2, 5, 5, 2, 2, 2, 2, 2),
+]
+
+
+def _pad_inputs(case):
+    B, H, W, C, Co, KH, KW, D1, D2, D3, s, pad = case
+    rng = np.random.default_rng(hash(case) & 0xffff)
+    I = rng.uniform(-1, 1, (B, H, W, C, D1, D2))
+    K = rng.uniform(-1, 1, (KH, KW, C, Co, D2, D3))
+    Ho, Wo = (H + 2 * pad - KH) // s + 1, (W + 2 * pad - KW) // s + 1
+    dO = rng.uniform(-1, 1, (B, Ho, Wo, Co, D1, D3))
+    return I, K, dO
+
+
+def _zero_pad(I, pad):
+    return np.pad(I, ((0, 0), (pad, pad), (pad, pad), (0, 0), (0, 0), (0, 0)))
+
+
+@pytest.mark.parametrize("case", PAD_CASES)
+def test_pad_shape_law(oracle_mod, case):
+    B, H, W, C, Co, KH, KW, D1, D2, D3, s, pad = case
+    assert oracle_mod.output_dims(H, W, KH, KW, s, pad) == ((H + 2 * pad - KH) // s + 1, (W + 2 * pad - KW) // s + 1)
+    # "same" capsule convolution: 3x3, stride 1, pad 1 keeps the spatial size
+    assert oracle_mod.output_dims(9, 7, 3, 3, 1, 1) == (9, 7)
+
+
+@pytest.mark.parametrize("case", PAD_CASES)
+def test_pad_equals_unpadded_on_zero_padded_input(oracle_mod, case):
+    B, H, W, C, Co, KH, KW, D1, D2, D3, s, pad = case
+    I, K, dO = _pad_inputs(case)
+    Ip = _zero_pad(I, pad)
+    O, _ = oracle_mod.fwd(I, K, s, pad)
+    Or, _ = oracle_mod.fwd(Ip, K, s)
+    np.testing.assert_allclose(O, Or, rtol=0, atol=1e-13)
+    # dK of the padded conv = dK of the plain conv on the padded input
+    dK, _ = oracle_mod.bwd_kernel(I, dO, s, KH, KW, pad)
+    dKr, _ = oracle_mod.bwd_kernel(Ip, dO, s, KH, KW)
+    np.testing.assert_allclose(dK, dKr, rtol=0, atol=1e-12)
+    # dI of the padded conv = the interior of dI of the plain conv on the padded grid
+    dI, _ = oracle_mod.bwd_data(dO, K, s, H, W, pad)
+    dIr, _ = oracle_mod.bwd_data(dO, K, s, H + 2 * pad, W + 2 * pad)
+    np.testing.assert_allclose(dI, dIr[:, pad:pad + H, pad:pad + W], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", PAD_CASES)
+def test_pad_adjoint_identities(oracle_mod, case):
+    """<fwd(I), dO> = <I, dI(dO)> = <K, dK(I, dO)> for the padded map."""
+    B, H, W, C, Co, KH, KW, D1, D2, D3, s, pad = case
+    I, K, dO = _pad_inputs(case)
+    O, _ = oracle_mod.fwd(I, K, s, pad)
+    dI, _ = oracle_mod.bwd_data(dO, K, s, H, W, pad)
+    dK, _ = oracle_mod.bwd_kernel(I, dO, s, KH, KW, pad)
+    a = float(np.sum(O * dO))
+    assert abs(a - float(np.sum(I * dI))) <= 1e-10 * max(1.0, abs(a))
+    assert abs(a - float(np.sum(K * dK))) <= 1e-10 * max(1.0, abs(a))
