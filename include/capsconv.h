@@ -152,6 +152,45 @@ CAPSCONV_API capsconv_status_t capsconv_bwd_kernel(capsconv_dtype_t dt,
         const void *I, const void *dO, float *dK,
         void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
 
+/* ---- Zero padding (SPEC.md:48-53 symmetric zero padding --
+ * the paper's own convolution has none).  Each call below is
+ * its unpadded namesake with one more extent, `pad` >= 0 (at most 2^20): the
+ * input is read through a view padded with `pad` zero pixels on every side of
+ * H and W, so Ho = (H + 2 pad - KH)/stride + 1, Wo likewise (KH <= H + 2 pad).
+ * Layouts, ownership, stream semantics and error behaviour are those of the
+ * unpadded calls; pad = 0 is exactly the unpadded call.  bwd_data returns dI
+ * for the real H x W pixels only (the padding has no gradient). */
+CAPSCONV_API capsconv_status_t capsconv_output_dims_pad(int64_t H, int64_t W, int64_t KH, int64_t KW,
+                                       int64_t stride, int64_t pad, int64_t *Ho, int64_t *Wo);
+
+CAPSCONV_API capsconv_status_t capsconv_workspace_bytes_pad(capsconv_op_t op, capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        size_t *bytes);
+
+CAPSCONV_API capsconv_status_t capsconv_select_path_pad(capsconv_op_t op, capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        capsconv_path_t *path);
+
+CAPSCONV_API capsconv_status_t capsconv_fwd_pad(capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        const void *I, const void *K, void *O,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+CAPSCONV_API capsconv_status_t capsconv_bwd_data_pad(capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        const void *dO, const void *K, void *dI,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+CAPSCONV_API capsconv_status_t capsconv_bwd_kernel_pad(capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        const void *I, const void *dO, float *dK,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
 /* Static description of a status code. */
 CAPSCONV_API const char *capsconv_status_string(capsconv_status_t status);
 

@@ -55,8 +55,16 @@ def load_library(path: Optional[str] = None):
         lib.capsconv_set_path_override.argtypes = [ctypes.c_int]
         for name in ("capsconv_fwd", "capsconv_bwd_data", "capsconv_bwd_kernel"):
             getattr(lib, name).argtypes = [ctypes.c_int] + ext + [vp, vp, vp, vp, sz, vp]
+        ext12 = [i64] * 12
+        lib.capsconv_output_dims_pad.argtypes = [i64] * 6 + [ctypes.POINTER(i64)] * 2
+        lib.capsconv_workspace_bytes_pad.argtypes = [ctypes.c_int, ctypes.c_int] + ext12 + [ctypes.POINTER(sz)]
+        lib.capsconv_select_path_pad.argtypes = [ctypes.c_int, ctypes.c_int] + ext12 + [ctypes.POINTER(ctypes.c_int)]
+        for name in ("capsconv_fwd_pad", "capsconv_bwd_data_pad", "capsconv_bwd_kernel_pad"):
+            getattr(lib, name).argtypes = [ctypes.c_int] + ext12 + [vp, vp, vp, vp, sz, vp]
         for name in ("capsconv_output_dims", "capsconv_workspace_bytes", "capsconv_select_path",
-                     "capsconv_set_path_override", "capsconv_fwd", "capsconv_bwd_data", "capsconv_bwd_kernel"):
+                     "capsconv_set_path_override", "capsconv_fwd", "capsconv_bwd_data", "capsconv_bwd_kernel",
+                     "capsconv_output_dims_pad", "capsconv_workspace_bytes_pad", "capsconv_select_path_pad",
+                     "capsconv_fwd_pad", "capsconv_bwd_data_pad", "capsconv_bwd_kernel_pad"):
             getattr(lib, name).restype = ctypes.c_int
         lib.capsconv_status_string.argtypes = [ctypes.c_int]
         lib.capsconv_status_string.restype = ctypes.c_char_p
@@ -89,13 +97,14 @@ def launch_count() -> int:
 _dims_cache = {}
 
 
-def output_dims(H: int, W: int, KH: int, KW: int, stride: int) -> Tuple[int, int]:
-    key = (H, W, KH, KW, stride)
+def output_dims(H: int, W: int, KH: int, KW: int, stride: int, pad: int = 0) -> Tuple[int, int]:
+    key = (H, W, KH, KW, stride, pad)
     v = _dims_cache.get(key)
     if v is None:
         lib = load_library()
         ho, wo = ctypes.c_int64(), ctypes.c_int64()
-        _check(lib.capsconv_output_dims(H, W, KH, KW, stride, ctypes.byref(ho), ctypes.byref(wo)), "output_dims")
+        _check(lib.capsconv_output_dims_pad(H, W, KH, KW, stride, pad, ctypes.byref(ho), ctypes.byref(wo)),
+               "output_dims")
         v = _dims_cache[key] = (ho.value, wo.value)
     return v
 
@@ -109,13 +118,20 @@ def _dt(dtype) -> int:
 _ws_size_cache = {}
 
 
+def _ext12(ext):
+    """Extents (B,H,W,C,Cout,KH,KW,D1,D2,D3,stride[,pad]); pad defaults to 0."""
+    ext = tuple(ext)
+    return ext + (0,) if len(ext) == 11 else ext
+
+
 def workspace_bytes(op: int, dtype, ext) -> int:
-    key = (op, dtype, tuple(ext), _device_key())
+    ext = _ext12(ext)
+    key = (op, dtype, ext, _device_key())
     v = _ws_size_cache.get(key)
     if v is None:
         lib = load_library()
         out = ctypes.c_size_t()
-        _check(lib.capsconv_workspace_bytes(op, _dt(dtype), *ext, ctypes.byref(out)), "workspace_bytes")
+        _check(lib.capsconv_workspace_bytes_pad(op, _dt(dtype), *ext, ctypes.byref(out)), "workspace_bytes")
         v = _ws_size_cache[key] = out.value
     return v
 
@@ -127,7 +143,7 @@ def _device_key():
 def select_path(op: int, dtype, ext) -> int:
     lib = load_library()
     out = ctypes.c_int()
-    _check(lib.capsconv_select_path(op, _dt(dtype), *ext, ctypes.byref(out)), "select_path")
+    _check(lib.capsconv_select_path_pad(op, _dt(dtype), *_ext12(ext), ctypes.byref(out)), "select_path")
     return out.value
 
 
@@ -167,9 +183,10 @@ def _call(name: str, op: int, dtype, ext, a, b, out, stream: Optional[torch.cuda
     lib = load_library()
     s = stream if stream is not None else torch.cuda.current_stream(out.device)
     handle = s.cuda_stream
+    ext = _ext12(ext)
     need = workspace_bytes(op, dtype, ext)
     ws = _workspace(need, out.device, handle)
-    fn = getattr(lib, name)
+    fn = getattr(lib, name + "_pad")
     with torch.cuda.device(out.device):
         st = fn(_dt(dtype), *ext, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
@@ -179,8 +196,9 @@ def _call(name: str, op: int, dtype, ext, a, b, out, stream: Optional[torch.cuda
 
 
 def fwd(I: torch.Tensor, K: torch.Tensor, stride: int = 1, out: Optional[torch.Tensor] = None,
-        stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-    """O = capsule_conv(I, K, stride) (capsconv_fwd)."""
+        stream: Optional[torch.cuda.Stream] = None, pad: int = 0) -> torch.Tensor:
+    """O = capsule_conv(I, K, stride) (capsconv_fwd); pad > 0: symmetric zero
+    padding of H and W (capsconv_fwd_pad)."""
     dev = _need_cuda(I, K)
     if I.dim() != 6 or K.dim() != 6:
         raise ValueError("I must be (B,H,W,C,D1,D2) and K (KH,KW,C,Cout,D2,D3)")
@@ -188,51 +206,53 @@ def fwd(I: torch.Tensor, K: torch.Tensor, stride: int = 1, out: Optional[torch.T
     KH, KW, C2, Cout, D2b, D3 = K.shape
     if C2 != C or D2b != D2 or I.dtype != K.dtype:
         raise ValueError("I %s and K %s disagree" % (tuple(I.shape), tuple(K.shape)))
-    Ho, Wo = output_dims(H, W, KH, KW, stride)
+    Ho, Wo = output_dims(H, W, KH, KW, stride, pad)
     shape = (B, Ho, Wo, Cout, D1, D3)
     if out is None:
         out = torch.empty(shape, dtype=I.dtype, device=dev)
     elif tuple(out.shape) != shape or out.dtype != I.dtype:
         raise ValueError("out has the wrong shape/dtype")
-    ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride)
+    ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
     return _call("capsconv_fwd", OP_FWD, I.dtype, ext, I, K, out, stream)
 
 
 def bwd_data(dO: torch.Tensor, K: torch.Tensor, stride: int, H: int, W: int,
-             out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+             out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
+             pad: int = 0) -> torch.Tensor:
     """dI (capsconv_bwd_data)."""
     dev = _need_cuda(dO, K)
     B, Ho, Wo, Cout, D1, D3 = dO.shape
     KH, KW, C, Cout2, D2, D3b = K.shape
     if Cout2 != Cout or D3b != D3 or dO.dtype != K.dtype:
         raise ValueError("dO %s and K %s disagree" % (tuple(dO.shape), tuple(K.shape)))
-    if output_dims(H, W, KH, KW, stride) != (Ho, Wo):
-        raise ValueError("dO spatial extent does not match H, W, K and stride")
+    if output_dims(H, W, KH, KW, stride, pad) != (Ho, Wo):
+        raise ValueError("dO spatial extent does not match H, W, K, stride and pad")
     shape = (B, H, W, C, D1, D2)
     if out is None:
         out = torch.empty(shape, dtype=dO.dtype, device=dev)
     elif tuple(out.shape) != shape or out.dtype != dO.dtype:
         raise ValueError("out has the wrong shape/dtype")
-    ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride)
+    ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
     return _call("capsconv_bwd_data", OP_BWD_DATA, dO.dtype, ext, dO, K, out, stream)
 
 
 def bwd_kernel(I: torch.Tensor, dO: torch.Tensor, stride: int, KH: int, KW: int,
-               out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+               out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
+               pad: int = 0) -> torch.Tensor:
     """dK in float32 (capsconv_bwd_kernel)."""
     dev = _need_cuda(I, dO)
     B, H, W, C, D1, D2 = I.shape
     B2, Ho, Wo, Cout, D1b, D3 = dO.shape
     if B2 != B or D1b != D1 or I.dtype != dO.dtype:
         raise ValueError("I %s and dO %s disagree" % (tuple(I.shape), tuple(dO.shape)))
-    if output_dims(H, W, KH, KW, stride) != (Ho, Wo):
-        raise ValueError("dO spatial extent does not match H, W, K and stride")
+    if output_dims(H, W, KH, KW, stride, pad) != (Ho, Wo):
+        raise ValueError("dO spatial extent does not match H, W, K, stride and pad")
     shape = (KH, KW, C, Cout, D2, D3)
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=dev)
     elif tuple(out.shape) != shape or out.dtype != torch.float32:
         raise ValueError("out must be float32 of the kernel's shape")
-    ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride)
+    ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
     return _call("capsconv_bwd_kernel", OP_BWD_KERNEL, I.dtype, ext, I, dO, out, stream)
 
 
@@ -240,10 +260,11 @@ class CapsConvFunction(torch.autograd.Function):
     """autograd wrapper: forward = capsconv_fwd, backward = bwd_kernel + bwd_data."""
 
     @staticmethod
-    def forward(ctx, I, K, stride):
+    def forward(ctx, I, K, stride, pad=0):
         ctx.save_for_backward(I, K)
         ctx.stride = stride
-        return fwd(I, K, stride)
+        ctx.pad = pad
+        return fwd(I, K, stride, pad=pad)
 
     @staticmethod
     def backward(ctx, dO):
@@ -251,12 +272,13 @@ class CapsConvFunction(torch.autograd.Function):
         dO = dO.contiguous()
         dI = dK = None
         if ctx.needs_input_grad[1]:
-            dK = bwd_kernel(I, dO, ctx.stride, K.shape[0], K.shape[1]).to(K.dtype)
+            dK = bwd_kernel(I, dO, ctx.stride, K.shape[0], K.shape[1], pad=ctx.pad).to(K.dtype)
         if ctx.needs_input_grad[0]:
-            dI = bwd_data(dO, K, ctx.stride, I.shape[1], I.shape[2])
-        return dI, dK, None
+            dI = bwd_data(dO, K, ctx.stride, I.shape[1], I.shape[2], pad=ctx.pad)
+        return dI, dK, None, None
 
 
-def caps_conv2d(I: torch.Tensor, K: torch.Tensor, stride: int = 1) -> torch.Tensor:
-    """Differentiable capsule convolution."""
-    return CapsConvFunction.apply(I, K, stride)
+def caps_conv2d(I: torch.Tensor, K: torch.Tensor, stride: int = 1, pad: int = 0) -> torch.Tensor:
+    """Differentiable capsule convolution; pad: symmetric
+    zero padding."""
+    return CapsConvFunction.apply(I, K, stride, pad)

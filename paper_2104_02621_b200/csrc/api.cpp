@@ -67,21 +67,22 @@ static bool mul_ok(int64_t a, int64_t b, int64_t *out) {
 
 static capsconv_status_t make_problem(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
                                       int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
-                                      int64_t s, Problem *p) {
+                                      int64_t s, int64_t pad, Problem *p) {
     if (dt != CAPSCONV_F32 && dt != CAPSCONV_BF16) return fail(CAPSCONV_ERR_DTYPE, "unknown dtype %d", (int)dt);
     if (s < 1) return fail(CAPSCONV_ERR_STRIDE, "stride %lld < 1", (long long)s);
+    if (pad < 0 || pad > (1 << 20)) return fail(CAPSCONV_ERR_SHAPE, "padding %lld out of [0, 2^20]", (long long)pad);
     const int64_t ext[] = {B, H, W, C, Cout, KH, KW, D1, D2, D3};
     const char *names[] = {"B", "H", "W", "C", "Cout", "KH", "KW", "D1", "D2", "D3"};
     for (int i = 0; i < 10; ++i)
         if (ext[i] < 1) return fail(CAPSCONV_ERR_SHAPE, "extent %s = %lld < 1", names[i], (long long)ext[i]);
-    if (KH > H || KW > W)
-        return fail(CAPSCONV_ERR_SHAPE, "kernel %lldx%lld larger than input %lldx%lld", (long long)KH,
-                    (long long)KW, (long long)H, (long long)W);
+    if (KH > H + 2 * pad || KW > W + 2 * pad)
+        return fail(CAPSCONV_ERR_SHAPE, "kernel %lldx%lld larger than padded input %lldx%lld", (long long)KH,
+                    (long long)KW, (long long)(H + 2 * pad), (long long)(W + 2 * pad));
     p->dt = dt;
     p->B = B; p->H = H; p->W = W; p->C = C; p->Cout = Cout;
-    p->KH = KH; p->KW = KW; p->D1 = D1; p->D2 = D2; p->D3 = D3; p->s = s;
-    p->Ho = (H - KH) / s + 1;
-    p->Wo = (W - KW) / s + 1;
+    p->KH = KH; p->KW = KW; p->D1 = D1; p->D2 = D2; p->D3 = D3; p->s = s; p->pad = pad;
+    p->Ho = (H + 2 * pad - KH) / s + 1;
+    p->Wo = (W + 2 * pad - KW) / s + 1;
     // Element counts (and their byte sizes) must fit comfortably in int64.
     int64_t n = 1;
     const int64_t in_f[] = {B, H, W, C, D1, D2, 8};
@@ -141,40 +142,59 @@ using namespace capsconv;
 
 extern "C" {
 
-capsconv_status_t capsconv_output_dims(int64_t H, int64_t W, int64_t KH, int64_t KW, int64_t stride, int64_t *Ho,
-                                       int64_t *Wo) {
+capsconv_status_t capsconv_output_dims_pad(int64_t H, int64_t W, int64_t KH, int64_t KW, int64_t stride,
+                                           int64_t pad, int64_t *Ho, int64_t *Wo) {
     if (!Ho || !Wo) return fail(CAPSCONV_ERR_NULL, "Ho/Wo output pointer is NULL");
     if (stride < 1) return fail(CAPSCONV_ERR_STRIDE, "stride %lld < 1", (long long)stride);
-    if (H < 1 || W < 1 || KH < 1 || KW < 1 || KH > H || KW > W)
-        return fail(CAPSCONV_ERR_SHAPE, "invalid spatial extents H=%lld W=%lld KH=%lld KW=%lld", (long long)H,
-                    (long long)W, (long long)KH, (long long)KW);
-    *Ho = (H - KH) / stride + 1;
-    *Wo = (W - KW) / stride + 1;
+    if (pad < 0 || pad > (1 << 20)) return fail(CAPSCONV_ERR_SHAPE, "padding %lld out of [0, 2^20]", (long long)pad);
+    if (H < 1 || W < 1 || KH < 1 || KW < 1 || KH > H + 2 * pad || KW > W + 2 * pad)
+        return fail(CAPSCONV_ERR_SHAPE, "invalid spatial extents H=%lld W=%lld KH=%lld KW=%lld pad=%lld",
+                    (long long)H, (long long)W, (long long)KH, (long long)KW, (long long)pad);
+    *Ho = (H + 2 * pad - KH) / stride + 1;
+    *Wo = (W + 2 * pad - KW) / stride + 1;
+    return CAPSCONV_OK;
+}
+
+capsconv_status_t capsconv_output_dims(int64_t H, int64_t W, int64_t KH, int64_t KW, int64_t stride, int64_t *Ho,
+                                       int64_t *Wo) {
+    return capsconv_output_dims_pad(H, W, KH, KW, stride, 0, Ho, Wo);
+}
+
+capsconv_status_t capsconv_workspace_bytes_pad(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H,
+                                               int64_t W, int64_t C, int64_t Cout, int64_t KH, int64_t KW,
+                                               int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+                                               size_t *bytes) {
+    if (!bytes) return fail(CAPSCONV_ERR_NULL, "bytes pointer is NULL");
+    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
+    Problem p;
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p);
+    if (st) return st;
+    *bytes = workspace_for(op, p);
     return CAPSCONV_OK;
 }
 
 capsconv_status_t capsconv_workspace_bytes(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W,
                                            int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2,
                                            int64_t D3, int64_t stride, size_t *bytes) {
-    if (!bytes) return fail(CAPSCONV_ERR_NULL, "bytes pointer is NULL");
+    return capsconv_workspace_bytes_pad(op, dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, 0, bytes);
+}
+
+capsconv_status_t capsconv_select_path_pad(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W,
+                                           int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2,
+                                           int64_t D3, int64_t stride, int64_t pad, capsconv_path_t *path) {
+    if (!path) return fail(CAPSCONV_ERR_NULL, "path pointer is NULL");
     if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
     Problem p;
-    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, &p);
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p);
     if (st) return st;
-    *bytes = workspace_for(op, p);
+    *path = choose_path(op, p);
     return CAPSCONV_OK;
 }
 
 capsconv_status_t capsconv_select_path(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W,
                                        int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2,
                                        int64_t D3, int64_t stride, capsconv_path_t *path) {
-    if (!path) return fail(CAPSCONV_ERR_NULL, "path pointer is NULL");
-    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
-    Problem p;
-    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, &p);
-    if (st) return st;
-    *path = choose_path(op, p);
-    return CAPSCONV_OK;
+    return capsconv_select_path_pad(op, dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, 0, path);
 }
 
 capsconv_status_t capsconv_set_path_override(capsconv_path_t path) {
@@ -186,7 +206,7 @@ capsconv_status_t capsconv_set_path_override(capsconv_path_t path) {
 
 #define CAPSCONV_PROLOGUE(OP, A, B_, OUT)                                                                     \
     Problem p;                                                                                                \
-    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, &p);                \
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p);           \
     if (st) return st;                                                                                        \
     if (!(A) || !(B_) || !(OUT)) return fail(CAPSCONV_ERR_NULL, "a tensor pointer is NULL");                  \
     const size_t need = workspace_for(OP, p);                                                                 \
@@ -199,33 +219,57 @@ capsconv_status_t capsconv_set_path_override(capsconv_path_t path) {
     const bool mma = choose_path(OP, p) == CAPSCONV_PATH_MMA && aligned16(A) && aligned16(B_) &&             \
                      aligned16(OUT) && (need == 0 || aligned16(workspace));
 
-capsconv_status_t capsconv_fwd(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
-                               int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
-                               const void *I, const void *K, void *O, void *workspace, size_t workspace_bytes,
-                               capsconv_stream_t stream) {
+capsconv_status_t capsconv_fwd_pad(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                                   int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                                   int64_t pad, const void *I, const void *K, void *O, void *workspace,
+                                   size_t workspace_bytes, capsconv_stream_t stream) {
     CAPSCONV_PROLOGUE(CAPSCONV_OP_FWD, I, K, O)
     cudaError_t e = mma ? mma_fwd(p, I, K, O, workspace, workspace_bytes, cs) : simt_fwd(p, I, K, O, cs);
     return finish(e, "capsconv_fwd");
 }
 
-capsconv_status_t capsconv_bwd_data(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
-                                    int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
-                                    const void *dO, const void *K, void *dI, void *workspace,
-                                    size_t workspace_bytes, capsconv_stream_t stream) {
+capsconv_status_t capsconv_fwd(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                               int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                               const void *I, const void *K, void *O, void *workspace, size_t workspace_bytes,
+                               capsconv_stream_t stream) {
+    return capsconv_fwd_pad(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, 0, I, K, O, workspace, workspace_bytes,
+                            stream);
+}
+
+capsconv_status_t capsconv_bwd_data_pad(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                        int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                                        int64_t stride, int64_t pad, const void *dO, const void *K, void *dI,
+                                        void *workspace, size_t workspace_bytes, capsconv_stream_t stream) {
     CAPSCONV_PROLOGUE(CAPSCONV_OP_BWD_DATA, dO, K, dI)
     cudaError_t e =
         mma ? mma_bwd_data(p, dO, K, dI, workspace, workspace_bytes, cs) : simt_bwd_data(p, dO, K, dI, cs);
     return finish(e, "capsconv_bwd_data");
 }
 
-capsconv_status_t capsconv_bwd_kernel(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
-                                      int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
-                                      int64_t stride, const void *I, const void *dO, float *dK, void *workspace,
-                                      size_t workspace_bytes, capsconv_stream_t stream) {
+capsconv_status_t capsconv_bwd_data(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                                    int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                                    const void *dO, const void *K, void *dI, void *workspace,
+                                    size_t workspace_bytes, capsconv_stream_t stream) {
+    return capsconv_bwd_data_pad(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, 0, dO, K, dI, workspace,
+                                 workspace_bytes, stream);
+}
+
+capsconv_status_t capsconv_bwd_kernel_pad(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                          int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                                          int64_t stride, int64_t pad, const void *I, const void *dO, float *dK,
+                                          void *workspace, size_t workspace_bytes, capsconv_stream_t stream) {
     CAPSCONV_PROLOGUE(CAPSCONV_OP_BWD_KERNEL, I, dO, dK)
     cudaError_t e = mma ? mma_bwd_kernel(p, I, dO, dK, workspace, workspace_bytes, cs)
                         : simt_bwd_kernel(p, I, dO, dK, workspace, workspace_bytes, cs);
     return finish(e, "capsconv_bwd_kernel");
+}
+
+capsconv_status_t capsconv_bwd_kernel(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                      int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                                      int64_t stride, const void *I, const void *dO, float *dK, void *workspace,
+                                      size_t workspace_bytes, capsconv_stream_t stream) {
+    return capsconv_bwd_kernel_pad(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, 0, I, dO, dK, workspace,
+                                   workspace_bytes, stream);
 }
 
 const char *capsconv_status_string(capsconv_status_t s) {

@@ -14,6 +14,7 @@ namespace capsconv {
 struct Problem {
     capsconv_dtype_t dt;
     int64_t B, H, W, C, Cout, KH, KW, D1, D2, D3, s;
+    int64_t pad;   // symmetric zero padding of H and W (0: the paper's valid convolution)
     int64_t Ho, Wo;
 
     size_t elem() const { return dt == CAPSCONV_BF16 ? 2 : 4; }

@@ -1052,6 +1052,7 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
 }  // namespace
 
 bool mma_supported(capsconv_op_t op, const Problem &p) {
+    if (p.pad != 0) return false;   // zero padding: SIMT path (tensor-core plans not extended yet)
     if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_supported(p);
     return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }

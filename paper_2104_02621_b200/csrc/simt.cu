@@ -77,6 +77,7 @@ template <> __device__ __forceinline__ void store_caps16<__nv_bfloat16>(__nv_bfl
 
 struct Dims {
     int64_t B, H, W, C, Cout, KH, KW, D1, D2, D3, s, Ho, Wo;
+    int64_t pad;   // symmetric zero padding: input pixel (x*s + p - pad, y*s + q - pad); outside = 0
 };
 
 // ============================================================ forward
@@ -100,8 +101,12 @@ __global__ void __launch_bounds__(128) fwd_d4(Dims d, const T *__restrict__ I, c
 #pragma unroll
         for (int e = 0; e < 16; ++e) acc[j][e] = 0.f;
     for (int64_t p = 0; p < d.KH; ++p) {
+        const int64_t h = x * d.s + p - d.pad;
+        if (h < 0 || h >= d.H) continue;
         for (int64_t q = 0; q < d.KW; ++q) {
-            const T *ip = I + (((b * d.H + x * d.s + p) * d.W + y * d.s + q) * d.C) * 16;
+            const int64_t w = y * d.s + q - d.pad;
+            if (w < 0 || w >= d.W) continue;
+            const T *ip = I + (((b * d.H + h) * d.W + w) * d.C) * 16;
             const T *kp = K + (((p * d.KW + q) * d.C) * d.Cout + co0) * 16;
             for (int64_t c = 0; c < d.C; ++c) {
                 float a[16];
@@ -145,7 +150,9 @@ __global__ void __launch_bounds__(256) fwd_gen(Dims d, const T *__restrict__ I, 
     float acc = 0.f;
     for (int64_t p = 0; p < d.KH; ++p)
         for (int64_t q = 0; q < d.KW; ++q) {
-            const T *ip = I + ((((b * d.H + x * d.s + p) * d.W + y * d.s + q) * d.C) * d.D1 + d1) * d.D2;
+            const int64_t h = x * d.s + p - d.pad, w = y * d.s + q - d.pad;
+            if (h < 0 || h >= d.H || w < 0 || w >= d.W) continue;
+            const T *ip = I + ((((b * d.H + h) * d.W + w) * d.C) * d.D1 + d1) * d.D2;
             const T *kp = K + ((((p * d.KW + q) * d.C) * d.Cout + co) * d.D2) * d.D3 + d3;
             for (int64_t c = 0; c < d.C; ++c)
                 for (int64_t t = 0; t < d.D2; ++t)
@@ -171,12 +178,12 @@ __global__ void __launch_bounds__(128) bwd_data_d4(Dims d, const T *__restrict__
 #pragma unroll
     for (int e = 0; e < 16; ++e) acc[e] = 0.f;
     for (int64_t p = 0; p < d.KH; ++p) {
-        const int64_t hx = h - p;
+        const int64_t hx = h + d.pad - p;
         if (hx < 0 || hx % d.s) continue;
         const int64_t x = hx / d.s;
         if (x >= d.Ho) continue;
         for (int64_t q = 0; q < d.KW; ++q) {
-            const int64_t wy = w - q;
+            const int64_t wy = w + d.pad - q;
             if (wy < 0 || wy % d.s) continue;
             const int64_t y = wy / d.s;
             if (y >= d.Wo) continue;
@@ -214,12 +221,12 @@ __global__ void __launch_bounds__(256) bwd_data_gen(Dims d, const T *__restrict_
     const int64_t b = r / d.H;
     float acc = 0.f;
     for (int64_t p = 0; p < d.KH; ++p) {
-        const int64_t hx = h - p;
+        const int64_t hx = h + d.pad - p;
         if (hx < 0 || hx % d.s) continue;
         const int64_t x = hx / d.s;
         if (x >= d.Ho) continue;
         for (int64_t q = 0; q < d.KW; ++q) {
-            const int64_t wy = w - q;
+            const int64_t wy = w + d.pad - q;
             if (wy < 0 || wy % d.s) continue;
             const int64_t y = wy / d.s;
             if (y >= d.Wo) continue;
@@ -258,8 +265,10 @@ __global__ void __launch_bounds__(128) bwd_kernel_d4(Dims d, const T *__restrict
         const int64_t y = rr % d.Wo; rr /= d.Wo;
         const int64_t x = rr % d.Ho;
         const int64_t b = rr / d.Ho;
+        const int64_t h = x * d.s + p - d.pad, w = y * d.s + q - d.pad;
+        if (h < 0 || h >= d.H || w < 0 || w >= d.W) continue;
         float a[16], g[16];
-        load_caps16<T>(I + (((b * d.H + x * d.s + p) * d.W + y * d.s + q) * d.C + c) * 16, a);
+        load_caps16<T>(I + (((b * d.H + h) * d.W + w) * d.C + c) * 16, a);
         load_caps16<T>(dO + (n * d.Cout + co) * 16, g);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -297,7 +306,9 @@ __global__ void __launch_bounds__(256) bwd_kernel_gen(Dims d, const T *__restric
         const int64_t y = rr % d.Wo; rr /= d.Wo;
         const int64_t x = rr % d.Ho;
         const int64_t b = rr / d.Ho;
-        const T *ip = I + ((((b * d.H + x * d.s + p) * d.W + y * d.s + q) * d.C + c) * d.D1) * d.D2 + t;
+        const int64_t h = x * d.s + p - d.pad, w = y * d.s + q - d.pad;
+        if (h < 0 || h >= d.H || w < 0 || w >= d.W) continue;
+        const T *ip = I + ((((b * d.H + h) * d.W + w) * d.C + c) * d.D1) * d.D2 + t;
         const T *gp = dO + ((n * d.Cout + co) * d.D1) * d.D3 + n3;
         for (int64_t i = 0; i < d.D1; ++i) acc = fmaf(ldf(ip + i * d.D2), ldf(gp + i * d.D3), acc);
     }
@@ -315,7 +326,7 @@ __global__ void __launch_bounds__(256) reduce_splits(const float *__restrict__ p
 }
 
 Dims dims_of(const Problem &p) {
-    return Dims{p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.Ho, p.Wo};
+    return Dims{p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.Ho, p.Wo, p.pad};
 }
 
 bool is_d4(const Problem &p) { return p.D1 == 4 && p.D2 == 4 && p.D3 == 4; }
