@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="stack", choices=["stack", "layer_s1", "layer_s2", "fc"])
+    ap.add_argument("--config", default="stack", choices=["stack", "stack_same", "layer_s1", "layer_s2", "fc"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce on the compute stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -59,6 +59,10 @@ def workload(cfg: str, world: int):
         specs = [LayerSpec(*l) for l in capsinputs.STACK_LAYERS]
         si = capsinputs.STACK_INPUT
         return specs, si["H"], si["W"], si["D"], capsinputs.STACK_BATCH, "capsnet_stack_3conv_fc_b1024"
+    if cfg == "stack_same":   # zero-padded ("same") 3x3 layers, SURVEY NEXT-2
+        specs = [LayerSpec(*l) for l in capsinputs.STACK_SAME_LAYERS]
+        si = capsinputs.STACK_INPUT
+        return specs, si["H"], si["W"], si["D"], capsinputs.STACK_BATCH, "capsnet_stack_same_pad1_b1024"
     L = capsinputs.CONFIGS[cfg]
     return [LayerSpec(L.C, L.Cout, L.KH, L.KW, L.stride)], L.H, L.W, L.D1, L.B, "single_layer_" + cfg
 
@@ -214,7 +218,7 @@ def run_reference(args, rank, world):
 
     def one(b):
         t0 = time.perf_counter()
-        oracle.stack_fwd_bwd(Xa[:b], Ks, strides, dYa[:b], dtype == torch.bfloat16)
+        oracle.stack_fwd_bwd(Xa[:b], Ks, strides[0], dYa[:b], dtype == torch.bfloat16, pads=strides[1])
         return time.perf_counter() - t0
 
     t1 = one(1)
@@ -240,7 +244,7 @@ def run_reference(args, rank, world):
 
 def stack_oracle_setup(specs, H, W, D, dtype):
     import oracle
-    layers, Ks, strides = [], [], []
+    layers, Ks, strides, pads = [], [], [], []
     h, w = H, W
     flops = 0
     for li, sp in enumerate(specs):
@@ -249,10 +253,11 @@ def stack_oracle_setup(specs, H, W, D, dtype):
         layers.append(L)
         Ks.append(capsinputs.make_kernel(L, dtype=dtype, layer_idx=li).to(torch.float64).numpy())
         strides.append(sp.stride)
-        ho, wo = oracle.output_dims(h, w, sp.KH, sp.KW, sp.stride)
+        pads.append(sp.pad)
+        ho, wo = oracle.output_dims(h, w, sp.KH, sp.KW, sp.stride, sp.pad)
         flops += 3 * 2 * ho * wo * D * sp.Cout * D * sp.KH * sp.KW * sp.C * D
         h, w = ho, wo
-    return flops, Ks, strides, layers
+    return flops, Ks, (strides, pads), layers
 
 
 def stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch):
@@ -261,7 +266,7 @@ def stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch):
     X = capsinputs.make_input(L0, dtype=dtype, batch=b).to(torch.float64).numpy()
     h, w = H, W
     for sp in specs:
-        h, w = oracle.output_dims(h, w, sp.KH, sp.KW, sp.stride)
+        h, w = oracle.output_dims(h, w, sp.KH, sp.KW, sp.stride, sp.pad)
     dY = capsinputs.make_grad_output((b, h, w, specs[-1].Cout, D, D), dtype=dtype, layer_idx=len(specs)).to(
         torch.float64).numpy()
     return X, dY
@@ -299,7 +304,7 @@ def main():
         L = capsinputs.Layer(B=gbatch, H=h, W=w, C=sp.C, Cout=sp.Cout, KH=sp.KH, KW=sp.KW, D1=D, D2=D, D3=D,
                              stride=sp.stride)
         weights.append(capsinputs.make_kernel(L, dtype=dtype, layer_idx=li))
-        h, w = pkg.output_dims(h, w, sp.KH, sp.KW, sp.stride)
+        h, w = pkg.output_dims(h, w, sp.KH, sp.KW, sp.stride, sp.pad)
     L0 = capsinputs.Layer(B=gbatch, H=H, W=W, C=specs[0].C, Cout=specs[0].Cout, KH=specs[0].KH, KW=specs[0].KW,
                           D1=D, D2=D, D3=D, stride=specs[0].stride)
     X_host = capsinputs.make_input(L0, dtype=dtype, batch_offset=lo, batch=batch).pin_memory()
@@ -476,12 +481,12 @@ def main():
             fl1, Ks, strides, layers = stack_oracle_setup(specs, H, W, D, dtype)
             Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, 1, dtype, gbatch)
             t0 = time.perf_counter()
-            oracle.stack_fwd_bwd(Xs, Ks, strides, dYs, dtype == torch.bfloat16)
+            oracle.stack_fwd_bwd(Xs, Ks, strides[0], dYs, dtype == torch.bfloat16, pads=strides[1])
             t1 = time.perf_counter() - t0
             b = int(max(1, min(gbatch, 10.0 / max(t1, 1e-6))))
             Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch)
             t0 = time.perf_counter()
-            oracle.stack_fwd_bwd(Xs, Ks, strides, dYs, dtype == torch.bfloat16)
+            oracle.stack_fwd_bwd(Xs, Ks, strides[0], dYs, dtype == torch.bfloat16, pads=strides[1])
             tb = time.perf_counter() - t0
             cpu = {"value": fl1 * b / tb / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
                    "sample": "oracle (C, fp64, OpenMP) %s fwd+bwd on %d of %d images, %.1f s" % (name, b, gbatch, tb)}
@@ -494,7 +499,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_max, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded capsinputs; random-init weights)",
             "config": {"workload": name, "global_batch": gbatch, "per_rank_batch": batch,
-                       "layers": ["%dx%d s%d %d->%d" % (s.KH, s.KW, s.stride, s.C, s.Cout) for s in specs],
+                       "layers": ["%dx%d s%d%s %d->%d" % (s.KH, s.KW, s.stride, " p%d" % s.pad if s.pad else "", s.C,
+                                                          s.Cout) for s in specs],
                        "input": "%dx%dx%d capsules %dx%d" % (H, W, specs[0].C, D, D),
                        "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
                        "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None,

@@ -76,6 +76,16 @@ STACK_LAYERS = [
     (32, 10, 8, 8, 1),
 ]
 
+# 6. the same stack with "same" zero padding on the 3x3 layers:
+#    24x24 -> 24x24 -> 12x12 -> 12x12 -> FC over the 12x12 map
+STACK_SAME_LAYERS = [
+    # (C, Cout, KH, KW, stride, pad)
+    (8, 8, 3, 3, 1, 1),
+    (8, 16, 3, 3, 2, 1),
+    (16, 32, 3, 3, 1, 1),
+    (32, 10, 12, 12, 1, 0),
+]
+
 
 def stack_layers(batch: int, out_hw) -> List[Layer]:
     """Materialise the stack for ``batch`` images.  ``out_hw(H, W, KH, KW, s)``

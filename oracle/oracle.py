@@ -167,7 +167,7 @@ def round_bf16(x) -> np.ndarray:
     return x
 
 
-def stack_fwd_bwd(X, Ks, strides, dY, bf16_boundaries: bool):
+def stack_fwd_bwd(X, Ks, strides, dY, bf16_boundaries: bool, pads=None):
     """Config-5 stack: layers composed with the identity between them
     (reading R17), forward then backward in reverse order.
 
@@ -175,10 +175,11 @@ def stack_fwd_bwd(X, Ks, strides, dY, bf16_boundaries: bool):
     propagated dI is rounded to bf16 where the GPU path stores bf16
     (reading R13).  Returns (outputs, dX, dKs, abs-sums dict).
     """
+    pads = list(pads) if pads is not None else [0] * len(Ks)
     acts = [_f64(X)]
     fabs_ = []
-    for K, s in zip(Ks, strides):
-        O, A = fwd(acts[-1], K, s)
+    for K, s, pd in zip(Ks, strides, pads):
+        O, A = fwd(acts[-1], K, s, pd)
         if bf16_boundaries:
             O = round_bf16(O)
         acts.append(O)
@@ -188,11 +189,11 @@ def stack_fwd_bwd(X, Ks, strides, dY, bf16_boundaries: bool):
     dKabs = [None] * len(Ks)
     dIabs = [None] * len(Ks)
     for li in range(len(Ks) - 1, -1, -1):
-        K, s = Ks[li], strides[li]
+        K, s, pd = Ks[li], strides[li], pads[li]
         x = acts[li]
-        dK, dKa = bwd_kernel(x, g, s, K.shape[0], K.shape[1])
+        dK, dKa = bwd_kernel(x, g, s, K.shape[0], K.shape[1], pd)
         dKs[li], dKabs[li] = dK, dKa
-        dI, dIa = bwd_data(g, K, s, x.shape[1], x.shape[2])
+        dI, dIa = bwd_data(g, K, s, x.shape[1], x.shape[2], pd)
         if bf16_boundaries:
             dI = round_bf16(dI)
         dIabs[li] = dIa

@@ -64,6 +64,9 @@ struct ConvMma {
     // segment of the window, boxes of h_box source rows x src_W pixels; a
     // per-item table maps window pixels to staged pixels (-1: zero)
     int stg_tall, h_box;
+    // zero padding: source (staging) coordinates are virtual - src_pad, output
+    // pixels are virtual - out_pad (fwd: src_pad = pad; dI: out_pad = pad)
+    int src_pad, out_pad;
     uint32_t tab_off;          // table offset from the dynamic smem base (npl * win_px int32)
     // ---- tensors
     const __nv_bfloat16 *src;  // A source, natural capsule layout, pixel = CS*16 elements

@@ -193,8 +193,8 @@ __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &
             for (int R = Ra; R <= Rb; ++R) {
                 const int b = floor_div(R, P.Hg);
                 const int Y = R - b * P.Hg;
-                tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px_bytes, &P.tmap, c0, P.pl_ox[k],
-                            P.pl_s * Y + P.pl_oy[k], b, mbar);
+                tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px_bytes, &P.tmap, c0, P.pl_ox[k] - P.src_pad,
+                            P.pl_s * Y + P.pl_oy[k] - P.src_pad, b, mbar);
                 bytes += (uint32_t)P.Wg * px_bytes;
             }
         }
@@ -485,10 +485,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                         const uint32_t rr = (uint32_t)u - b * HgWg;
                         const uint32_t Y = P.fd_Wg.div(rr);
                         const uint32_t X = rr - Y * (uint32_t)P.Wg;
-                        const int oy = P.og_s * (int)Y + P.og_oy[g];
-                        const int ox = P.og_s * (int)X + P.og_ox[g];
-                        valid = oy < P.out_H && ox < P.out_W;
-                        opix = ((size_t)b * P.out_H + oy) * P.out_W + ox;
+                        const int oy = P.og_s * (int)Y + P.og_oy[g] - P.out_pad;
+                        const int ox = P.og_s * (int)X + P.og_ox[g] - P.out_pad;
+                        valid = oy >= 0 && ox >= 0 && oy < P.out_H && ox < P.out_W;
+                        opix = valid ? ((size_t)b * P.out_H + oy) * P.out_W + ox : 0;
                     }
                 }
                 const uint32_t tcol = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(((abuf * P.gpi + gg) * P.G + gi) * P.N_tile);
@@ -682,9 +682,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ C
     const uint32_t Y = P.fd_Wg.div(rr);
     const uint32_t X = rr - Y * (uint32_t)P.Wg;
     const int g = 0;  // split-K is planned only for single-group problems
-    const int oy = P.og_s * (int)Y + P.og_oy[g];
-    const int ox = P.og_s * (int)X + P.og_ox[g];
-    if (oy >= P.out_H || ox >= P.out_W) return;
+    const int oy = P.og_s * (int)Y + P.og_oy[g] - P.out_pad;
+    const int ox = P.og_s * (int)X + P.og_ox[g] - P.out_pad;
+    if (oy < 0 || ox < 0 || oy >= P.out_H || ox >= P.out_W) return;
     const size_t rows_total = (size_t)P.n_mtiles * 128;
     const size_t ntot = (size_t)P.n_ntiles * P.N_tile;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -718,7 +718,9 @@ Plan make_plan(const Problem &p, bool dgrad) {
     Plan pl;
     ConvMma &P = pl.P;
     if (p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return pl;
-    const bool full_extent = (p.KH == p.H && p.KW == p.W);
+    const bool full_extent = (p.KH == p.H && p.KW == p.W && p.pad == 0);
+    P.src_pad = dgrad ? 0 : (int)p.pad;
+    P.out_pad = dgrad ? (int)p.pad : 0;
     const int s = (int)p.s;
     P.Bn = (int)p.B;
     int KWv, Cv, Coutv;
@@ -741,8 +743,9 @@ Plan make_plan(const Problem &p, bool dgrad) {
         if (s > 2 || p.KH * p.KW > kMaxTaps) return pl;
         if (dgrad && (p.KH < s || p.KW < s)) return pl;   // a dI phase with no taps
         KWv = (int)p.KW; Cv = (int)p.C; Coutv = (int)p.Cout;
-        P.Hg = ceil_div(p.H, s);
-        P.Wg = ceil_div(p.W, s);
+        // the virtual grid covers the zero-padded input (pad = 0: the input)
+        P.Hg = ceil_div(p.H + 2 * p.pad, s);
+        P.Wg = ceil_div(p.W + 2 * p.pad, s);
         if (!dgrad) {
             P.CS = (int)p.C; P.NCH = (int)p.Cout;
             P.src_H = (int)p.H; P.src_W = (int)p.W;
@@ -864,7 +867,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const bool bres = (gpi == P.nog && nchunks == 1 && P.n_ntiles == 1);
             // staging of the natural layout (whole virtual rows, or BB-image boxes)
             const bool batch_mode = (P.Hg * P.Wg == 1);
-            const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1;
+            const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1 && p.pad == 0;
             if (!batch_mode && !rows_mode && P.Wg * s > 256) continue;
             const int BB = std::min(win_px, 256);
             // tall boxes: unit-stride source planes outside batch/rows mode
@@ -872,6 +875,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
             // (only when a virtual-row box is small: <= 2.5 KB per TMA op is
             // op-rate bound, measured: L3 dI 146 -> 99 us; 3 KB rows are not)
             const bool tall_ok = !batch_mode && !rows_mode && P.pl_s == 1 && !no_tall && P.src_W <= 256 &&
+                                 p.pad == 0 &&
                                  P.Wg * cc * 32 <= 2560;
             const int nrows = (win_px - 1) / P.Wg + 2;
             const int nseg = (nrows - 1) / P.Hg + 2;
@@ -1016,10 +1020,10 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
 // microseconds; a training step calls the same shapes every iteration).
 struct PlanKey {
     int op, dt, dev, nsm;
-    int64_t e[11];
+    int64_t e[12];
     bool operator==(const PlanKey &o) const {
         if (op != o.op || dt != o.dt || dev != o.dev || nsm != o.nsm) return false;
-        for (int i = 0; i < 11; ++i)
+        for (int i = 0; i < 12; ++i)
             if (e[i] != o.e[i]) return false;
         return true;
     }
@@ -1029,7 +1033,7 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
     static std::mutex mu;
     static std::vector<std::pair<PlanKey, Plan>> cache;
     const DeviceInfo &di = device_info();
-    PlanKey k{dgrad ? 1 : 0, (int)p.dt, di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s}};
+    PlanKey k{dgrad ? 1 : 0, (int)p.dt, di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.pad}};
     std::lock_guard<std::mutex> lock(mu);
     for (auto &kv : cache)
         if (kv.first == k) return kv.second;
@@ -1052,7 +1056,6 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
 }  // namespace
 
 bool mma_supported(capsconv_op_t op, const Problem &p) {
-    if (p.pad != 0) return false;   // zero padding: SIMT path (tensor-core plans not extended yet)
     if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_supported(p);
     return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }

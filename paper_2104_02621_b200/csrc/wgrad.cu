@@ -114,6 +114,7 @@ struct WgradMma {
     // copy j read at virtual pixel u - j, side by side in N; D column block j
     // of a slot for tap (p, q) is the gradient of tap (p, q + s*j)
     int nq, KWv;
+    int pad;       // zero padding: input coordinates are virtual - pad (tensor-map boxes zero-fill outside)
     int b_pstep;                           // staged dO pixels per B-loader iteration (loader threads / (2*Cout))
     // bdesc: B holds ONE dO copy over KP + nq - 1 pixels; copy j is the same
     // buffer at descriptor offset (nq-1-j) pixels (64 B), one N = 4*Cout MMA per copy
@@ -162,7 +163,8 @@ __device__ __forceinline__ uint32_t w_stage_window(const WgradMma &P, const CUte
                 if (issue && (box_id & 31) == lane) {
                     const int b = floor_div(R, P.Hg);
                     const int Y = R - b * P.Hg;
-                    tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px, tm, c0, ox, cs * Y + oy, b, mbar);
+                    tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px, tm, c0, ox - P.pad, cs * Y + oy - P.pad, b,
+                                mbar);
                 }
                 ++box_id;
                 bytes += (uint32_t)P.Wg * px;
@@ -951,7 +953,8 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     WPlan pl;
     WgradMma &P = pl.P;
     if (p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return pl;
-    const bool fc = (p.KH == p.H && p.KW == p.W);
+    const bool fc = (p.KH == p.H && p.KW == p.W && p.pad == 0);
+    P.pad = (int)p.pad;
     const int s = fc ? 1 : (int)p.s;
     if (s > 2) return pl;
     P.s = s;
@@ -970,7 +973,8 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
         if (p.KH * p.KW > kMaxTaps) return pl;
         P.C = (int)p.C; P.Cout = (int)p.Cout;
         P.Bn = (int)p.B;
-        P.Hg = cdiv(p.H, s); P.Wg = cdiv(p.W, s); P.batch_mode = 0;
+        // the virtual grid covers the zero-padded input (pad = 0: the input)
+        P.Hg = cdiv(p.H + 2 * p.pad, s); P.Wg = cdiv(p.W + 2 * p.pad, s); P.batch_mode = 0;
         if (P.Wg * s > 256) return pl;
         P.ntaps = (int)(p.KH * p.KW);
         int plane_of[2][2] = {{-1, -1}, {-1, -1}}, npl = 0;
@@ -984,8 +988,9 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
         pl.I_B = p.B; pl.I_H = p.H; pl.I_W = p.W; pl.I_C = p.C;
         pl.O_B = p.B; pl.O_H = p.Ho; pl.O_W = p.Wo; pl.O_C = p.Cout;
     }
-    P.I_contig = (!fc && s == 1 && P.C <= 16) ? 1 : 0;
-    P.I_rows = (!fc && s == 2 && P.C <= 16) ? 1 : 0;
+    // contiguous input staging needs the virtual grid to be the input itself
+    P.I_contig = (!fc && s == 1 && P.C <= 16 && p.pad == 0) ? 1 : 0;
+    P.I_rows = (!fc && s == 2 && P.C <= 16 && p.pad == 0) ? 1 : 0;
     P.Hin = (int)p.H; P.Win = (int)p.W; P.Bin = (int)p.B;
     P.Ho = (int)pl.O_H; P.Wo = (int)pl.O_W;
     const long long vt = (long long)P.Bn * P.Hg * P.Wg;
@@ -1195,10 +1200,10 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
 
 struct WKey {
     int dev, nsm;
-    int64_t e[11];
+    int64_t e[12];
     bool operator==(const WKey &o) const {
         if (dev != o.dev || nsm != o.nsm) return false;
-        for (int i = 0; i < 11; ++i)
+        for (int i = 0; i < 12; ++i)
             if (e[i] != o.e[i]) return false;
         return true;
     }
@@ -1208,7 +1213,7 @@ const WPlan &cached_wplan(const Problem &p) {
     static std::mutex mu;
     static std::vector<std::pair<WKey, WPlan>> cache;
     const DeviceInfo &di = device_info();
-    WKey k{di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s}};
+    WKey k{di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.pad}};
     if (p.dt != CAPSCONV_BF16) k.e[7] = -1;
     std::lock_guard<std::mutex> lock(mu);
     for (auto &kv : cache)

@@ -32,6 +32,7 @@ class LayerSpec:
     KH: int
     KW: int
     stride: int
+    pad: int = 0      # symmetric zero padding
 
 
 def shard_range(global_batch: int, rank: int, world: int):
@@ -60,7 +61,7 @@ class CapsStack:
         self.hw = [(H, W)]
         for sp in self.specs:
             h, w = self.hw[-1]
-            self.hw.append(ops.output_dims(h, w, sp.KH, sp.KW, sp.stride))
+            self.hw.append(ops.output_dims(h, w, sp.KH, sp.KW, sp.stride, sp.pad))
         # static buffers (stable pointers: the step can be captured in a CUDA graph).
         # acts[0] is the caller's input itself when it already has the layer-0
         # layout (no copy); the static buffer is only used otherwise.
@@ -102,7 +103,7 @@ class CapsStack:
         self._bind_input(x)
         for li, sp in enumerate(self.specs):
             dst = self.acts[li + 1] if li + 1 < len(self.specs) else self.out
-            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst)
+            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst, pad=sp.pad)
         return self.out
 
     def backward(self, dy: torch.Tensor, timer=None) -> List[torch.Tensor]:
@@ -112,7 +113,7 @@ class CapsStack:
             sp = self.specs[li]
             h, w = self.hw[li]
             if timer: timer.begin(li, "dK")
-            self.ops.bwd_kernel(self.acts[li], g, sp.stride, sp.KH, sp.KW, out=self.dK[li])
+            self.ops.bwd_kernel(self.acts[li], g, sp.stride, sp.KH, sp.KW, out=self.dK[li], pad=sp.pad)
             if timer: timer.end(li, "dK")
             if self.world > 1:
                 if self.overlap:
@@ -123,7 +124,7 @@ class CapsStack:
                 else:
                     dist.all_reduce(self.dK[li], op=dist.ReduceOp.SUM, group=self.group)
             if timer: timer.begin(li, "dI")
-            self.ops.bwd_data(g, self.K[li], sp.stride, h, w, out=self.grads[li])
+            self.ops.bwd_data(g, self.K[li], sp.stride, h, w, out=self.grads[li], pad=sp.pad)
             if timer: timer.end(li, "dI")
             g = self.grads[li]
         if self.world > 1 and self.overlap:
@@ -138,6 +139,6 @@ class CapsStack:
         for li, sp in enumerate(self.specs):
             dst = self.acts[li + 1] if li + 1 < len(self.specs) else self.out
             timer.begin(li, "fwd")
-            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst)
+            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst, pad=sp.pad)
             timer.end(li, "fwd")
         return self.backward(dy, timer)

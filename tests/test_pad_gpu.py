@@ -86,6 +86,10 @@ def test_pad_exact(cc, oracle_mod, path, case):
     np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
     np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
     np.testing.assert_array_equal(to_np(dK), rdK)
+    if path == "auto" and KH <= 3:   # bf16 4x4 capsules with padding run on the tensor-core kernels
+        # (5x5 over 4 channels exceeds the dK slot capacity and takes SIMT for dK)
+        ext = (B, H, W, C, Co, KH, KW, 4, 4, 4, s, pad)
+        assert [cc.select_path(op, torch.bfloat16, ext) for op in (0, 1, 2)] == [cc.PATH_MMA] * 3
 
 
 def test_pad_zero_is_unpadded(cc):
@@ -121,3 +125,40 @@ def test_pad_validation(cc):
     with pytest.raises(cc.CapsConvError):
         cc.output_dims(2, 2, 7, 7, 1, 2)
     assert cc.output_dims(2, 2, 5, 5, 1, 2) == (2, 2)
+
+
+def _same_stack_layers(oracle_mod, batch):
+    si = capsinputs.STACK_INPUT
+    h, w = si["H"], si["W"]
+    out = []
+    for (C, Co, KH, KW, s, pad) in capsinputs.STACK_SAME_LAYERS:
+        out.append((batch, h, w, C, Co, KH, KW, s, pad))
+        h, w = oracle_mod.output_dims(h, w, KH, KW, s, pad)
+    return out
+
+
+@pytest.mark.parametrize("li", range(len(capsinputs.STACK_SAME_LAYERS)))
+def test_same_stack_layers_full_batch_exact(cc, oracle_mod, li):
+    """Each layer of the zero-padded stack (bench.py --config stack_same) at
+    global batch 1024, exact-integer inputs: bitwise equal to the oracle, on
+    the tensor-core path."""
+    case = _same_stack_layers(oracle_mod, capsinputs.STACK_BATCH)[li]
+    B, H, W, C, Co, KH, KW, s, pad = case
+    L = capsinputs.Layer(B, H, W, C, Co, KH, KW, 4, 4, 4, s)
+    I = capsinputs.make_input(L, "int1", torch.bfloat16, layer_idx=li)
+    K = capsinputs.make_kernel(L, "int1", torch.bfloat16, layer_idx=li)
+    Ho, Wo = oracle_mod.output_dims(H, W, KH, KW, s, pad)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "int1", torch.bfloat16, layer_idx=li)
+    ext = (B, H, W, C, Co, KH, KW, 4, 4, 4, s, pad)
+    assert [cc.select_path(op, torch.bfloat16, ext) for op in (0, 1, 2)] == [cc.PATH_MMA] * 3
+    Id, Kd, dOd = I.to(DEV), K.to(DEV), dO.to(DEV)
+    O = cc.fwd(Id, Kd, s, pad=pad)
+    dI = cc.bwd_data(dOd, Kd, s, H, W, pad=pad)
+    dK = cc.bwd_kernel(Id, dOd, s, KH, KW, pad=pad)
+    torch.cuda.synchronize()
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), s, pad)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), s, H, W, pad)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), s, KH, KW, pad)
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)

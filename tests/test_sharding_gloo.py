@@ -29,24 +29,24 @@ class OracleOps:
     """Compute backend shim with the binding's signatures (test only)."""
 
     @staticmethod
-    def output_dims(H, W, KH, KW, s):
-        return oracle.output_dims(H, W, KH, KW, s)
+    def output_dims(H, W, KH, KW, s, pad=0):
+        return oracle.output_dims(H, W, KH, KW, s, pad)
 
     @staticmethod
-    def fwd(I, K, stride, out=None):
-        O, _ = oracle.fwd(I.numpy(), K.numpy(), stride)
+    def fwd(I, K, stride, out=None, pad=0):
+        O, _ = oracle.fwd(I.numpy(), K.numpy(), stride, pad)
         out.copy_(torch.from_numpy(O))
         return out
 
     @staticmethod
-    def bwd_data(dO, K, stride, H, W, out=None):
-        dI, _ = oracle.bwd_data(dO.numpy(), K.numpy(), stride, H, W)
+    def bwd_data(dO, K, stride, H, W, out=None, pad=0):
+        dI, _ = oracle.bwd_data(dO.numpy(), K.numpy(), stride, H, W, pad)
         out.copy_(torch.from_numpy(dI))
         return out
 
     @staticmethod
-    def bwd_kernel(I, dO, stride, KH, KW, out=None):
-        dK, _ = oracle.bwd_kernel(I.numpy(), dO.numpy(), stride, KH, KW)
+    def bwd_kernel(I, dO, stride, KH, KW, out=None, pad=0):
+        dK, _ = oracle.bwd_kernel(I.numpy(), dO.numpy(), stride, KH, KW, pad)
         out.copy_(torch.from_numpy(dK))
         return out
 
@@ -130,3 +130,22 @@ def test_single_process_stack_matches_oracle():
     for li in range(len(SPECS)):
         np.testing.assert_allclose(dKs[li].numpy(), rdKs[li], rtol=1e-12, atol=1e-12)
     assert st.step_flops() == 3 * sum(st.layer_flops(i) for i in range(len(SPECS)))
+
+
+def test_single_process_padded_stack_matches_oracle():
+    """The stack driver threads each layer's zero padding."""
+    specs = [LayerSpec(2, 3, 3, 3, 1, 1), LayerSpec(3, 2, 3, 3, 2, 1), LayerSpec(2, 2, 4, 4, 1, 0)]
+    g = torch.Generator().manual_seed(11)
+    weights = [torch.rand((s.KH, s.KW, s.C, s.Cout, D, D), generator=g, dtype=torch.float64) - 0.5 for s in specs]
+    X = torch.rand((GB, H, W, specs[0].C, D, D), generator=g, dtype=torch.float64) - 0.5
+    h, w = H, W
+    for s in specs:
+        h, w = oracle.output_dims(h, w, s.KH, s.KW, s.stride, s.pad)
+    dY = torch.rand((GB, h, w, specs[-1].Cout, D, D), generator=g, dtype=torch.float64) - 0.5
+    st = CapsStack(specs, H, W, D, GB, weights, "cpu", ops=OracleOps)
+    dKs = st.step(X, dY)
+    acts, dX, rdKs, _ = oracle.stack_fwd_bwd(X.numpy(), [w_.numpy() for w_ in weights], [s.stride for s in specs],
+                                             dY.numpy(), False, pads=[s.pad for s in specs])
+    np.testing.assert_allclose(st.out.numpy(), acts[-1], rtol=1e-12, atol=1e-12)
+    for li in range(len(specs)):
+        np.testing.assert_allclose(dKs[li].numpy(), rdKs[li], rtol=1e-12, atol=1e-12)
