@@ -114,6 +114,7 @@ struct WgradMma {
     // copy j read at virtual pixel u - j, side by side in N; D column block j
     // of a slot for tap (p, q) is the gradient of tap (p, q + s*j)
     int nq, KWv;
+    int tiles_uniform;   // FC view with more tiles than the table holds: tile mt = tile[0] shifted by 32*mt channels
     int pad;       // zero padding: input coordinates are virtual - pad (tensor-map boxes zero-fill outside)
     int b_pstep;                           // staged dO pixels per B-loader iteration (loader threads / (2*Cout))
     // bdesc: B holds ONE dO copy over KP + nq - 1 pixels; copy j is the same
@@ -450,11 +451,12 @@ __device__ __forceinline__ void w_lane_setup(const WgradMma &P, int g, int q, in
         L.loff[tt] = 0;
         L.sp0[tt] = 0;
         if (tt >= L.ntl) continue;
-        const WTile &T = P.tile[g * P.TG + tt];
+        const WTile &T = P.tile[P.tiles_uniform ? 0 : g * P.TG + tt];
+        const int cshift = P.tiles_uniform ? (g * P.TG + tt) * 32 : 0;
         for (int j = 0; j < T.nslots; ++j) {
             const WSlot &S = T.slot[j];
             if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
-                const int c = S.c0 + ((row - S.row0) >> 2);
+                const int c = S.c0 + cshift + ((row - S.row0) >> 2);
                 if (c >= P.C) break;
                 int k = 0;
                 while (P.g_plane[g][k] != S.plane) ++k;
@@ -773,13 +775,14 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                     const int tt = unit / nch, n0 = (unit - tt * nch) * 16;
                     if (tt != cur_tt) {
                         cur_tt = tt;
-                        const WTile &T = P.tile[g * P.TG + tt];
+                        const WTile &T = P.tile[P.tiles_uniform ? 0 : g * P.TG + tt];
+                        const int cshift = P.tiles_uniform ? (g * P.TG + tt) * 32 : 0;
                         tap = -1; c = 0;
                         for (int j = 0; j < T.nslots; ++j) {
                             const WSlot &S = T.slot[j];
                             if (row >= S.row0 && row < S.row0 + 4 * S.cn) {
                                 tap = S.tap;
-                                c = S.c0 + ((row - S.row0) >> 2);
+                                c = S.c0 + cshift + ((row - S.row0) >> 2);
                             }
                         }
                         // column n = (block, c', d3); block bi is shift j of the slot's tap (p, q)
@@ -1058,7 +1061,13 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
                 tiles.push_back(T);
             }
     }
-    if ((int)tiles.size() > kWMaxTiles) return pl;
+    // FC view (one tap, 32-channel tiles): beyond the table's capacity the
+    // tiles are uniform and computed from tile 0 in the kernel
+    P.tiles_uniform = 0;
+    if ((int)tiles.size() > kWMaxTiles) {
+        if (!fc || tiles[0].nslots != 1 || tiles[0].slot[0].cn != 32) return pl;
+        P.tiles_uniform = 1;
+    }
     P.n_mtiles = (int)tiles.size();
     for (int i = 0; i < P.n_mtiles; ++i) {
         WTile &T = tiles[i];
@@ -1071,7 +1080,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             T.span[k] = std::max(T.span[k], T.slot[j].shift);
         }
         for (int k = 0; k < T.np; ++k) T.span[k] -= T.minsh[k];
-        P.tile[i] = T;
+        if (i < kWMaxTiles) P.tile[i] = T;
     }
     const int nsm = device_info().num_sms;
     P.CBO = std::min(16, P.Cout);
@@ -1083,12 +1092,13 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     for (int TG = std::min(P.n_mtiles, kWMaxTG); TG >= 1 && !found; --TG) {
         if (force_tg && TG != force_tg) continue;
         const int ngroups = cdiv(P.n_mtiles, TG);
+        if (ngroups > kWMaxTiles) continue;   // per-group tables hold kWMaxTiles entries
         // group unions
         int gmax_np = 1, gmax_span = 0, gmax_ci = 0, gmax_msh = 0;
         for (int g = 0; g < ngroups; ++g) {
             int np = 0, plane[4], mn[4], mx[4], clo = 1 << 30, chi = 0;
             for (int mt = g * TG; mt < std::min(P.n_mtiles, (g + 1) * TG); ++mt) {
-                const WTile &T = P.tile[mt];
+                const WTile &T = tiles[mt];
                 clo = std::min(clo, T.c_lo); chi = std::max(chi, T.c_hi);
                 for (int j = 0; j < T.nslots; ++j) {
                     int k = 0;
