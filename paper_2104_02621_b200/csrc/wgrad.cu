@@ -198,12 +198,19 @@ __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint
 
 // stride-2 rows mode: global input rows [rA, rB] covering every plane window
 // of the stage (virtual rows R = b*Hg + Y map to input rows b*H + 2Y + a)
+// rows mode: global input rows [rA, rB] covering every plane window of the
+// stage (virtual row Y of image b is input row s*Y + oy - pad of plane oy;
+// rows outside the image are padding and are not staged)
 __device__ __forceinline__ void w_in_rows(const WgradMma &P, int wlo, int whi, int &rA, int &rB) {
     const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
     const uint32_t bA = P.fd_HgWg.div((uint32_t)wlo), bB = P.fd_HgWg.div((uint32_t)whi);
     const int YA = (int)P.fd_Wg.div((uint32_t)wlo - bA * HgWg), YB = (int)P.fd_Wg.div((uint32_t)whi - bB * HgWg);
-    rA = (int)bA * P.Hin + 2 * YA;
-    rB = min((int)bB * P.Hin + 2 * YB + 1, P.Bin * P.Hin - 1);
+    // a window starting in the bottom padding of image bA starts at row 0 of
+    // bA + 1; one ending in the top padding of bB ends at the last row of bB - 1
+    const int ylo = P.s * YA - P.pad, yhi = P.s * YB + P.s - 1 - P.pad;
+    rA = ylo >= P.Hin ? ((int)bA + 1) * P.Hin : (int)bA * P.Hin + max(0, ylo);
+    rB = yhi < 0 ? (int)bB * P.Hin - 1 : (int)bB * P.Hin + min(P.Hin - 1, yhi);
+    rB = min(rB, P.Bin * P.Hin - 1);
     if (rB < rA) rB = rA - 1;
 }
 
@@ -497,8 +504,8 @@ __device__ __forceinline__ void w_build_table(const WgradMma &P, const WGroup &G
                 const uint32_t rr = (uint32_t)v - b * HgWg;
                 const uint32_t Y = P.fd_Wg.div(rr);
                 const uint32_t X = rr - Y * (uint32_t)P.Wg;
-                const int y = 2 * (int)Y + G.oy[k], x = 2 * (int)X + G.ox[k];
-                if (y < P.Hin && x < P.Win) idx = ((int)b * P.Hin + y - rA) * P.Win + x;
+                const int y = P.s * (int)Y + G.oy[k] - P.pad, x = P.s * (int)X + G.ox[k] - P.pad;
+                if (y >= 0 && x >= 0 && y < P.Hin && x < P.Win) idx = ((int)b * P.Hin + y - rA) * P.Win + x;
             }
         }
         asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(tab + (uint32_t)e * 4u), "r"(idx) : "memory");
@@ -993,7 +1000,8 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     }
     // contiguous input staging needs the virtual grid to be the input itself
     P.I_contig = (!fc && s == 1 && P.C <= 16 && p.pad == 0) ? 1 : 0;
-    P.I_rows = (!fc && s == 2 && P.C <= 16 && p.pad == 0) ? 1 : 0;
+    // whole input rows + a plane table: stride 2, or any padded layer
+    P.I_rows = (!fc && (s == 2 || p.pad > 0) && P.C <= 16) ? 1 : 0;
     P.Hin = (int)p.H; P.Win = (int)p.W; P.Bin = (int)p.B;
     P.Ho = (int)pl.O_H; P.Wo = (int)pl.O_W;
     const long long vt = (long long)P.Bn * P.Hg * P.Wg;
@@ -1130,7 +1138,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             const uint32_t acc = (uint32_t)(TG * P.N_tile);
             const uint32_t abuf = (uint32_t)(2 * TG * KP);      // TG tiles x KP/4 k-steps x 8 columns
             // rows mode: both parities of every virtual row the union window touches
-            const int rows_mode_cap = 2 * ((KP + gmax_span + gmax_msh - 1) / P.Wg + 2) * P.Win;
+            const int rows_mode_cap = s * ((KP + gmax_span + gmax_msh - 1) / P.Wg + 2) * P.Win;
             const int capI = P.batch_mode ? KP
                              : P.I_contig ? KP + gmax_span
                              : P.I_rows   ? rows_mode_cap

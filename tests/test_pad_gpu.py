@@ -21,6 +21,8 @@ CASES = [
     (2, 6, 5, 4, 4, 5, 5, 1, 2),        # "same" 5x5, ragged C
     (1, 5, 5, 3, 2, 3, 3, 2, 1),        # odd channels
     (34, 12, 12, 8, 8, 3, 3, 1, 1),     # several M tiles, ragged tail
+    (2, 9, 9, 16, 32, 3, 3, 1, 2),      # windows starting/ending inside padding rows
+    (2, 10, 11, 8, 16, 3, 3, 2, 2),     # stride 2, pad 2
 ]
 
 
