@@ -75,12 +75,17 @@ __device__ __forceinline__ int staging_off(const ConvMma &P, int v0) {
 // of every plane (virtual row R = b*Hg + Y -> input rows b*H + 2Y + a)
 __device__ __forceinline__ void conv_in_rows(const ConvMma &P, int v0, int &rA, int &rB) {
     const int wlo = max(v0, 0), whi = min(v0 + P.win_px, P.Bn * P.Hg * P.Wg) - 1;
-    const int Ra = wlo / P.Wg, Rb = whi / P.Wg;
-    const int bA = Ra / P.Hg, YA = Ra - bA * P.Hg;
-    const int bB = Rb / P.Hg, YB = Rb - bB * P.Hg;
-    rA = bA * P.Hin + 2 * YA;
-    rB = min(bB * P.Hin + 2 * YB + 1, P.Bin * P.Hin - 1);
-    if (whi < wlo) rB = rA - 1;
+    const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
+    const uint32_t bA = P.fd_HgWg.div((uint32_t)wlo), bB = P.fd_HgWg.div((uint32_t)max(whi, 0));
+    const int YA = (int)P.fd_Wg.div((uint32_t)wlo - bA * HgWg), YB = (int)P.fd_Wg.div((uint32_t)max(whi, 0) - bB * HgWg);
+    // input rows 2Y + a - pad of both parities; rows inside the padding are not
+    // staged (a window starting in the bottom padding of image bA starts at
+    // row 0 of bA + 1, one ending in the top padding of bB ends in bB - 1)
+    const int ylo = 2 * YA - P.src_pad, yhi = 2 * YB + 1 - P.src_pad;
+    rA = ylo >= P.Hin ? ((int)bA + 1) * P.Hin : (int)bA * P.Hin + max(0, ylo);
+    rB = yhi < 0 ? (int)bB * P.Hin - 1 : (int)bB * P.Hin + min(P.Hin - 1, yhi);
+    rB = min(rB, P.Bin * P.Hin - 1);
+    if (whi < wlo || rB < rA) rB = rA - 1;
 }
 
 // Tall-box staging: the window's source rows, image by image.  Segment of
@@ -242,8 +247,8 @@ __device__ __forceinline__ void build_table(const ConvMma &P, const Item &it, ui
             const uint32_t rr = (uint32_t)v - b * HgWg;
             const uint32_t Y = P.fd_Wg.div(rr);
             const uint32_t X = rr - Y * (uint32_t)P.Wg;
-            const int y = 2 * (int)Y + P.pl_oy[k], x = 2 * (int)X + P.pl_ox[k];
-            if (y < P.Hin && x < P.Win) idx = ((int)b * P.Hin + y - rA) * P.Win + x;
+            const int y = 2 * (int)Y + P.pl_oy[k] - P.src_pad, x = 2 * (int)X + P.pl_ox[k] - P.src_pad;
+            if (y >= 0 && x >= 0 && y < P.Hin && x < P.Win) idx = ((int)b * P.Hin + y - rA) * P.Win + x;
         }
         asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(tab + (uint32_t)e * 4u), "r"(idx) : "memory");
     }
@@ -867,7 +872,9 @@ Plan make_plan(const Problem &p, bool dgrad) {
             const bool bres = (gpi == P.nog && nchunks == 1 && P.n_ntiles == 1);
             // staging of the natural layout (whole virtual rows, or BB-image boxes)
             const bool batch_mode = (P.Hg * P.Wg == 1);
-            const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1 && p.pad == 0;
+            // (whole rows are staged in the natural layout: the pixel stride is
+            // CS*32 bytes, so the channel count must equal the padded chunk)
+            const bool rows_mode = !dgrad && !full_extent && s == 2 && nchunks == 1 && P.CS == P.CSpad;
             if (!batch_mode && !rows_mode && P.Wg * s > 256) continue;
             const int BB = std::min(win_px, 256);
             // tall boxes: unit-stride source planes outside batch/rows mode
