@@ -1,0 +1,269 @@
+// fc_hmma.cu -- the fully-connected capsule layer (R18: a full-extent
+// capsule convolution viewed as 1x1 over C = KH*KW*Cin channels) on warp-level
+// mma.sync tensor-core instructions, reading the natural capsule layout
+// directly into register fragments.
+//
+// Why not tcgen05 here: the FC passes are streaming GEMMs (forward: M = B*4,
+// K = 4*C = 8192, N = 4*Cout = 40; 40 flop/byte, HBM-bound at ~260 TFLOP/s,
+// well inside the ~550 TFLOP/s legacy HMMA sustains on B200, tests/probe/
+// hmma_probe.cu).  The m16n8k16 A fragment's k-pairs are (d2, d2+1) of one
+// capsule row -- 4 contiguous bytes of I[b][c][d1][d2] -- so the operand
+// needs no shared-memory staging or D1 repack at all, which is what bounds the
+// tcgen05 path on this layer (producer repack and split-K bookkeeping).
+//
+//   O[b, c', d1, d3] = sum_{c, d2} I[b, c, d1, d2] * K[c, c', d2, d3]
+//   rows m = (b, d1), k = (c, d2), columns n = (c', d3)        (R18)
+//
+// Work: CTA = (K split ks, block of 8 warps x 2 m-tiles); each warp keeps
+// 2 x ceil(N/8) accumulator fragments over its K range; the K slice of the
+// weights (prepacked in fragment order) sits in shared memory.  Split
+// partials are summed in a fixed order by fc_finalize (deterministic).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace capsconv {
+namespace {
+
+constexpr int kFcWarps = 8;
+constexpr int kFcMt = 2;          // m-tiles (16 rows) per warp
+constexpr int kFcMaxNt = 8;       // n-tiles of 8 columns (N <= 64)
+
+struct FcPlan {
+    bool ok = false;
+    int B, C, Cout, NT;           // NT = n-tiles of 8
+    int ksteps;                   // K steps of 16 (4 channels)
+    int ksplit, kslice;           // K splits, k-steps per split
+    int mblocks;                  // M blocks of kFcWarps * kFcMt * 16 rows
+    size_t wpack_bytes, part_bytes;
+    uint32_t smem;
+};
+
+FcPlan fc_plan(const Problem &p) {
+    FcPlan f;
+    const bool full = p.KH == p.H && p.KW == p.W && p.pad == 0;
+    if (!full || p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return f;
+    f.B = (int)p.B;
+    f.C = (int)(p.KH * p.KW * p.C);
+    f.Cout = (int)p.Cout;
+    f.NT = (int)((p.Cout * 4 + 7) / 8);
+    if (f.NT > kFcMaxNt || f.C % 4 != 0 || p.B > (1 << 24)) return f;
+    f.ksteps = f.C / 4;
+    const int rows = f.B * 4;
+    f.mblocks = (rows + kFcWarps * kFcMt * 16 - 1) / (kFcWarps * kFcMt * 16);
+    // K splits: one wave of two CTAs per SM (a partial second wave doubles the
+    // kernel time), slices of at most 64 k-steps (weight slice <= 64*NT*256 B)
+    const int nsm = device_info().num_sms;
+    int ks = std::max(1, (2 * nsm) / f.mblocks);
+    ks = std::max(ks, (f.ksteps + 63) / 64);
+    ks = std::min(ks, f.ksteps);
+    f.kslice = (f.ksteps + ks - 1) / ks;
+    f.ksplit = (f.ksteps + f.kslice - 1) / f.kslice;
+    f.smem = (uint32_t)f.kslice * f.NT * 256u;
+    f.wpack_bytes = ((size_t)f.ksteps * f.NT * 256 + 255) & ~(size_t)255;
+    f.part_bytes = ((size_t)f.ksplit * rows * f.NT * 8 * 4 + 255) & ~(size_t)255;
+    f.ok = true;
+    return f;
+}
+
+// Fragment k order.  The MMA's k index inside a 16-step may be any
+// permutation shared by A and B; here fragment k-pair (2t, 2t+1) is
+// (channel 4*kstep + t, d2 0..1) and (2t+8, 2t+9) is (same channel, d2 2..3),
+// and fragment rows g, g+8 are capsule rows d1 = 2(g%2), 2(g%2)+1 of image g/2:
+// a thread's whole A fragment is then the 16 contiguous bytes
+// I[b][c][d1..d1+1][0..3] -- one vector load.
+//
+// Weights -> fragment order: wp[kstep][nt][lane] = {b0, b1} (two bf16x2),
+// b0 = (c = 4*kstep + t, d2 = 0, 1; n = g), b1 = (same c, d2 = 2, 3; n = g), with
+// g = lane/4, t = lane%4, n = (c' = (8nt+g)/4, d3 = (8nt+g)%4), value
+// K[c][c'][d2][d3]; columns past 4*Cout are zero.
+__global__ void __launch_bounds__(256) fc_pack(const __nv_bfloat16 *__restrict__ K, uint32_t *__restrict__ wp,
+                                               int ksteps, int NT, int Cout) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)ksteps * NT * 32;
+    if (idx >= total) return;
+    const int lane = (int)(idx % 32);
+    const int nt = (int)((idx / 32) % NT);
+    const int kstep = (int)(idx / 32 / NT);
+    const int g = lane >> 2, t = lane & 3;
+    const int n = nt * 8 + g;
+    uint32_t out[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        __nv_bfloat16 v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 4 * kstep + t, d2 = 2 * h + e;
+            v[e] = __float2bfloat16_rn(0.f);
+            if (n < 4 * Cout) v[e] = K[(((size_t)c * Cout + n / 4) * 4 + d2) * 4 + (n % 4)];
+        }
+        out[h] = (uint32_t)__bfloat16_as_ushort(v[0]) | ((uint32_t)__bfloat16_as_ushort(v[1]) << 16);
+    }
+    reinterpret_cast<uint2 *>(wp)[idx] = make_uint2(out[0], out[1]);
+}
+
+__device__ __forceinline__ void hmma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// A fragment of m-tile (4 images from b0) at k-step kstep: lane (g, t) loads
+// I[b0 + g/2][4*kstep + t][2(g%2) .. 2(g%2)+1][0..3] (16 bytes) = {a0, a2, a1, a3}.
+__device__ __forceinline__ void load_a(const uint4 *__restrict__ I16, int C, int B, int b0, int kstep, int g, int t,
+                                       uint32_t (&a)[4]) {
+    const int b = b0 + (g >> 1);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (b < B) v = __ldg(I16 + ((size_t)b * C + 4 * kstep + t) * 2 + (g & 1));
+    a[0] = v.x;   // row g:     d2 0..1
+    a[2] = v.y;   // row g:     d2 2..3
+    a[1] = v.z;   // row g + 8: d2 0..1
+    a[3] = v.w;   // row g + 8: d2 2..3
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat16 *__restrict__ I,
+                                                                const uint32_t *__restrict__ wp,
+                                                                float *__restrict__ part, int B, int C, int kslice,
+                                                                int ksteps) {
+    extern __shared__ __align__(16) uint32_t wsm[];
+    const int ks = blockIdx.x, mb = blockIdx.y;
+    const int k0 = ks * kslice, k1 = min(ksteps, k0 + kslice);
+    const int nk = k1 - k0;
+    // weight slice -> shared memory (fragment order, contiguous in global)
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(wp + (size_t)k0 * NT * 64);
+        uint4 *dst = reinterpret_cast<uint4 *>(wsm);
+        for (int i = threadIdx.x; i < nk * NT * 16; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int rows = B * 4;
+    const int r0 = (mb * kFcWarps + warp) * kFcMt * 16;   // first row (= 4 * first image) of the warp
+    const uint4 *I16 = reinterpret_cast<const uint4 *>(I);
+    float acc[kFcMt][NT][4];
+#pragma unroll
+    for (int m = 0; m < kFcMt; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[m][n][e] = 0.f;
+    // software pipeline: the A fragments of the next kPf k-steps are in flight
+    constexpr int kPf = 4;
+    uint32_t a[kPf][kFcMt][4];
+#pragma unroll
+    for (int j = 0; j < kPf; ++j)
+#pragma unroll
+        for (int m = 0; m < kFcMt; ++m) {
+            if (j < nk) load_a(I16, C, B, (r0 >> 2) + 4 * m, k0 + j, g, t, a[j][m]);
+            else { a[j][m][0] = a[j][m][1] = a[j][m][2] = a[j][m][3] = 0u; }
+        }
+    for (int kk = 0; kk < nk; kk += kPf) {
+#pragma unroll
+        for (int j = 0; j < kPf; ++j) {
+            if (kk + j < nk) {
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const uint2 bb = reinterpret_cast<const uint2 *>(wsm)[((kk + j) * NT + n) * 32 + lane];
+#pragma unroll
+                    for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m][n], a[j][m], bb.x, bb.y);
+                }
+            }
+            // refill this slot with k-step kk + j + kPf
+#pragma unroll
+            for (int m = 0; m < kFcMt; ++m)
+                if (kk + j + kPf < nk) load_a(I16, C, B, (r0 >> 2) + 4 * m, k0 + kk + j + kPf, g, t, a[j][m]);
+        }
+    }
+    // partials part[ks][row = 4b + d1][NT*8]: c0,c1 -> fragment row g = (image g/2,
+    // d1 = 2(g%2)), cols 2t, 2t+1; c2,c3 -> row g + 8 = (same image, d1 + 1)
+    const int ncol = NT * 8;
+    float *pk = part + (size_t)ks * rows * ncol;
+#pragma unroll
+    for (int m = 0; m < kFcMt; ++m) {
+        const int b = (r0 >> 2) + 4 * m + (g >> 1);
+        const int ra = 4 * b + 2 * (g & 1);
+        if (b < B) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const int col = n * 8 + 2 * t;
+                *reinterpret_cast<float2 *>(pk + (size_t)ra * ncol + col) = make_float2(acc[m][n][0], acc[m][n][1]);
+                *reinterpret_cast<float2 *>(pk + (size_t)(ra + 1) * ncol + col) =
+                    make_float2(acc[m][n][2], acc[m][n][3]);
+            }
+        }
+    }
+}
+
+// O[b][c'][d1][d3] = sum over splits (fixed order) of part[ks][(b, d1)][(c', d3)], rounded to bf16
+__global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ part, __nv_bfloat16 *__restrict__ O,
+                                                   int B, int Cout, int ncol, int ksplit) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (row, c')
+    const int64_t rows = (int64_t)B * 4;
+    if (idx >= rows * Cout) return;
+    const int co = (int)(idx % Cout);
+    const int64_t r = idx / Cout;
+    const int64_t b = r >> 2;
+    const int d1 = (int)(r & 3);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < ksplit; ++k) {
+        const float4 v = *reinterpret_cast<const float4 *>(part + ((size_t)k * rows + r) * ncol + co * 4);
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(s.x, s.y), hi = __floats2bfloat162_rn(s.z, s.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t *>(&lo);
+    w.y = *reinterpret_cast<uint32_t *>(&hi);
+    *reinterpret_cast<uint2 *>(O + (((size_t)b * Cout + co) * 4 + d1) * 4) = w;
+}
+
+}  // namespace
+
+bool fc_hmma_fwd_supported(const Problem &p) {
+    static const bool off = getenv("CAPSCONV_NO_FC_HMMA") != nullptr;
+    return !off && fc_plan(p).ok;
+}
+
+size_t fc_hmma_fwd_workspace(const Problem &p) {
+    const FcPlan f = fc_plan(p);
+    return f.ok ? f.wpack_bytes + f.part_bytes : 0;
+}
+
+cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
+                        cudaStream_t st) {
+    const FcPlan f = fc_plan(p);
+    if (!f.ok || ws_bytes < f.wpack_bytes + f.part_bytes) return cudaErrorInvalidValue;
+    uint32_t *wp = static_cast<uint32_t *>(ws);
+    float *part = reinterpret_cast<float *>(static_cast<uint8_t *>(ws) + f.wpack_bytes);
+    const int64_t npk = (int64_t)f.ksteps * f.NT * 32;
+    fc_pack<<<(unsigned)((npk + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps, f.NT,
+                                                            f.Cout);
+    note_launches(1);
+    const dim3 grid((unsigned)f.ksplit, (unsigned)f.mblocks);
+    const __nv_bfloat16 *Ib = static_cast<const __nv_bfloat16 *>(I);
+    cudaError_t e = cudaSuccess;
+    switch (f.NT) {
+#define FC_CASE(nt)                                                                                               \
+    case nt:                                                                                                      \
+        e = cudaFuncSetAttribute(fc_fwd_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);    \
+        if (e != cudaSuccess) return e;                                                                           \
+        fc_fwd_kernel<nt><<<grid, kFcWarps * 32, f.smem, st>>>(Ib, wp, part, f.B, f.C, f.kslice, f.ksteps);        \
+        break;
+        FC_CASE(1) FC_CASE(2) FC_CASE(3) FC_CASE(4) FC_CASE(5) FC_CASE(6) FC_CASE(7) FC_CASE(8)
+#undef FC_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    note_launches(1);
+    const int64_t nfin = (int64_t)f.B * 4 * f.Cout;
+    fc_finalize<<<(unsigned)((nfin + 255) / 256), 256, 0, st>>>(part, static_cast<__nv_bfloat16 *>(O), f.B, f.Cout,
+                                                                f.NT * 8, f.ksplit);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace capsconv

@@ -46,6 +46,11 @@ cudaError_t simt_bwd_kernel(const Problem &p, const void *I, const void *dO, flo
 // ---------------------------------------------------------------- tcgen05 (MMA) path
 // Returns true when the MMA path can take the problem (alignment excluded).
 bool mma_supported(capsconv_op_t op, const Problem &p);
+// fully-connected view (R18) forward on warp-level mma.sync (csrc/fc_hmma.cu)
+bool fc_hmma_fwd_supported(const Problem &p);
+size_t fc_hmma_fwd_workspace(const Problem &p);
+cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
+                        cudaStream_t st);
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O,
                     void *ws, size_t ws_bytes, cudaStream_t st);

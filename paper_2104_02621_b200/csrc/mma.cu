@@ -1064,17 +1064,20 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
 
 bool mma_supported(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_supported(p);
+    if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return true;
     return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }
 
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_workspace_bytes(p);
+    if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return fc_hmma_fwd_workspace(p);
     const Plan &pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
     return pl.ok ? pl.wpack_bytes + pl.part_bytes : 0;
 }
 
 cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
+    if (fc_hmma_fwd_supported(p)) return fc_hmma_fwd(p, I, K, O, ws, ws_bytes, st);
     Plan pl = cached_plan(p, false);
     if (!pl.ok) return cudaErrorNotSupported;
     return run_plan(pl, I, K, O, ws, ws_bytes, st);
