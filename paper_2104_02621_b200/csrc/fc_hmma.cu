@@ -222,6 +222,114 @@ __global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ par
     *reinterpret_cast<uint2 *>(O + (((size_t)b * Cout + co) * 4 + d1) * 4) = w;
 }
 
+// ------------------------------------------------------------------ dI
+// dI[b, c, d1, d2] = sum_{c', d3} dO[b, c', d1, d3] * K[c, c', d2, d3]
+// rows m = (b, d1), k = (c', d3) (K = 4*Cout, zero-padded to 16-steps),
+// columns n = (c, d2) (N = 4*C).  Same fragment permutation as the forward:
+// k-pair (2t, 2t+1) = (c' = 4*kstep + t, d3 0..1), (2t+8, 2t+9) = (same c',
+// d3 2..3); fragment rows g, g+8 = d1 = 2(g%2), 2(g%2)+1 of image g/2, so a
+// thread's A fragment is the 16 bytes dO[b][c'][d1..d1+1][0..3].
+//
+// Weights -> wpd[kstep][nt][lane] = {b0, b1}: b0 = (c' = 4*kstep + t, d3 = 0, 1;
+// n = 8nt + g), b1 = (same c', d3 = 2, 3), n = (c = n/4, d2 = n%4), value
+// K[c][c'][d2][d3]; c' >= Cout is zero.
+__global__ void __launch_bounds__(256) fc_pack_dgrad(const __nv_bfloat16 *__restrict__ K, uint32_t *__restrict__ wp,
+                                                     int ksteps, int NT, int Cout) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)ksteps * NT * 32;
+    if (idx >= total) return;
+    const int lane = (int)(idx % 32);
+    const int nt = (int)((idx / 32) % NT);
+    const int kstep = (int)(idx / 32 / NT);
+    const int g = lane >> 2, t = lane & 3;
+    const int n = nt * 8 + g;
+    const int co = 4 * kstep + t;
+    uint32_t out[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        __nv_bfloat16 v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int d3 = 2 * h + e;
+            v[e] = __float2bfloat16_rn(0.f);
+            if (co < Cout) v[e] = K[(((size_t)(n / 4) * Cout + co) * 4 + (n % 4)) * 4 + d3];
+        }
+        out[h] = (uint32_t)__bfloat16_as_ushort(v[0]) | ((uint32_t)__bfloat16_as_ushort(v[1]) << 16);
+    }
+    reinterpret_cast<uint2 *>(wp)[idx] = make_uint2(out[0], out[1]);
+}
+
+constexpr int kFcDgKs = 4;     // max k-steps (4*Cout <= 64)
+constexpr int kFcDgNt = 64;    // n-tiles per CTA column block (512 columns)
+
+// CTA = (column block of kFcDgNt n-tiles, 8 warps x 2 m-tiles of rows); each
+// warp loads its dO fragments once and walks the column block.
+__global__ void __launch_bounds__(kFcWarps * 32) fc_dgrad_kernel(const __nv_bfloat16 *__restrict__ dO,
+                                                                  const uint32_t *__restrict__ wp,
+                                                                  __nv_bfloat16 *__restrict__ dI, int B, int C,
+                                                                  int Cout, int ksteps, int NTall) {
+    extern __shared__ __align__(16) uint32_t wsm[];
+    const int nb = blockIdx.x, mb = blockIdx.y;
+    const int nt0 = nb * kFcDgNt, nt1 = min(NTall, nt0 + kFcDgNt);
+    const int nnt = nt1 - nt0;
+    // weights of this column block, all k-steps: wsm[kstep][ntl][lane]
+    for (int i = threadIdx.x; i < ksteps * nnt * 16; i += blockDim.x) {
+        const int kstep = i / (nnt * 16), rem = i - kstep * nnt * 16;
+        reinterpret_cast<uint4 *>(wsm)[i] =
+            reinterpret_cast<const uint4 *>(wp)[((size_t)kstep * NTall + nt0) * 16 + rem];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int img0 = (mb * kFcWarps + warp) * kFcMt * 4;   // first image of the warp
+    uint32_t a[kFcDgKs][kFcMt][4];
+#pragma unroll
+    for (int j = 0; j < kFcDgKs; ++j)
+#pragma unroll
+        for (int m = 0; m < kFcMt; ++m) {
+            a[j][m][0] = a[j][m][1] = a[j][m][2] = a[j][m][3] = 0u;
+            const int b = img0 + 4 * m + (g >> 1), co = 4 * j + t;
+            if (j < ksteps && b < B && co < Cout) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(dO) + ((size_t)b * Cout + co) * 2 + (g & 1));
+                a[j][m][0] = v.x; a[j][m][2] = v.y; a[j][m][1] = v.z; a[j][m][3] = v.w;
+            }
+        }
+    for (int ntl = 0; ntl < nnt; ++ntl) {
+        float acc[kFcMt][4];
+#pragma unroll
+        for (int m = 0; m < kFcMt; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+#pragma unroll
+        for (int j = 0; j < kFcDgKs; ++j) {
+            if (j < ksteps) {
+                const uint2 bb = reinterpret_cast<const uint2 *>(wsm)[(j * nnt + ntl) * 32 + lane];
+#pragma unroll
+                for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m], a[j][m], bb.x, bb.y);
+            }
+        }
+        // c0,c1: row (image g/2, d1 = 2(g%2)), columns n = 8nt + 2t, +1 =
+        // (c = n/4, d2 = 2(t%2) .. +1); c2,c3: row d1 + 1.  Lanes t and t^1 hold
+        // the two d2 halves of the same capsule rows: one exchange gives the
+        // even lane row d1 and the odd lane row d1 + 1 whole (8 bytes), so a warp
+        // store writes full 64-byte capsule pairs.
+        const int n = (nt0 + ntl) * 8 + 2 * t;
+        const int c = n >> 2;
+        const bool odd = t & 1;
+#pragma unroll
+        for (int m = 0; m < kFcMt; ++m) {
+            const int b = img0 + 4 * m + (g >> 1);
+            __nv_bfloat162 lo = __floats2bfloat162_rn(acc[m][0], acc[m][1]);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(acc[m][2], acc[m][3]);
+            const uint32_t ulo = *reinterpret_cast<uint32_t *>(&lo), uhi = *reinterpret_cast<uint32_t *>(&hi);
+            const uint32_t x = __shfl_xor_sync(0xffffffffu, odd ? ulo : uhi, 1);
+            if (b < B && c < C) {
+                const int row = 2 * (g & 1) + (odd ? 1 : 0);
+                const uint2 w = odd ? make_uint2(x, uhi) : make_uint2(ulo, x);
+                *reinterpret_cast<uint2 *>(dI + (((size_t)b * C + c) * 4 + row) * 4) = w;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 bool fc_hmma_fwd_supported(const Problem &p) {
@@ -262,6 +370,61 @@ cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O,
     const int64_t nfin = (int64_t)f.B * 4 * f.Cout;
     fc_finalize<<<(unsigned)((nfin + 255) / 256), 256, 0, st>>>(part, static_cast<__nv_bfloat16 *>(O), f.B, f.Cout,
                                                                 f.NT * 8, f.ksplit);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+
+namespace {
+struct FcDgPlan {
+    bool ok = false;
+    int B, C, Cout, ksteps, NTall, nblocks, mblocks;
+    size_t wpack_bytes;
+    uint32_t smem;
+};
+FcDgPlan fc_dg_plan(const Problem &p) {
+    FcDgPlan f;
+    const bool full = p.KH == p.H && p.KW == p.W && p.pad == 0;
+    if (!full || p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return f;
+    f.B = (int)p.B;
+    f.C = (int)(p.KH * p.KW * p.C);
+    f.Cout = (int)p.Cout;
+    f.ksteps = (f.Cout + 3) / 4;
+    if (f.ksteps > kFcDgKs || p.B > (1 << 24)) return f;
+    f.NTall = (f.C * 4 + 7) / 8;
+    f.nblocks = (f.NTall + kFcDgNt - 1) / kFcDgNt;
+    f.mblocks = (f.B + kFcWarps * kFcMt * 4 - 1) / (kFcWarps * kFcMt * 4);
+    f.smem = (uint32_t)f.ksteps * kFcDgNt * 256u;
+    f.wpack_bytes = ((size_t)f.ksteps * f.NTall * 256 + 255) & ~(size_t)255;
+    f.ok = true;
+    return f;
+}
+}  // namespace
+
+bool fc_hmma_dgrad_supported(const Problem &p) {
+    static const bool off = getenv("CAPSCONV_NO_FC_HMMA") != nullptr;
+    return !off && fc_dg_plan(p).ok;
+}
+
+size_t fc_hmma_dgrad_workspace(const Problem &p) {
+    const FcDgPlan f = fc_dg_plan(p);
+    return f.ok ? f.wpack_bytes : 0;
+}
+
+cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,
+                          cudaStream_t st) {
+    const FcDgPlan f = fc_dg_plan(p);
+    if (!f.ok || ws_bytes < f.wpack_bytes) return cudaErrorInvalidValue;
+    uint32_t *wp = static_cast<uint32_t *>(ws);
+    const int64_t npk = (int64_t)f.ksteps * f.NTall * 32;
+    fc_pack_dgrad<<<(unsigned)((npk + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps,
+                                                                  f.NTall, f.Cout);
+    note_launches(1);
+    cudaError_t e = cudaFuncSetAttribute(fc_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
+    if (e != cudaSuccess) return e;
+    fc_dgrad_kernel<<<dim3((unsigned)f.nblocks, (unsigned)f.mblocks), kFcWarps * 32, f.smem, st>>>(
+        static_cast<const __nv_bfloat16 *>(dO), wp, static_cast<__nv_bfloat16 *>(dI), f.B, f.C, f.Cout, f.ksteps,
+        f.NTall);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -51,6 +51,10 @@ bool fc_hmma_fwd_supported(const Problem &p);
 size_t fc_hmma_fwd_workspace(const Problem &p);
 cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
                         cudaStream_t st);
+bool fc_hmma_dgrad_supported(const Problem &p);
+size_t fc_hmma_dgrad_workspace(const Problem &p);
+cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,
+                          cudaStream_t st);
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O,
                     void *ws, size_t ws_bytes, cudaStream_t st);

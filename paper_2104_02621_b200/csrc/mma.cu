@@ -1065,12 +1065,14 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
 bool mma_supported(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_supported(p);
     if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return true;
+    if (op == CAPSCONV_OP_BWD_DATA && fc_hmma_dgrad_supported(p)) return true;
     return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }
 
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_workspace_bytes(p);
     if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return fc_hmma_fwd_workspace(p);
+    if (op == CAPSCONV_OP_BWD_DATA && fc_hmma_dgrad_supported(p)) return fc_hmma_dgrad_workspace(p);
     const Plan &pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
     return pl.ok ? pl.wpack_bytes + pl.part_bytes : 0;
 }
@@ -1085,6 +1087,7 @@ cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O, voi
 
 cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,
                          cudaStream_t st) {
+    if (fc_hmma_dgrad_supported(p)) return fc_hmma_dgrad(p, dO, K, dI, ws, ws_bytes, st);
     Plan pl = cached_plan(p, true);
     if (!pl.ok) return cudaErrorNotSupported;
     return run_plan(pl, dO, K, dI, ws, ws_bytes, st);
