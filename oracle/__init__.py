@@ -10,7 +10,10 @@ outermost output index); this module only builds it with gcc, marshals numpy
 arrays through ctypes and composes single layers into the stack of config 5.
 
 Parity status of every function (see DESIGN.md §3 "Oracle pins"):
-  output_dims, fwd, bwd_data, bwd_kernel  -- pinned (tests/test_oracle_pins.py)
+  output_dims, fwd, bwd_data, bwd_kernel  -- pinned (tests/test_oracle_pins.py),
+                                             incl. their pad > 0 forms (R21)
+  fwd/bwd_data/bwd_kernel_slices          -- pinned: slice-wise = the matrix
+                                             oracle per slice, Fig 2 rank-3, adjoints
   round_bf16                              -- pinned (torch bf16 cast, exact cases)
   stack_fwd_bwd                           -- composition of pinned layers;
                                              pinned by the depth-1 reduction and
@@ -23,6 +26,9 @@ from .oracle import (  # noqa: F401
     fwd,
     bwd_data,
     bwd_kernel,
+    fwd_slices,
+    bwd_data_slices,
+    bwd_kernel_slices,
     round_bf16,
     num_threads,
     stack_fwd_bwd,

@@ -356,3 +356,133 @@ int oracle_bwd_kernel_pad(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Co
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * S-slice capsules (SPEC.md:30-35, 90 -- PoseDims (S, M, K):
+ * a rank-3 capsule is S matrices, multiplied slice-wise, which is how
+ * PAPER.md:44-53's 3x3x3 capsules are read).  Layouts (reading R22):
+ *   I [B][H][W][C][S][D1][D2], K [KH][KW][C][Cout][S][D2][D3],
+ *   O [B][Ho][Wo][Cout][S][D1][D3]
+ *   O[b,x',y',c',s,d1,d3] = sum_{p,q,c,d2} I[b,x's+p,y's+q,c,s,d1,d2] K[p,q,c,c',s,d2,d3]
+ * (no padding; S = 1 is the matrix-capsule convolution above).
+ * ------------------------------------------------------------------------ */
+int oracle_fwd_slices(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                      int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3,
+                      int64_t stride, const double *I, const double *K, double *O, double *Oabs)
+{
+    int64_t Ho, Wo;
+    int rc = oracle_output_dims(H, W, KH, KW, stride, &Ho, &Wo);
+    if (rc) return rc;
+    if (B < 1 || C < 1 || Cout < 1 || S < 1 || D1 < 1 || D2 < 1 || D3 < 1) return OR_ERR_SHAPE;
+    const int64_t n_out = B * Ho * Wo * Cout * S * D1 * D3;
+#pragma omp parallel for schedule(static)
+    for (int64_t o = 0; o < n_out; ++o) {
+        int64_t r = o;
+        const int64_t d3 = r % D3; r /= D3;
+        const int64_t d1 = r % D1; r /= D1;
+        const int64_t sl = r % S; r /= S;
+        const int64_t co = r % Cout; r /= Cout;
+        const int64_t y = r % Wo; r /= Wo;
+        const int64_t x = r % Ho; r /= Ho;
+        const int64_t b = r;
+        double acc = 0.0, aabs = 0.0;
+        for (int64_t p = 0; p < KH; ++p)
+            for (int64_t q = 0; q < KW; ++q)
+                for (int64_t c = 0; c < C; ++c)
+                    for (int64_t d2 = 0; d2 < D2; ++d2) {
+                        const int64_t ii = ((((((b * H + x * stride + p) * W + y * stride + q) * C + c) * S + sl)
+                                             * D1 + d1) * D2 + d2);
+                        const int64_t kk = ((((((p * KW + q) * C + c) * Cout + co) * S + sl) * D2 + d2) * D3 + d3);
+                        const double t = I[ii] * K[kk];
+                        acc += t;
+                        aabs += fabs(t);
+                    }
+        O[o] = acc;
+        if (Oabs) Oabs[o] = aabs;
+    }
+    return OR_OK;
+}
+
+/* dI and dK of the slice-wise map, as adjoints (R10/R11 per slice). */
+int oracle_bwd_data_slices(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                           int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3,
+                           int64_t stride, const double *dO, const double *K, double *dI, double *dIabs)
+{
+    int64_t Ho, Wo;
+    int rc = oracle_output_dims(H, W, KH, KW, stride, &Ho, &Wo);
+    if (rc) return rc;
+    if (B < 1 || C < 1 || Cout < 1 || S < 1 || D1 < 1 || D2 < 1 || D3 < 1) return OR_ERR_SHAPE;
+    const int64_t n_in = B * H * W * C * S * D1 * D2;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_in; ++e) {
+        int64_t r = e;
+        const int64_t d2 = r % D2; r /= D2;
+        const int64_t d1 = r % D1; r /= D1;
+        const int64_t sl = r % S; r /= S;
+        const int64_t c = r % C; r /= C;
+        const int64_t w = r % W; r /= W;
+        const int64_t h = r % H; r /= H;
+        const int64_t b = r;
+        double acc = 0.0, aabs = 0.0;
+        for (int64_t p = 0; p < KH; ++p) {
+            const int64_t hx = h - p;
+            if (hx < 0 || hx % stride != 0) continue;
+            const int64_t x = hx / stride;
+            if (x >= Ho) continue;
+            for (int64_t q = 0; q < KW; ++q) {
+                const int64_t wy = w - q;
+                if (wy < 0 || wy % stride != 0) continue;
+                const int64_t y = wy / stride;
+                if (y >= Wo) continue;
+                for (int64_t co = 0; co < Cout; ++co)
+                    for (int64_t d3 = 0; d3 < D3; ++d3) {
+                        const int64_t oo = ((((((b * Ho + x) * Wo + y) * Cout + co) * S + sl) * D1 + d1) * D3 + d3);
+                        const int64_t kk = ((((((p * KW + q) * C + c) * Cout + co) * S + sl) * D2 + d2) * D3 + d3);
+                        const double t = dO[oo] * K[kk];
+                        acc += t;
+                        aabs += fabs(t);
+                    }
+            }
+        }
+        dI[e] = acc;
+        if (dIabs) dIabs[e] = aabs;
+    }
+    return OR_OK;
+}
+
+int oracle_bwd_kernel_slices(int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                             int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3,
+                             int64_t stride, const double *I, const double *dO, double *dK, double *dKabs)
+{
+    int64_t Ho, Wo;
+    int rc = oracle_output_dims(H, W, KH, KW, stride, &Ho, &Wo);
+    if (rc) return rc;
+    if (B < 1 || C < 1 || Cout < 1 || S < 1 || D1 < 1 || D2 < 1 || D3 < 1) return OR_ERR_SHAPE;
+    const int64_t n_k = KH * KW * C * Cout * S * D2 * D3;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n_k; ++e) {
+        int64_t r = e;
+        const int64_t d3 = r % D3; r /= D3;
+        const int64_t d2 = r % D2; r /= D2;
+        const int64_t sl = r % S; r /= S;
+        const int64_t co = r % Cout; r /= Cout;
+        const int64_t c = r % C; r /= C;
+        const int64_t q = r % KW; r /= KW;
+        const int64_t p = r;
+        double acc = 0.0, aabs = 0.0;
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t x = 0; x < Ho; ++x)
+                for (int64_t y = 0; y < Wo; ++y)
+                    for (int64_t d1 = 0; d1 < D1; ++d1) {
+                        const int64_t ii = ((((((b * H + x * stride + p) * W + y * stride + q) * C + c) * S + sl)
+                                             * D1 + d1) * D2 + d2);
+                        const int64_t oo = ((((((b * Ho + x) * Wo + y) * Cout + co) * S + sl) * D1 + d1) * D3 + d3);
+                        const double t = I[ii] * dO[oo];
+                        acc += t;
+                        aabs += fabs(t);
+                    }
+        dK[e] = acc;
+        if (dKabs) dKabs[e] = aabs;
+    }
+    return OR_OK;
+}

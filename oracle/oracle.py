@@ -59,6 +59,10 @@ def _load():
                 fp = getattr(lib, name + "_pad")
                 fp.argtypes = [i64] * 12 + [dp] * 4
                 fp.restype = ctypes.c_int
+            for name in ("oracle_fwd_slices", "oracle_bwd_data_slices", "oracle_bwd_kernel_slices"):
+                fn = getattr(lib, name)
+                fn.argtypes = [i64] * 12 + [dp] * 4
+                fn.restype = ctypes.c_int
             lib.oracle_output_dims_pad.argtypes = [i64] * 6 + [ctypes.POINTER(i64)] * 2
             lib.oracle_output_dims_pad.restype = ctypes.c_int
             lib.oracle_round_bf16_array.argtypes = [dp, i64]
@@ -157,6 +161,53 @@ def bwd_kernel(I, dO, stride, KH, KW, pad=0):
                                        _ptr(I), _ptr(dO), _ptr(dK), _ptr(A))
     if rc:
         raise OracleError("oracle_bwd_kernel: status %d" % rc)
+    return dK, A
+
+
+def fwd_slices(I, K, stride):
+    """S-slice capsules: I (B,H,W,C,S,D1,D2),
+    K (KH,KW,C,Cout,S,D2,D3) -> O (B,Ho,Wo,Cout,S,D1,D3), slice-wise products."""
+    I, K = _f64(I), _f64(K)
+    B, H, W, C, S, D1, D2 = I.shape
+    KH, KW, C2, Cout, S2, D2b, D3 = K.shape
+    if C2 != C or S2 != S or D2b != D2:
+        raise OracleError("channel / slice / inner capsule dims disagree")
+    Ho, Wo = output_dims(H, W, KH, KW, stride)
+    O = np.empty((B, Ho, Wo, Cout, S, D1, D3))
+    A = np.empty_like(O)
+    rc = _load().oracle_fwd_slices(B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride, _ptr(I), _ptr(K), _ptr(O), _ptr(A))
+    if rc:
+        raise OracleError("oracle_fwd_slices: status %d" % rc)
+    return O, A
+
+
+def bwd_data_slices(dO, K, stride, H, W):
+    dO, K = _f64(dO), _f64(K)
+    B, Ho, Wo, Cout, S, D1, D3 = dO.shape
+    KH, KW, C, Cout2, S2, D2, D3b = K.shape
+    if Cout2 != Cout or S2 != S or D3b != D3 or output_dims(H, W, KH, KW, stride) != (Ho, Wo):
+        raise OracleError("shapes disagree")
+    dI = np.empty((B, H, W, C, S, D1, D2))
+    A = np.empty_like(dI)
+    rc = _load().oracle_bwd_data_slices(B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride, _ptr(dO), _ptr(K), _ptr(dI),
+                                        _ptr(A))
+    if rc:
+        raise OracleError("oracle_bwd_data_slices: status %d" % rc)
+    return dI, A
+
+
+def bwd_kernel_slices(I, dO, stride, KH, KW):
+    I, dO = _f64(I), _f64(dO)
+    B, H, W, C, S, D1, D2 = I.shape
+    B2, Ho, Wo, Cout, S2, D1b, D3 = dO.shape
+    if B2 != B or S2 != S or D1b != D1 or output_dims(H, W, KH, KW, stride) != (Ho, Wo):
+        raise OracleError("shapes disagree")
+    dK = np.empty((KH, KW, C, Cout, S, D2, D3))
+    A = np.empty_like(dK)
+    rc = _load().oracle_bwd_kernel_slices(B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride, _ptr(I), _ptr(dO),
+                                          _ptr(dK), _ptr(A))
+    if rc:
+        raise OracleError("oracle_bwd_kernel_slices: status %d" % rc)
     return dK, A
 
 

@@ -467,3 +467,60 @@ def test_pad_adjoint_identities(oracle_mod, case):
     a = float(np.sum(O * dO))
     assert abs(a - float(np.sum(I * dI))) <= 1e-10 * max(1.0, abs(a))
     assert abs(a - float(np.sum(K * dK))) <= 1e-10 * max(1.0, abs(a))
+
+
+# ---------------------------------------------------------------- S-slice capsules
+SLICE_CASES = [
+    # B, H, W, C, Cout, KH, KW, S, D1, D2, D3, s
+    (2, 5, 6, 2, 3, 3, 3, 2, 2, 3, 2, 1),
+    (1, 7, 7, 3, 2, 3, 3, 3, 3, 3, 3, 2),
+    (2, 4, 5, 1, 2, 2, 3, 1, 4, 4, 4, 1),
+]
+
+
+def _slice_inputs(case):
+    B, H, W, C, Co, KH, KW, S, D1, D2, D3, s = case
+    rng = np.random.default_rng(sum(case))
+    Ho, Wo = (H - KH) // s + 1, (W - KW) // s + 1
+    return (rng.uniform(-1, 1, (B, H, W, C, S, D1, D2)), rng.uniform(-1, 1, (KH, KW, C, Co, S, D2, D3)),
+            rng.uniform(-1, 1, (B, Ho, Wo, Co, S, D1, D3)))
+
+
+@pytest.mark.parametrize("case", SLICE_CASES)
+def test_slices_are_independent_matrix_convolutions(oracle_mod, case):
+    """Slice s of every result is the (pinned) matrix-capsule oracle applied to
+    slice s of the operands (numpy slicing, not the oracle's own indexing)."""
+    B, H, W, C, Co, KH, KW, S, D1, D2, D3, s = case
+    I, K, dO = _slice_inputs(case)
+    O, _ = oracle_mod.fwd_slices(I, K, s)
+    dI, _ = oracle_mod.bwd_data_slices(dO, K, s, H, W)
+    dK, _ = oracle_mod.bwd_kernel_slices(I, dO, s, KH, KW)
+    for sl in range(S):
+        Or, _ = oracle_mod.fwd(I[:, :, :, :, sl], K[:, :, :, :, sl], s)
+        dIr, _ = oracle_mod.bwd_data(dO[:, :, :, :, sl], K[:, :, :, :, sl], s, H, W)
+        dKr, _ = oracle_mod.bwd_kernel(I[:, :, :, :, sl], dO[:, :, :, :, sl], s, KH, KW)
+        np.testing.assert_allclose(O[:, :, :, :, sl], Or, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(dI[:, :, :, :, sl], dIr, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(dK[:, :, :, :, sl], dKr, rtol=0, atol=1e-12)
+
+
+def test_slices_fig2_rank3_reading(oracle_mod):
+    """PAPER.md:44-53 with 3x3x3 capsules read as S = 3 slices of 3x3: all-ones
+    5x5 input, all-ones 4x4 kernel -> 2x2 output of 48s (16 taps x inner dim 3)."""
+    I = np.ones((1, 5, 5, 1, 3, 3, 3))
+    K = np.ones((4, 4, 1, 1, 3, 3, 3))
+    O, _ = oracle_mod.fwd_slices(I, K, 1)
+    assert O.shape == (1, 2, 2, 1, 3, 3, 3)
+    assert np.all(O == 48.0)
+
+
+@pytest.mark.parametrize("case", SLICE_CASES)
+def test_slices_adjoint_identities(oracle_mod, case):
+    B, H, W, C, Co, KH, KW, S, D1, D2, D3, s = case
+    I, K, dO = _slice_inputs(case)
+    O, _ = oracle_mod.fwd_slices(I, K, s)
+    dI, _ = oracle_mod.bwd_data_slices(dO, K, s, H, W)
+    dK, _ = oracle_mod.bwd_kernel_slices(I, dO, s, KH, KW)
+    a = float(np.sum(O * dO))
+    assert abs(a - float(np.sum(I * dI))) <= 1e-10 * max(1.0, abs(a))
+    assert abs(a - float(np.sum(K * dK))) <= 1e-10 * max(1.0, abs(a))
