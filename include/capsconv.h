@@ -191,6 +191,39 @@ CAPSCONV_API capsconv_status_t capsconv_bwd_kernel_pad(capsconv_dtype_t dt,
         const void *I, const void *dO, float *dK,
         void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
 
+/* ---- S-slice capsules (reading R22): a
+ * capsule is S matrices multiplied slice-wise (PAPER.md:44-53's 3x3x3
+ * capsules are S = 3 slices of 3x3).  Layouts, row-major, no padding:
+ *   I, dI [B][H][W][C][S][D1][D2]; K [KH][KW][C][Cout][S][D2][D3];
+ *   O, dO [B][Ho][Wo][Cout][S][D1][D3]; dK [KH][KW][C][Cout][S][D2][D3] (fp32)
+ *   O[b,x',y',c',s,d1,d3] = sum_{p,q,c,d2} I[b,x's+p,y's+q,c,s,d1,d2] K[p,q,c,c',s,d2,d3].
+ * Computed as the matrix-capsule convolution over C*S / Cout*S channels with a
+ * block-diagonal kernel built in the workspace (S x the useful flops); the
+ * workspace (query with capsconv_workspace_bytes_slices) is required, 1 <= S <= 64.
+ * Errors, ownership and stream semantics are those of the matrix calls. */
+CAPSCONV_API capsconv_status_t capsconv_workspace_bytes_slices(capsconv_op_t op, capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+        size_t *bytes);
+
+CAPSCONV_API capsconv_status_t capsconv_fwd_slices(capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+        const void *I, const void *K, void *O,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+CAPSCONV_API capsconv_status_t capsconv_bwd_data_slices(capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+        const void *dO, const void *K, void *dI,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+CAPSCONV_API capsconv_status_t capsconv_bwd_kernel_slices(capsconv_dtype_t dt,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+        const void *I, const void *dO, float *dK,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
 /* Static description of a status code. */
 CAPSCONV_API const char *capsconv_status_string(capsconv_status_t status);
 

@@ -14,9 +14,12 @@ from .capsconv import (  # noqa: F401
     PATH_MMA,
     PATH_SIMT,
     bwd_data,
+    bwd_data_slices,
     bwd_kernel,
+    bwd_kernel_slices,
     caps_conv2d,
     fwd,
+    fwd_slices,
     launch_count,
     load_library,
     output_dims,

@@ -61,6 +61,11 @@ def load_library(path: Optional[str] = None):
         lib.capsconv_select_path_pad.argtypes = [ctypes.c_int, ctypes.c_int] + ext12 + [ctypes.POINTER(ctypes.c_int)]
         for name in ("capsconv_fwd_pad", "capsconv_bwd_data_pad", "capsconv_bwd_kernel_pad"):
             getattr(lib, name).argtypes = [ctypes.c_int] + ext12 + [vp, vp, vp, vp, sz, vp]
+        lib.capsconv_workspace_bytes_slices.argtypes = [ctypes.c_int, ctypes.c_int] + [i64] * 12 + [ctypes.POINTER(sz)]
+        for name in ("capsconv_fwd_slices", "capsconv_bwd_data_slices", "capsconv_bwd_kernel_slices"):
+            getattr(lib, name).argtypes = [ctypes.c_int] + [i64] * 12 + [vp, vp, vp, vp, sz, vp]
+            getattr(lib, name).restype = ctypes.c_int
+        lib.capsconv_workspace_bytes_slices.restype = ctypes.c_int
         for name in ("capsconv_output_dims", "capsconv_workspace_bytes", "capsconv_select_path",
                      "capsconv_set_path_override", "capsconv_fwd", "capsconv_bwd_data", "capsconv_bwd_kernel",
                      "capsconv_output_dims_pad", "capsconv_workspace_bytes_pad", "capsconv_select_path_pad",
@@ -254,6 +259,73 @@ def bwd_kernel(I: torch.Tensor, dO: torch.Tensor, stride: int, KH: int, KW: int,
         raise ValueError("out must be float32 of the kernel's shape")
     ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
     return _call("capsconv_bwd_kernel", OP_BWD_KERNEL, I.dtype, ext, I, dO, out, stream)
+
+
+# ------------------------------------------------------------ S-slice capsules (R22)
+def _slices_call(name: str, op: int, dtype, ext, a, b, out, stream):
+    lib = load_library()
+    s = stream if stream is not None else torch.cuda.current_stream(out.device)
+    handle = s.cuda_stream
+    need = ctypes.c_size_t()
+    _check(lib.capsconv_workspace_bytes_slices(op, _dt(dtype), *ext, ctypes.byref(need)), "workspace_bytes_slices")
+    ws = _workspace(need.value, out.device, handle)
+    with torch.cuda.device(out.device):
+        st = getattr(lib, name)(_dt(dtype), *ext, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                                ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
+                                ctypes.c_size_t(need.value), ctypes.c_void_p(handle))
+    _check(st, name)
+    return out
+
+
+def fwd_slices(I: torch.Tensor, K: torch.Tensor, stride: int = 1, out: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """S-slice capsules: I (B,H,W,C,S,D1,D2), K (KH,KW,C,Cout,S,D2,D3) -> O (B,Ho,Wo,Cout,S,D1,D3)."""
+    dev = _need_cuda(I, K)
+    B, H, W, C, S, D1, D2 = I.shape
+    KH, KW, C2, Cout, S2, D2b, D3 = K.shape
+    if C2 != C or S2 != S or D2b != D2 or I.dtype != K.dtype:
+        raise ValueError("I %s and K %s disagree" % (tuple(I.shape), tuple(K.shape)))
+    Ho, Wo = output_dims(H, W, KH, KW, stride)
+    shape = (B, Ho, Wo, Cout, S, D1, D3)
+    out = torch.empty(shape, dtype=I.dtype, device=dev) if out is None else out
+    if tuple(out.shape) != shape or out.dtype != I.dtype:
+        raise ValueError("out has the wrong shape/dtype")
+    ext = (B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride)
+    return _slices_call("capsconv_fwd_slices", OP_FWD, I.dtype, ext, I, K, out, stream)
+
+
+def bwd_data_slices(dO: torch.Tensor, K: torch.Tensor, stride: int, H: int, W: int,
+                    out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    dev = _need_cuda(dO, K)
+    B, Ho, Wo, Cout, S, D1, D3 = dO.shape
+    KH, KW, C, Cout2, S2, D2, D3b = K.shape
+    if Cout2 != Cout or S2 != S or D3b != D3 or dO.dtype != K.dtype:
+        raise ValueError("dO %s and K %s disagree" % (tuple(dO.shape), tuple(K.shape)))
+    if output_dims(H, W, KH, KW, stride) != (Ho, Wo):
+        raise ValueError("dO spatial extent does not match H, W, K and stride")
+    shape = (B, H, W, C, S, D1, D2)
+    out = torch.empty(shape, dtype=dO.dtype, device=dev) if out is None else out
+    if tuple(out.shape) != shape or out.dtype != dO.dtype:
+        raise ValueError("out has the wrong shape/dtype")
+    ext = (B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride)
+    return _slices_call("capsconv_bwd_data_slices", OP_BWD_DATA, dO.dtype, ext, dO, K, out, stream)
+
+
+def bwd_kernel_slices(I: torch.Tensor, dO: torch.Tensor, stride: int, KH: int, KW: int,
+                      out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    dev = _need_cuda(I, dO)
+    B, H, W, C, S, D1, D2 = I.shape
+    B2, Ho, Wo, Cout, S2, D1b, D3 = dO.shape
+    if B2 != B or S2 != S or D1b != D1 or I.dtype != dO.dtype:
+        raise ValueError("I %s and dO %s disagree" % (tuple(I.shape), tuple(dO.shape)))
+    if output_dims(H, W, KH, KW, stride) != (Ho, Wo):
+        raise ValueError("dO spatial extent does not match H, W, K and stride")
+    shape = (KH, KW, C, Cout, S, D2, D3)
+    out = torch.empty(shape, dtype=torch.float32, device=dev) if out is None else out
+    if tuple(out.shape) != shape or out.dtype != torch.float32:
+        raise ValueError("out must be float32 of the kernel's shape")
+    ext = (B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride)
+    return _slices_call("capsconv_bwd_kernel_slices", OP_BWD_KERNEL, I.dtype, ext, I, dO, out, stream)
 
 
 class CapsConvFunction(torch.autograd.Function):

@@ -136,6 +136,41 @@ static capsconv_status_t finish(cudaError_t e, const char *what) {
     return CAPSCONV_OK;
 }
 
+// Path choice + launch for a validated problem (the body shared by the
+// plain, padded and S-slice entry points).
+static cudaError_t dispatch(capsconv_op_t op, const Problem &p, const void *a, const void *b, void *out, void *ws,
+                            size_t ws_bytes, cudaStream_t cs) {
+    const size_t need = workspace_for(op, p);
+    const bool mma = choose_path(op, p) == CAPSCONV_PATH_MMA && aligned16(a) && aligned16(b) && aligned16(out) &&
+                     (need == 0 || aligned16(ws));
+    switch (op) {
+        case CAPSCONV_OP_FWD: return mma ? mma_fwd(p, a, b, out, ws, ws_bytes, cs) : simt_fwd(p, a, b, out, cs);
+        case CAPSCONV_OP_BWD_DATA:
+            return mma ? mma_bwd_data(p, a, b, out, ws, ws_bytes, cs) : simt_bwd_data(p, a, b, out, cs);
+        default:
+            return mma ? mma_bwd_kernel(p, a, b, static_cast<float *>(out), ws, ws_bytes, cs)
+                       : simt_bwd_kernel(p, a, b, static_cast<float *>(out), ws, ws_bytes, cs);
+    }
+}
+
+// S-slice capsules (R22): the expanded problem (C*S, Cout*S channels) and
+// the workspace = [expanded kernel K' (fwd, dI) or expanded dK' (fp32, dK)] +
+// the expanded problem's own workspace.
+static capsconv_status_t make_slices(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                                     int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3,
+                                     int64_t s, Problem *pe) {
+    if (S < 1 || S > 64) return fail(CAPSCONV_ERR_SHAPE, "slice count S = %lld out of [1, 64]", (long long)S);
+    int64_t cs = 0, cos = 0;
+    if (!mul_ok(C, S, &cs) || !mul_ok(Cout, S, &cos)) return fail(CAPSCONV_ERR_OVERFLOW, "C*S or Cout*S overflows");
+    return make_problem(dt, B, H, W, cs, cos, KH, KW, D1, D2, D3, s, 0, pe);
+}
+
+static size_t slices_aux_bytes(capsconv_op_t op, const Problem &pe) {
+    const size_t n = (size_t)pe.KH * pe.KW * pe.C * pe.Cout * pe.D2 * pe.D3;   // expanded kernel elements
+    const size_t b = op == CAPSCONV_OP_BWD_KERNEL ? 4 * n : pe.elem() * n;
+    return (b + 255) & ~(size_t)255;
+}
+
 }  // namespace capsconv
 
 using namespace capsconv;
@@ -270,6 +305,66 @@ capsconv_status_t capsconv_bwd_kernel(capsconv_dtype_t dt, int64_t B, int64_t H,
                                       size_t workspace_bytes, capsconv_stream_t stream) {
     return capsconv_bwd_kernel_pad(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, 0, I, dO, dK, workspace,
                                    workspace_bytes, stream);
+}
+
+capsconv_status_t capsconv_workspace_bytes_slices(capsconv_op_t op, capsconv_dtype_t dt, int64_t B, int64_t H,
+                                                  int64_t W, int64_t C, int64_t Cout, int64_t KH, int64_t KW,
+                                                  int64_t S, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                                                  size_t *bytes) {
+    if (!bytes) return fail(CAPSCONV_ERR_NULL, "bytes pointer is NULL");
+    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
+    Problem pe;
+    capsconv_status_t st = make_slices(dt, B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride, &pe);
+    if (st) return st;
+    *bytes = slices_aux_bytes(op, pe) + workspace_for(op, pe);
+    return CAPSCONV_OK;
+}
+
+#define CAPSCONV_SLICES_PROLOGUE(OP, A, B_, OUT)                                                              \
+    Problem pe;                                                                                               \
+    capsconv_status_t st = make_slices(dt, B, H, W, C, Cout, KH, KW, S, D1, D2, D3, stride, &pe);             \
+    if (st) return st;                                                                                        \
+    if (!(A) || !(B_) || !(OUT)) return fail(CAPSCONV_ERR_NULL, "a tensor pointer is NULL");                  \
+    const size_t aux = slices_aux_bytes(OP, pe), need = aux + workspace_for(OP, pe);                          \
+    if (workspace_bytes < need)                                                                               \
+        return fail(CAPSCONV_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);     \
+    if (!workspace) return fail(CAPSCONV_ERR_NULL, "workspace is NULL but %zu bytes are required", need);     \
+    st = check_device();                                                                                      \
+    if (st) return st;                                                                                        \
+    cudaStream_t cs = (cudaStream_t)stream;                                                                   \
+    uint8_t *ws8 = static_cast<uint8_t *>(workspace);                                                         \
+    void *inner_ws = aux < workspace_bytes ? ws8 + aux : nullptr;                                             \
+    const size_t inner_bytes = workspace_bytes - aux;
+
+capsconv_status_t capsconv_fwd_slices(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                                      int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3,
+                                      int64_t stride, const void *I, const void *K, void *O, void *workspace,
+                                      size_t workspace_bytes, capsconv_stream_t stream) {
+    CAPSCONV_SLICES_PROLOGUE(CAPSCONV_OP_FWD, I, K, O)
+    cudaError_t e = slices_expand_kernel(dt, K, ws8, KH * KW, C, Cout, S, D2 * D3, cs);
+    if (e == cudaSuccess) e = dispatch(CAPSCONV_OP_FWD, pe, I, ws8, O, inner_ws, inner_bytes, cs);
+    return finish(e, "capsconv_fwd_slices");
+}
+
+capsconv_status_t capsconv_bwd_data_slices(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                           int64_t Cout, int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2,
+                                           int64_t D3, int64_t stride, const void *dO, const void *K, void *dI,
+                                           void *workspace, size_t workspace_bytes, capsconv_stream_t stream) {
+    CAPSCONV_SLICES_PROLOGUE(CAPSCONV_OP_BWD_DATA, dO, K, dI)
+    cudaError_t e = slices_expand_kernel(dt, K, ws8, KH * KW, C, Cout, S, D2 * D3, cs);
+    if (e == cudaSuccess) e = dispatch(CAPSCONV_OP_BWD_DATA, pe, dO, ws8, dI, inner_ws, inner_bytes, cs);
+    return finish(e, "capsconv_bwd_data_slices");
+}
+
+capsconv_status_t capsconv_bwd_kernel_slices(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
+                                             int64_t Cout, int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2,
+                                             int64_t D3, int64_t stride, const void *I, const void *dO, float *dK,
+                                             void *workspace, size_t workspace_bytes, capsconv_stream_t stream) {
+    CAPSCONV_SLICES_PROLOGUE(CAPSCONV_OP_BWD_KERNEL, I, dO, dK)
+    float *dKx = reinterpret_cast<float *>(ws8);
+    cudaError_t e = dispatch(CAPSCONV_OP_BWD_KERNEL, pe, I, dO, dKx, inner_ws, inner_bytes, cs);
+    if (e == cudaSuccess) e = slices_extract_dk(dKx, dK, KH * KW, C, Cout, S, D2 * D3, cs);
+    return finish(e, "capsconv_bwd_kernel_slices");
 }
 
 const char *capsconv_status_string(capsconv_status_t s) {
