@@ -330,6 +330,168 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dgrad_kernel(const __nv_bflo
     }
 }
 
+// ------------------------------------------------------------------ dK
+// dK[c, c', d2, d3] = sum_{b, d1} I[b, c, d1, d2] * dO[b, c', d1, d3]
+// rows m = (c, d2), columns n = (c', d3), k = (b, d1).  The contraction runs
+// over d1, the row index of both capsules, so a fragment register needs two
+// elements of one capsule *column*: fragment rows g, g+8 = (channel c0 + g/4,
+// c0 + 2 + g/4; d2 = g%4), k-pair (2t, 2t+1) = (image b0 + t, d1 0..1), (2t+8,
+// 2t+9) = (same image, d1 2..3).  A thread loads the whole 32-byte capsule
+// (the four threads of a channel read the same address: an L1 broadcast) and
+// extracts its column pair with one PRMT per register; B (dO) likewise with
+// n = 8nt + g = (c' = 2nt + g/4, d3 = g%4).
+__device__ __forceinline__ void caps_cols(const uint4 &lo, const uint4 &hi, int col, uint32_t &r01, uint32_t &r23) {
+    // capsule words: row d1 = words 2*d1, 2*d1+1 (element d2 at word 2*d1 + d2/2, half d2%2)
+    const uint32_t sel = (col & 1) ? 0x7632u : 0x5410u;
+    const uint32_t w0 = (col & 2) ? lo.y : lo.x;   // row 0
+    const uint32_t w1 = (col & 2) ? lo.w : lo.z;   // row 1
+    const uint32_t w2 = (col & 2) ? hi.y : hi.x;   // row 2
+    const uint32_t w3 = (col & 2) ? hi.w : hi.z;   // row 3
+    r01 = __byte_perm(w0, w1, sel);
+    r23 = __byte_perm(w2, w3, sel);
+}
+
+constexpr int kFcDkNt = 8;     // n-tiles (4*Cout <= 64)
+
+// I stream of the dK kernel: a ring of kDkStages stages, each 4 images x the
+// CTA's 64 channels; an image row holds the 64 low capsule halves (d1 0..1),
+// then the 64 high halves, then 32 B of padding, so that the 8 capsules a
+// warp's fragment read touches (4 images x 2 channels) fall in 8 distinct
+// 16-B bank groups (row stride = 32 mod 128 B).
+constexpr int kDkStages = 8;
+static_assert(kFcWarps * kFcMt * 4 == 64, "fc_dk_kernel stages 64 channels per CTA");
+constexpr int kDkRowBytes = 64 * 32 + 32;
+constexpr int kDkORowBytes = 2 * 16 * 16 + 32;   // dO row: <= 16 low halves, 16 high halves, padding
+constexpr int kDkStageBytes = 4 * kDkRowBytes + 4 * kDkORowBytes;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int NT>
+__global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat16 *__restrict__ I,
+                                                               const __nv_bfloat16 *__restrict__ dO,
+                                                               float *__restrict__ part, int B, int C, int Cout,
+                                                               int bslice) {
+    extern __shared__ __align__(128) uint8_t dk_smem[];
+    uint8_t *ring = dk_smem;   // kDkStages x (4 I rows, then 4 dO rows)
+    const int ks = blockIdx.x, mb = blockIdx.y;
+    const int b_lo = ks * bslice, b_hi = min(B, b_lo + bslice);
+    const int nks = (b_hi - b_lo + 3) / 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int c0 = mb * 64, nc = min(64, C - c0);
+    const uint4 *I16 = reinterpret_cast<const uint4 *>(I);
+    const uint4 *O16 = reinterpret_cast<const uint4 *>(dO);
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    // per-thread copy slots (hoisted): two 16-B I chunks and at most one dO chunk per stage
+    const uint4 *isrc[2];
+    uint32_t idst[2];
+    int iimg[2];
+    bool icc[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int e = threadIdx.x + r * kFcWarps * 32;   // 512 16-B chunks per stage
+        const int img = e >> 7, j = e & 127, cc = j >> 1, hf = j & 1;
+        iimg[r] = img;
+        icc[r] = cc < nc;
+        isrc[r] = I16 + (((size_t)(b_lo + img) * C + c0 + (icc[r] ? cc : 0)) * 2 + hf);
+        idst[r] = img * kDkRowBytes + hf * 1024 + cc * 16;
+    }
+    const bool has_o = threadIdx.x < 8 * Cout;
+    const int oimg = threadIdx.x / (2 * Cout), oj = threadIdx.x % (2 * Cout);
+    const uint4 *osrc = O16 + (((size_t)(b_lo + oimg) * Cout + (oj >> 1)) * 2 + (oj & 1));
+    const uint32_t odst = 4 * kDkRowBytes + oimg * kDkORowBytes + (oj & 1) * 256 + (oj >> 1) * 16;
+    auto issue = [&](int kk) {
+        if (kk < nks) {
+            const uint32_t st = ring_s + (uint32_t)(kk % kDkStages) * kDkStageBytes;
+            const int bb = b_lo + 4 * kk;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const bool ok = icc[r] && bb + iimg[r] < b_hi;
+                cp_async16(st + idst[r], ok ? isrc[r] + (size_t)kk * 8 * C : I16, ok);
+            }
+            if (has_o) {
+                const bool ok = bb + oimg < b_hi;
+                cp_async16(st + odst, ok ? osrc + (size_t)kk * 8 * Cout : O16, ok);
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < kDkStages - 1; ++s0) issue(s0);
+    float acc[kFcMt][NT][4];
+#pragma unroll
+    for (int m = 0; m < kFcMt; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[m][n][e] = 0.f;
+    // Fragment reads: lane (g, t) needs column d2 (A) / d3 (B) = g % 4 of capsules of image t;
+    // column j sits in word j/2 of every capsule row, half j%2 (bf16 pairs are rows d1, d1+1).
+    const int cw = warp * kFcMt * 4;   // first channel of the warp within the CTA block
+    const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+    const int wofs = (g & 2) ? 4 : 0;
+    const uint8_t *abase = ring + t * kDkRowBytes + (cw + (g >> 2)) * 16 + wofs;
+    const uint8_t *obase = ring + 4 * kDkRowBytes + t * kDkORowBytes + (g >> 2) * 16 + wofs;
+    auto w32 = [](const uint8_t *p) { return *reinterpret_cast<const uint32_t *>(p); };
+    for (int k = 0; k < nks; ++k) {
+        cp_async_wait<kDkStages - 2>();
+        __syncthreads();   // stage k landed for all threads; stage k-1 is free
+        issue(k + kDkStages - 1);
+        const int so = (k % kDkStages) * kDkStageBytes;
+        const uint8_t *pa = abase + so, *po = obase + so;
+        uint32_t a[kFcMt][4];
+#pragma unroll
+        for (int m = 0; m < kFcMt; ++m)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint8_t *q = pa + (4 * m + 2 * h) * 16;   // a0/a1: d1 0..1, a2/a3: d1 2..3
+                a[m][h] = __byte_perm(w32(q), w32(q + 8), sel);
+                a[m][h + 2] = __byte_perm(w32(q + 1024), w32(q + 1032), sel);
+            }
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const uint8_t *q = po + 2 * n * 16;   // c' = 2n + g/4; past Cout: garbage columns, never stored
+            const uint32_t b01 = __byte_perm(w32(q), w32(q + 8), sel);
+            const uint32_t b23 = __byte_perm(w32(q + 256), w32(q + 264), sel);
+#pragma unroll
+            for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m][n], a[m], b01, b23);
+        }
+    }
+    cp_async_wait<0>();
+    // partials in dK layout: part[ks][c][c'][d2][d3]; c0,c1 -> row g (c, d2 = g%4),
+    // cols n = 8nt + 2t, +1 = (c' = 2nt + t/2, d3 = 2(t%2), +1); c2,c3 -> channel c + 2
+    float *pk = part + (size_t)ks * C * Cout * 16;
+#pragma unroll
+    for (int m = 0; m < kFcMt; ++m)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + cw + 4 * m + 2 * h + (g >> 2), d2 = g & 3;
+            if (c >= C) continue;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const int co = 2 * n + (t >> 1), d3 = 2 * (t & 1);
+                if (co < Cout)
+                    *reinterpret_cast<float2 *>(pk + (((size_t)c * Cout + co) * 4 + d2) * 4 + d3) =
+                        make_float2(acc[m][n][2 * h], acc[m][n][2 * h + 1]);
+            }
+        }
+}
+
+__global__ void __launch_bounds__(256) fc_dk_finalize(const float *__restrict__ part, float *__restrict__ dK,
+                                                      int64_t n, int ksplit) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float s = 0.f;
+    for (int k = 0; k < ksplit; ++k) s += part[(size_t)k * n + i];
+    dK[i] = s;
+}
+
 }  // namespace
 
 bool fc_hmma_fwd_supported(const Problem &p) {
@@ -425,6 +587,72 @@ cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void 
     fc_dgrad_kernel<<<dim3((unsigned)f.nblocks, (unsigned)f.mblocks), kFcWarps * 32, f.smem, st>>>(
         static_cast<const __nv_bfloat16 *>(dO), wp, static_cast<__nv_bfloat16 *>(dI), f.B, f.C, f.Cout, f.ksteps,
         f.NTall);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+
+namespace {
+struct FcDkPlan {
+    bool ok = false;
+    int B, C, Cout, NT, mblocks, ksplit, bslice;
+    size_t part_bytes;
+};
+FcDkPlan fc_dk_plan(const Problem &p) {
+    FcDkPlan f;
+    const bool full = p.KH == p.H && p.KW == p.W && p.pad == 0;
+    if (!full || p.dt != CAPSCONV_BF16 || p.D1 != 4 || p.D2 != 4 || p.D3 != 4) return f;
+    f.B = (int)p.B;
+    f.C = (int)(p.KH * p.KW * p.C);
+    f.Cout = (int)p.Cout;
+    f.NT = (f.Cout * 4 + 7) / 8;
+    if (f.NT > kFcDkNt || p.B > (1 << 24)) return f;
+    f.mblocks = (f.C + kFcWarps * kFcMt * 4 - 1) / (kFcWarps * kFcMt * 4);
+    // image splits: one wave of two CTAs per SM
+    const int nsm = device_info().num_sms;
+    int ks = std::max(1, (2 * nsm) / f.mblocks);
+    ks = std::min(ks, (f.B + 3) / 4);
+    f.bslice = ((f.B + ks - 1) / ks + 3) / 4 * 4;
+    f.ksplit = (f.B + f.bslice - 1) / f.bslice;
+    f.part_bytes = ((size_t)f.ksplit * f.C * f.Cout * 16 * 4 + 255) & ~(size_t)255;
+    f.ok = true;
+    return f;
+}
+}  // namespace
+
+bool fc_hmma_dk_supported(const Problem &p) {
+    static const bool off = getenv("CAPSCONV_NO_FC_HMMA") != nullptr;
+    return !off && fc_dk_plan(p).ok;
+}
+
+size_t fc_hmma_dk_workspace(const Problem &p) {
+    const FcDkPlan f = fc_dk_plan(p);
+    return f.ok ? f.part_bytes : 0;
+}
+
+cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    const FcDkPlan f = fc_dk_plan(p);
+    if (!f.ok || ws_bytes < f.part_bytes) return cudaErrorInvalidValue;
+    float *part = static_cast<float *>(ws);
+    const dim3 grid((unsigned)f.ksplit, (unsigned)f.mblocks);
+    const __nv_bfloat16 *Ib = static_cast<const __nv_bfloat16 *>(I), *Ob = static_cast<const __nv_bfloat16 *>(dO);
+    const uint32_t smem = kDkStages * kDkStageBytes;
+    cudaError_t e = cudaSuccess;
+    switch (f.NT) {
+#define DK_CASE(nt)                                                                                         \
+    case nt:                                                                                                \
+        e = cudaFuncSetAttribute(fc_dk_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        if (e != cudaSuccess) return e;                                                                         \
+        fc_dk_kernel<nt><<<grid, kFcWarps * 32, smem, st>>>(Ib, Ob, part, f.B, f.C, f.Cout, f.bslice);       \
+        break;
+        DK_CASE(1) DK_CASE(2) DK_CASE(3) DK_CASE(4) DK_CASE(5) DK_CASE(6) DK_CASE(7) DK_CASE(8)
+#undef DK_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    note_launches(1);
+    const int64_t n = (int64_t)f.C * f.Cout * 16;
+    fc_dk_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, dK, n, f.ksplit);
     note_launches(1);
     return cudaGetLastError();
 }

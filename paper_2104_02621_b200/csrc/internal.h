@@ -56,6 +56,10 @@ cudaError_t slices_expand_kernel(capsconv_dtype_t dt, const void *K, void *Kx, i
                                  int64_t S, int64_t D23, cudaStream_t st);
 cudaError_t slices_extract_dk(const float *dKx, float *dK, int64_t taps, int64_t C, int64_t Cout, int64_t S,
                               int64_t D23, cudaStream_t st);
+bool fc_hmma_dk_supported(const Problem &p);
+size_t fc_hmma_dk_workspace(const Problem &p);
+cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
+                       cudaStream_t st);
 bool fc_hmma_dgrad_supported(const Problem &p);
 size_t fc_hmma_dgrad_workspace(const Problem &p);
 cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,

@@ -1063,14 +1063,14 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
 }  // namespace
 
 bool mma_supported(capsconv_op_t op, const Problem &p) {
-    if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_supported(p);
+    if (op == CAPSCONV_OP_BWD_KERNEL) return fc_hmma_dk_supported(p) || wgrad_supported(p);
     if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return true;
     if (op == CAPSCONV_OP_BWD_DATA && fc_hmma_dgrad_supported(p)) return true;
     return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
 }
 
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
-    if (op == CAPSCONV_OP_BWD_KERNEL) return wgrad_workspace_bytes(p);
+    if (op == CAPSCONV_OP_BWD_KERNEL) return fc_hmma_dk_supported(p) ? fc_hmma_dk_workspace(p) : wgrad_workspace_bytes(p);
     if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return fc_hmma_fwd_workspace(p);
     if (op == CAPSCONV_OP_BWD_DATA && fc_hmma_dgrad_supported(p)) return fc_hmma_dgrad_workspace(p);
     const Plan &pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
@@ -1095,6 +1095,7 @@ cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *
 
 cudaError_t mma_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
                            cudaStream_t st) {
+    if (fc_hmma_dk_supported(p)) return fc_hmma_dk(p, I, dO, dK, ws, ws_bytes, st);
     return wgrad_run(p, I, dO, dK, ws, ws_bytes, st);
 }
 
