@@ -31,6 +31,15 @@ constexpr int kFcWarps = 8;
 constexpr int kFcMt = 2;          // m-tiles (16 rows) per warp
 constexpr int kFcMaxNt = 8;       // n-tiles of 8 columns (N <= 64)
 
+// I stream of the forward kernel: a ring of kFwdStages stages, each kFwdKs
+// k-steps of the CTA's 64 images (image row = kFwdKs * 4 channels * 32 B,
+// contiguous in I); a warp's fragment read (4 images x 128 B) is 4 wavefronts.
+constexpr int kFwdStages = 4;
+constexpr int kFwdKs = 2;
+constexpr int kFwdRowBytes = kFwdKs * 128;
+constexpr int kFwdStageBytes = 64 * kFwdRowBytes;
+static_assert(kFcWarps * kFcMt * 4 == 64, "fc_fwd_kernel stages 64 images per CTA");
+
 struct FcPlan {
     bool ok = false;
     int B, C, Cout, NT;           // NT = n-tiles of 8
@@ -54,14 +63,15 @@ FcPlan fc_plan(const Problem &p) {
     const int rows = f.B * 4;
     f.mblocks = (rows + kFcWarps * kFcMt * 16 - 1) / (kFcWarps * kFcMt * 16);
     // K splits: one wave of two CTAs per SM (a partial second wave doubles the
-    // kernel time), slices of at most 64 k-steps (weight slice <= 64*NT*256 B)
+    // kernel time), weight slices of at most 48 KB (beside the 64 KB I ring)
     const int nsm = device_info().num_sms;
     int ks = std::max(1, (2 * nsm) / f.mblocks);
-    ks = std::max(ks, (f.ksteps + 63) / 64);
+    const int kmax = (48 * 1024) / (f.NT * 256);   // weight slice <= 48 KB: two CTAs per SM with the I ring
+    ks = std::max(ks, (f.ksteps + kmax - 1) / kmax);
     ks = std::min(ks, f.ksteps);
     f.kslice = (f.ksteps + ks - 1) / ks;
     f.ksplit = (f.ksteps + f.kslice - 1) / f.kslice;
-    f.smem = (uint32_t)f.kslice * f.NT * 256u;
+    f.smem = kFwdStages * kFwdStageBytes + (uint32_t)f.kslice * f.NT * 256u;
     f.wpack_bytes = ((size_t)f.ksteps * f.NT * 256 + 255) & ~(size_t)255;
     f.part_bytes = ((size_t)f.ksplit * rows * f.NT * 8 * 4 + 255) & ~(size_t)255;
     f.ok = true;
@@ -104,6 +114,14 @@ __global__ void __launch_bounds__(256) fc_pack(const __nv_bfloat16 *__restrict__
     reinterpret_cast<uint2 *>(wp)[idx] = make_uint2(out[0], out[1]);
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ void hmma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -130,22 +148,46 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat
                                                                 const uint32_t *__restrict__ wp,
                                                                 float *__restrict__ part, int B, int C, int kslice,
                                                                 int ksteps) {
-    extern __shared__ __align__(16) uint32_t wsm[];
+    extern __shared__ __align__(128) uint8_t fw_smem[];
+    uint8_t *ring = fw_smem;
+    uint32_t *wsm = reinterpret_cast<uint32_t *>(fw_smem + kFwdStages * kFwdStageBytes);
     const int ks = blockIdx.x, mb = blockIdx.y;
     const int k0 = ks * kslice, k1 = min(ksteps, k0 + kslice);
     const int nk = k1 - k0;
-    // weight slice -> shared memory (fragment order, contiguous in global)
+    const int nst = (nk + kFwdKs - 1) / kFwdKs;
+    const int b_lo = mb * 64;
+    const uint4 *I16 = reinterpret_cast<const uint4 *>(I);
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    // per-thread copy slots: 64 images x kFwdKs*8 chunks of 16 B per stage
+    constexpr int kChunks = 64 * kFwdKs * 8 / (kFcWarps * 32);
+    auto issue = [&](int st) {
+        if (st < nst) {
+            const uint32_t dst0 = ring_s + (uint32_t)(st % kFwdStages) * kFwdStageBytes;
+#pragma unroll
+            for (int r = 0; r < kChunks; ++r) {
+                const int e = threadIdx.x + r * kFcWarps * 32;
+                const int img = e / (kFwdKs * 8), j = e % (kFwdKs * 8);
+                const int b = b_lo + img, kstep = k0 + st * kFwdKs + j / 8;
+                const bool ok = b < B && kstep < k1;
+                const uint4 *src = ok ? I16 + (((size_t)b * C + 4 * kstep) * 2 + (j & 7)) : I16;
+                cp_async16(dst0 + img * kFwdRowBytes + j * 16, src, ok);
+            }
+        }
+        cp_async_commit();
+    };
+    // weight slice -> shared memory (fragment order, contiguous in global), committed
+    // with I stage 0, so the first stage wait covers it
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(wp + (size_t)k0 * NT * 64);
-        uint4 *dst = reinterpret_cast<uint4 *>(wsm);
-        for (int i = threadIdx.x; i < nk * NT * 16; i += blockDim.x) dst[i] = src[i];
+        const uint32_t ws0 = (uint32_t)__cvta_generic_to_shared(wsm);
+        for (int i = threadIdx.x; i < nk * NT * 16; i += blockDim.x) cp_async16(ws0 + i * 16, src + i, true);
     }
-    __syncthreads();
+#pragma unroll
+    for (int s0 = 0; s0 < kFwdStages - 1; ++s0) issue(s0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int rows = B * 4;
     const int r0 = (mb * kFcWarps + warp) * kFcMt * 16;   // first row (= 4 * first image) of the warp
-    const uint4 *I16 = reinterpret_cast<const uint4 *>(I);
     float acc[kFcMt][NT][4];
 #pragma unroll
     for (int m = 0; m < kFcMt; ++m)
@@ -153,33 +195,34 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat
         for (int n = 0; n < NT; ++n)
 #pragma unroll
             for (int e = 0; e < 4; ++e) acc[m][n][e] = 0.f;
-    // software pipeline: the A fragments of the next kPf k-steps are in flight
-    constexpr int kPf = 4;
-    uint32_t a[kPf][kFcMt][4];
+    // lane (g, t) of m-tile m: image 8*warp + 4m + g/2, channel 4*kstep + t, half g%2
+    // = {a0, a2, a1, a3} (see load_a)
+    const uint8_t *abase = ring + (8 * warp + (g >> 1)) * kFwdRowBytes + t * 32 + (g & 1) * 16;
+    for (int st = 0; st < nst; ++st) {
+        cp_async_wait<kFwdStages - 2>();
+        __syncthreads();   // stage st landed for all threads (and, at st = 0, the weights); st-1 is free
+        issue(st + kFwdStages - 1);
+        const uint8_t *pa = abase + (st % kFwdStages) * kFwdStageBytes;
 #pragma unroll
-    for (int j = 0; j < kPf; ++j)
+        for (int j = 0; j < kFwdKs; ++j) {
+            const int kk = st * kFwdKs + j;
+            if (kk < nk) {
+                uint32_t a[kFcMt][4];
 #pragma unroll
-        for (int m = 0; m < kFcMt; ++m) {
-            if (j < nk) load_a(I16, C, B, (r0 >> 2) + 4 * m, k0 + j, g, t, a[j][m]);
-            else { a[j][m][0] = a[j][m][1] = a[j][m][2] = a[j][m][3] = 0u; }
-        }
-    for (int kk = 0; kk < nk; kk += kPf) {
-#pragma unroll
-        for (int j = 0; j < kPf; ++j) {
-            if (kk + j < nk) {
+                for (int m = 0; m < kFcMt; ++m) {
+                    const uint4 v = *reinterpret_cast<const uint4 *>(pa + 4 * m * kFwdRowBytes + j * 128);
+                    a[m][0] = v.x; a[m][2] = v.y; a[m][1] = v.z; a[m][3] = v.w;
+                }
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
-                    const uint2 bb = reinterpret_cast<const uint2 *>(wsm)[((kk + j) * NT + n) * 32 + lane];
+                    const uint2 bb = reinterpret_cast<const uint2 *>(wsm)[(kk * NT + n) * 32 + lane];
 #pragma unroll
-                    for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m][n], a[j][m], bb.x, bb.y);
+                    for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m][n], a[m], bb.x, bb.y);
                 }
             }
-            // refill this slot with k-step kk + j + kPf
-#pragma unroll
-            for (int m = 0; m < kFcMt; ++m)
-                if (kk + j + kPf < nk) load_a(I16, C, B, (r0 >> 2) + 4 * m, k0 + kk + j + kPf, g, t, a[j][m]);
         }
     }
+    cp_async_wait<0>();
     // partials part[ks][row = 4b + d1][NT*8]: c0,c1 -> fragment row g = (image g/2,
     // d1 = 2(g%2)), cols 2t, 2t+1; c2,c3 -> row g + 8 = (same image, d1 + 1)
     const int ncol = NT * 8;
@@ -211,6 +254,7 @@ __global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ par
     const int64_t b = r >> 2;
     const int d1 = (int)(r & 3);
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
     for (int k = 0; k < ksplit; ++k) {
         const float4 v = *reinterpret_cast<const float4 *>(part + ((size_t)k * rows + r) * ncol + co * 4);
         s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
@@ -260,25 +304,28 @@ __global__ void __launch_bounds__(256) fc_pack_dgrad(const __nv_bfloat16 *__rest
 }
 
 constexpr int kFcDgKs = 4;     // max k-steps (4*Cout <= 64)
-constexpr int kFcDgNt = 64;    // n-tiles per CTA column block (512 columns)
+constexpr int kFcDgNt = 64;    // max n-tiles per CTA column block (512 columns)
 
 // CTA = (column block of kFcDgNt n-tiles, 8 warps x 2 m-tiles of rows); each
 // warp loads its dO fragments once and walks the column block.
 __global__ void __launch_bounds__(kFcWarps * 32) fc_dgrad_kernel(const __nv_bfloat16 *__restrict__ dO,
                                                                   const uint32_t *__restrict__ wp,
                                                                   __nv_bfloat16 *__restrict__ dI, int B, int C,
-                                                                  int Cout, int ksteps, int NTall) {
+                                                                  int Cout, int ksteps, int NTall, int ntper) {
     extern __shared__ __align__(16) uint32_t wsm[];
     const int nb = blockIdx.x, mb = blockIdx.y;
-    const int nt0 = nb * kFcDgNt, nt1 = min(NTall, nt0 + kFcDgNt);
+    const int nt0 = nb * ntper, nt1 = min(NTall, nt0 + ntper);
     const int nnt = nt1 - nt0;
-    // weights of this column block, all k-steps: wsm[kstep][ntl][lane]
-    for (int i = threadIdx.x; i < ksteps * nnt * 16; i += blockDim.x) {
-        const int kstep = i / (nnt * 16), rem = i - kstep * nnt * 16;
-        reinterpret_cast<uint4 *>(wsm)[i] =
-            reinterpret_cast<const uint4 *>(wp)[((size_t)kstep * NTall + nt0) * 16 + rem];
+    // weights of this column block, all k-steps: wsm[kstep][ntl][lane] (async, overlaps the dO loads)
+    {
+        const uint32_t ws0 = (uint32_t)__cvta_generic_to_shared(wsm);
+        for (int i = threadIdx.x; i < ksteps * nnt * 16; i += blockDim.x) {
+            const int kstep = i / (nnt * 16), rem = i - kstep * nnt * 16;
+            cp_async16(ws0 + i * 16, reinterpret_cast<const uint4 *>(wp) + ((size_t)kstep * NTall + nt0) * 16 + rem,
+                       true);
+        }
+        cp_async_commit();
     }
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int img0 = (mb * kFcWarps + warp) * kFcMt * 4;   // first image of the warp
@@ -294,6 +341,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dgrad_kernel(const __nv_bflo
                 a[j][m][0] = v.x; a[j][m][2] = v.y; a[j][m][1] = v.z; a[j][m][3] = v.w;
             }
         }
+    cp_async_wait<0>();
+    __syncthreads();
     for (int ntl = 0; ntl < nnt; ++ntl) {
         float acc[kFcMt][4];
 #pragma unroll
@@ -363,14 +412,6 @@ static_assert(kFcWarps * kFcMt * 4 == 64, "fc_dk_kernel stages 64 channels per C
 constexpr int kDkRowBytes = 64 * 32 + 32;
 constexpr int kDkORowBytes = 2 * 16 * 16 + 32;   // dO row: <= 16 low halves, 16 high halves, padding
 constexpr int kDkStageBytes = 4 * kDkRowBytes + 4 * kDkORowBytes;
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int NT>
 __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat16 *__restrict__ I,
@@ -540,7 +581,7 @@ cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O,
 namespace {
 struct FcDgPlan {
     bool ok = false;
-    int B, C, Cout, ksteps, NTall, nblocks, mblocks;
+    int B, C, Cout, ksteps, NTall, ntper, nblocks, mblocks;
     size_t wpack_bytes;
     uint32_t smem;
 };
@@ -554,9 +595,13 @@ FcDgPlan fc_dg_plan(const Problem &p) {
     f.ksteps = (f.Cout + 3) / 4;
     if (f.ksteps > kFcDgKs || p.B > (1 << 24)) return f;
     f.NTall = (f.C * 4 + 7) / 8;
-    f.nblocks = (f.NTall + kFcDgNt - 1) / kFcDgNt;
     f.mblocks = (f.B + kFcWarps * kFcMt * 4 - 1) / (kFcWarps * kFcMt * 4);
-    f.smem = (uint32_t)f.ksteps * kFcDgNt * 256u;
+    // column blocks: one wave of three CTAs per SM (72 registers x 256 threads)
+    const int nsm = device_info().num_sms;
+    const int nb = std::max(1, (3 * nsm) / f.mblocks);
+    f.ntper = std::min(kFcDgNt, (f.NTall + nb - 1) / nb);
+    f.nblocks = (f.NTall + f.ntper - 1) / f.ntper;
+    f.smem = (uint32_t)f.ksteps * f.ntper * 256u;
     f.wpack_bytes = ((size_t)f.ksteps * f.NTall * 256 + 255) & ~(size_t)255;
     f.ok = true;
     return f;
@@ -586,7 +631,7 @@ cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void 
     if (e != cudaSuccess) return e;
     fc_dgrad_kernel<<<dim3((unsigned)f.nblocks, (unsigned)f.mblocks), kFcWarps * 32, f.smem, st>>>(
         static_cast<const __nv_bfloat16 *>(dO), wp, static_cast<__nv_bfloat16 *>(dI), f.B, f.C, f.Cout, f.ksteps,
-        f.NTall);
+        f.NTall, f.ntper);
     note_launches(1);
     return cudaGetLastError();
 }
