@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "umma.cuh"
 
 namespace capsconv {
 namespace {
@@ -400,71 +401,67 @@ __device__ __forceinline__ void caps_cols(const uint4 &lo, const uint4 &hi, int 
     r23 = __byte_perm(w2, w3, sel);
 }
 
+using namespace umma;   // mbarriers and 1-D bulk copies of the dK stream
 constexpr int kFcDkNt = 8;     // n-tiles (4*Cout <= 64)
 
-// I stream of the dK kernel: a ring of kDkStages stages, each 4 images x the
-// CTA's 64 channels; an image row holds the 64 low capsule halves (d1 0..1),
-// then the 64 high halves, then 32 B of padding, so that the 8 capsules a
-// warp's fragment read touches (4 images x 2 channels) fall in 8 distinct
-// 16-B bank groups (row stride = 32 mod 128 B).
-constexpr int kDkStages = 8;
+// I / dO stream of the dK kernel: a ring of kDkStages stages, each the 4
+// images of one k-step: the CTA's 64 channels of I (one 1-D bulk copy per
+// image, <= 2 KB) and the image's dO (<= 16 capsules), completion on one
+// mbarrier per stage.  Image row t sits at t * row + {0, 16, 64, 80}[t] bytes:
+// a warp's 32-bit fragment read touches, per image, the banks {0,1,8,9} + x
+// (two channels 32 B apart, two column words), and the per-image offsets
+// {0, 4, 16, 20} banks keep the four images disjoint -- one wavefront.
+constexpr int kDkStages = 4;
+constexpr int kDkKs = 2;            // k-steps (4 images each) per stage
+constexpr int kDkImg = 4 * kDkKs;   // images per stage
 static_assert(kFcWarps * kFcMt * 4 == 64, "fc_dk_kernel stages 64 channels per CTA");
-constexpr int kDkRowBytes = 64 * 32 + 32;
-constexpr int kDkORowBytes = 2 * 16 * 16 + 32;   // dO row: <= 16 low halves, 16 high halves, padding
-constexpr int kDkStageBytes = 4 * kDkRowBytes + 4 * kDkORowBytes;
+constexpr int kDkIRow = 64 * 32 + 128;
+constexpr int kDkORow = 16 * 32 + 128;
+constexpr int kDkStageBytes = kDkImg * kDkIRow + kDkImg * kDkORow;
+constexpr uint32_t kDkBfrBytes = 2 * kDkKs * kFcDkNt * 32 * 8;
+__device__ __forceinline__ int dk_row_extra(int t) { return ((t & 1) ? 16 : 0) + ((t & 2) ? 64 : 0); }
 
 template <int NT>
 __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat16 *__restrict__ I,
                                                                const __nv_bfloat16 *__restrict__ dO,
                                                                float *__restrict__ part, int B, int C, int Cout,
-                                                               int bslice) {
+                                                               int bslice, int dbg) {
     extern __shared__ __align__(128) uint8_t dk_smem[];
     uint8_t *ring = dk_smem;   // kDkStages x (4 I rows, then 4 dO rows)
+    uint2 *bfr = reinterpret_cast<uint2 *>(dk_smem + kDkStages * kDkStageBytes);   // [2][kDkKs][NT][32] B fragments
+    uint64_t *full = reinterpret_cast<uint64_t *>(dk_smem + kDkStages * kDkStageBytes + kDkBfrBytes);
     const int ks = blockIdx.x, mb = blockIdx.y;
     const int b_lo = ks * bslice, b_hi = min(B, b_lo + bslice);
-    const int nks = (b_hi - b_lo + 3) / 4;
+    const int nimg = b_hi - b_lo;
+    const int nks = (nimg + 3) / 4;                 // k-steps
+    const int nst = (nimg + kDkImg - 1) / kDkImg;   // stages
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     const int c0 = mb * 64, nc = min(64, C - c0);
-    const uint4 *I16 = reinterpret_cast<const uint4 *>(I);
-    const uint4 *O16 = reinterpret_cast<const uint4 *>(dO);
-    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
-    // per-thread copy slots (hoisted): two 16-B I chunks and at most one dO chunk per stage
-    const uint4 *isrc[2];
-    uint32_t idst[2];
-    int iimg[2];
-    bool icc[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const int e = threadIdx.x + r * kFcWarps * 32;   // 512 16-B chunks per stage
-        const int img = e >> 7, j = e & 127, cc = j >> 1, hf = j & 1;
-        iimg[r] = img;
-        icc[r] = cc < nc;
-        isrc[r] = I16 + (((size_t)(b_lo + img) * C + c0 + (icc[r] ? cc : 0)) * 2 + hf);
-        idst[r] = img * kDkRowBytes + hf * 1024 + cc * 16;
+    if (threadIdx.x == 0) {
+        for (int s0 = 0; s0 < kDkStages; ++s0) mbar_init(&full[s0], 1);
+        mbar_fence_init();
     }
-    const bool has_o = threadIdx.x < 8 * Cout;
-    const int oimg = threadIdx.x / (2 * Cout), oj = threadIdx.x % (2 * Cout);
-    const uint4 *osrc = O16 + (((size_t)(b_lo + oimg) * Cout + (oj >> 1)) * 2 + (oj & 1));
-    const uint32_t odst = 4 * kDkRowBytes + oimg * kDkORowBytes + (oj & 1) * 256 + (oj >> 1) * 16;
-    auto issue = [&](int kk) {
-        if (kk < nks) {
-            const uint32_t st = ring_s + (uint32_t)(kk % kDkStages) * kDkStageBytes;
-            const int bb = b_lo + 4 * kk;
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const bool ok = icc[r] && bb + iimg[r] < b_hi;
-                cp_async16(st + idst[r], ok ? isrc[r] + (size_t)kk * 8 * C : I16, ok);
-            }
-            if (has_o) {
-                const bool ok = bb + oimg < b_hi;
-                cp_async16(st + odst, ok ? osrc + (size_t)kk * 8 * Cout : O16, ok);
-            }
+    __syncthreads();
+    // thread 0: stage ss <- images b_lo + kDkImg*ss .. (valid ones only; the rest are masked in the fragments)
+    auto issue = [&](int ss) {
+        if (ss >= nst || (dbg & 1)) return;
+        uint8_t *st = ring + (ss % kDkStages) * kDkStageBytes;
+        const int ni = min(kDkImg, nimg - kDkImg * ss);
+        mbar_arrive_expect_tx(&full[ss % kDkStages], (uint32_t)ni * (nc + Cout) * 32u);
+        for (int tt = 0; tt < ni; ++tt) {
+            const size_t b = (size_t)(b_lo + kDkImg * ss + tt);
+            bulk_g2s(st + tt * kDkIRow + dk_row_extra(tt), I + (b * C + c0) * 16, (uint32_t)nc * 32u,
+                     &full[ss % kDkStages]);
+            bulk_g2s(st + kDkImg * kDkIRow + tt * kDkORow + dk_row_extra(tt), dO + b * Cout * 16,
+                     (uint32_t)Cout * 32u, &full[ss % kDkStages]);
         }
-        cp_async_commit();
     };
-#pragma unroll
-    for (int s0 = 0; s0 < kDkStages - 1; ++s0) issue(s0);
+    auto wait_stage = [&](int ss) {
+        if (ss < nst && !(dbg & 1)) mbar_wait(&full[ss % kDkStages], (uint32_t)(ss / kDkStages) & 1u);
+    };
+    if (threadIdx.x == 0)
+        for (int s0 = 0; s0 < kDkStages - 1; ++s0) issue(s0);
     float acc[kFcMt][NT][4];
 #pragma unroll
     for (int m = 0; m < kFcMt; ++m)
@@ -473,38 +470,60 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
 #pragma unroll
             for (int e = 0; e < 4; ++e) acc[m][n][e] = 0.f;
     // Fragment reads: lane (g, t) needs column d2 (A) / d3 (B) = g % 4 of capsules of image t;
-    // column j sits in word j/2 of every capsule row, half j%2 (bf16 pairs are rows d1, d1+1).
+    // column j sits in word j/2 of every capsule row (8 B), half j%2.
     const int cw = warp * kFcMt * 4;   // first channel of the warp within the CTA block
     const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
     const int wofs = (g & 2) ? 4 : 0;
-    const uint8_t *abase = ring + t * kDkRowBytes + (cw + (g >> 2)) * 16 + wofs;
-    const uint8_t *obase = ring + 4 * kDkRowBytes + t * kDkORowBytes + (g >> 2) * 16 + wofs;
+    const uint8_t *abase = ring + t * kDkIRow + dk_row_extra(t) + (cw + (g >> 2)) * 32 + wofs;
     auto w32 = [](const uint8_t *p) { return *reinterpret_cast<const uint32_t *>(p); };
-    for (int k = 0; k < nks; ++k) {
-        cp_async_wait<kDkStages - 2>();
-        __syncthreads();   // stage k landed for all threads; stage k-1 is free
-        issue(k + kDkStages - 1);
-        const int so = (k % kDkStages) * kDkStageBytes;
-        const uint8_t *pa = abase + so, *po = obase + so;
+    // B fragments are the same for every warp: the CTA extracts those of stage ss
+    // into bfr[ss % 2] one iteration ahead (entry e = (j, n, lane), j the k-step in the stage)
+    auto extract_b = [&](int ss) {
+        if (ss >= nst) return;
+        for (int e = threadIdx.x; e < kDkKs * NT * 32; e += kFcWarps * 32) {
+            const int j = e / (NT * 32), n = (e >> 5) % NT, ln = e & 31, gg = ln >> 2, tt = ln & 3;
+            const int im = 4 * j + tt;   // image within the stage
+            uint2 v = make_uint2(0u, 0u);
+            if (kDkImg * ss + im < nimg) {
+                const uint32_t sl = (gg & 1) ? 0x7632u : 0x5410u;
+                const uint8_t *q = ring + (ss % kDkStages) * kDkStageBytes + kDkImg * kDkIRow + im * kDkORow +
+                                   dk_row_extra(tt) + (2 * n + (gg >> 2)) * 32 + ((gg & 2) ? 4 : 0);
+                v = make_uint2(__byte_perm(w32(q), w32(q + 8), sl), __byte_perm(w32(q + 16), w32(q + 24), sl));
+            }
+            bfr[(ss & 1) * kDkKs * NT * 32 + e] = v;
+        }
+    };
+    wait_stage(0);
+    extract_b(0);
+    for (int ss = 0; ss < nst; ++ss) {
+        wait_stage(ss + 1);
+        __syncthreads();   // B(ss) extracted; every thread is done with stage ss-1 (and waited for ss, ss+1)
+        if (threadIdx.x == 0) issue(ss + kDkStages - 1);
+        extract_b(ss + 1);
+        if (dbg & 2) continue;
+#pragma unroll
+        for (int j = 0; j < kDkKs; ++j) {
+        const int k = ss * kDkKs + j;
+        if (k >= nks) break;
+        const uint8_t *pa = abase + (ss % kDkStages) * kDkStageBytes + 4 * j * kDkIRow;
+        const bool tv = 4 * k + t < nimg;   // past the slice: zero A (smem holds stale data)
         uint32_t a[kFcMt][4];
 #pragma unroll
         for (int m = 0; m < kFcMt; ++m)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const uint8_t *q = pa + (4 * m + 2 * h) * 16;   // a0/a1: d1 0..1, a2/a3: d1 2..3
-                a[m][h] = __byte_perm(w32(q), w32(q + 8), sel);
-                a[m][h + 2] = __byte_perm(w32(q + 1024), w32(q + 1032), sel);
+                const uint8_t *q = pa + (4 * m + 2 * h) * 32;   // a0/a1: d1 0..1, a2/a3: d1 2..3
+                a[m][h] = tv ? __byte_perm(w32(q), w32(q + 8), sel) : 0u;
+                a[m][h + 2] = tv ? __byte_perm(w32(q + 16), w32(q + 24), sel) : 0u;
             }
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            const uint8_t *q = po + 2 * n * 16;   // c' = 2n + g/4; past Cout: garbage columns, never stored
-            const uint32_t b01 = __byte_perm(w32(q), w32(q + 8), sel);
-            const uint32_t b23 = __byte_perm(w32(q + 256), w32(q + 264), sel);
+        for (int n = 0; n < NT; ++n) {   // c' = 2n + g/4; past Cout: garbage columns, never stored
+            const uint2 bb = bfr[((ss & 1) * kDkKs + j) * NT * 32 + n * 32 + lane];
 #pragma unroll
-            for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m][n], a[m], b01, b23);
+            for (int m = 0; m < kFcMt; ++m) hmma16816(acc[m][n], a[m], bb.x, bb.y);
+        }
         }
     }
-    cp_async_wait<0>();
     // partials in dK layout: part[ks][c][c'][d2][d3]; c0,c1 -> row g (c, d2 = g%4),
     // cols n = 8nt + 2t, +1 = (c' = 2nt + t/2, d3 = 2(t%2), +1); c2,c3 -> channel c + 2
     float *pk = part + (size_t)ks * C * Cout * 16;
@@ -526,11 +545,16 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
 
 __global__ void __launch_bounds__(256) fc_dk_finalize(const float *__restrict__ part, float *__restrict__ dK,
                                                       int64_t n, int ksplit) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float s = 0.f;
-    for (int k = 0; k < ksplit; ++k) s += part[(size_t)k * n + i];
-    dK[i] = s;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // float4 index, n % 4 == 0
+    if (i >= n / 4) return;
+    const float4 *p4 = reinterpret_cast<const float4 *>(part);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int k = 0; k < ksplit; ++k) {
+        const float4 v = p4[(size_t)k * (n / 4) + i];
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    reinterpret_cast<float4 *>(dK)[i] = s;
 }
 
 }  // namespace
@@ -682,14 +706,15 @@ cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *d
     float *part = static_cast<float *>(ws);
     const dim3 grid((unsigned)f.ksplit, (unsigned)f.mblocks);
     const __nv_bfloat16 *Ib = static_cast<const __nv_bfloat16 *>(I), *Ob = static_cast<const __nv_bfloat16 *>(dO);
-    const uint32_t smem = kDkStages * kDkStageBytes;
+    const uint32_t smem = kDkStages * kDkStageBytes + kDkBfrBytes + kDkStages * 8;
+    static const int dbg = getenv("CAPSCONV_FC_DBG") ? atoi(getenv("CAPSCONV_FC_DBG")) : 0;   // probe only
     cudaError_t e = cudaSuccess;
     switch (f.NT) {
 #define DK_CASE(nt)                                                                                         \
     case nt:                                                                                                \
         e = cudaFuncSetAttribute(fc_dk_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
         if (e != cudaSuccess) return e;                                                                         \
-        fc_dk_kernel<nt><<<grid, kFcWarps * 32, smem, st>>>(Ib, Ob, part, f.B, f.C, f.Cout, f.bslice);       \
+        fc_dk_kernel<nt><<<grid, kFcWarps * 32, smem, st>>>(Ib, Ob, part, f.B, f.C, f.Cout, f.bslice, dbg);       \
         break;
         DK_CASE(1) DK_CASE(2) DK_CASE(3) DK_CASE(4) DK_CASE(5) DK_CASE(6) DK_CASE(7) DK_CASE(8)
 #undef DK_CASE
@@ -697,7 +722,7 @@ cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *d
     }
     note_launches(1);
     const int64_t n = (int64_t)f.C * f.Cout * 16;
-    fc_dk_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, dK, n, f.ksplit);
+    fc_dk_finalize<<<(unsigned)((n / 4 + 255) / 256), 256, 0, st>>>(part, dK, n, f.ksplit);
     note_launches(1);
     return cudaGetLastError();
 }
