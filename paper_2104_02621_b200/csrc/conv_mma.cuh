@@ -112,7 +112,7 @@ struct ConvMma {
     int b_resident;            // one B stage for the whole kernel
     uint32_t smem_bytes;
     uint32_t tmem_cols;
-    int dbg;                   // bench-only bits: 1 skip loads, 2 skip MMAs, 4 skip stores
+    int dbg;                   // bench-only bits: 1 skip loads, 2 skip MMAs, 4 skip stores, 64 skip repack
     unsigned long long *trace; // debug: globaltimer stamps of CTA 0 [role][item][4]
 };
 

@@ -255,8 +255,10 @@ __device__ __forceinline__ void build_table(const ConvMma &P, const Item &it, ui
 }
 
 __device__ __forceinline__ void repack_rows(const ConvMma &P, uint32_t stg, uint32_t tab, uint32_t a_stage, int tid) {
-    // thread -> fixed unit (c, i); pixels advance by pstep = threads / units
-    // with incremental (plane, pixel) counters: no division, no plane loop
+    // thread -> fixed unit (c, i); pixels advance by pstep = threads / units.
+    // Plane-outer loop and batches of 4 pixels: the table loads, then the
+    // staged-unit loads, then the stores, so each thread has 4 smem round
+    // trips in flight instead of one dependent chain per pixel.
     const int upp = 2 * P.CC;
     const int pstep = kProducerThreads / upp;
     const int p0 = tid / upp, u2 = tid - p0 * upp;
@@ -265,20 +267,32 @@ __device__ __forceinline__ void repack_rows(const ConvMma &P, uint32_t stg, uint
     const uint32_t px_bytes = (uint32_t)P.CC * 32u;
     const uint32_t soff = (uint32_t)u2 * 16u;
     const uint32_t dcol = a_stage + (c >> 1) * P.a_lbo + (uint32_t)(2 * i) * 16u + (c & 1) * 8u;
-    const int total = P.npl * P.win_px;
-    int k = 0, vl = p0;
-    while (vl >= P.win_px) { vl -= P.win_px; ++k; }
-#pragma unroll 2
-    for (int pix = p0; pix < total; pix += pstep) {
-        int idx;
-        asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx) : "r"(tab + (uint32_t)pix * 4u));
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (idx >= 0) v = ld_shared_v4(stg + (uint32_t)idx * px_bytes + soff);
-        const uint32_t dst = dcol + k * P.plane_bytes + (uint32_t)vl * 64u;
-        st_shared_v2(dst, v.x, v.y);
-        st_shared_v2(dst + 16u, v.z, v.w);
-        vl += pstep;
-        while (vl >= P.win_px) { vl -= P.win_px; ++k; }
+    for (int k = 0; k < P.npl; ++k) {
+        const uint32_t tabk = tab + (uint32_t)(k * P.win_px) * 4u;
+        const uint32_t dstk = dcol + k * P.plane_bytes;
+        for (int vl = p0; vl < P.win_px; vl += 4 * pstep) {
+            int idx[4];
+            uint4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                idx[j] = -1;
+                if (vl + j * pstep < P.win_px)
+                    asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(idx[j]) : "r"(tabk + (uint32_t)(vl + j * pstep) * 4u));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[j] = make_uint4(0, 0, 0, 0);
+                if (idx[j] >= 0) v[j] = ld_shared_v4(stg + (uint32_t)idx[j] * px_bytes + soff);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (vl + j * pstep < P.win_px) {
+                    const uint32_t dst = dstk + (uint32_t)(vl + j * pstep) * 64u;
+                    st_shared_v2(dst, v[j].x, v[j].y);
+                    st_shared_v2(dst + 16u, v[j].z, v[j].w);
+                }
+            }
+        }
     }
 }
 
@@ -433,7 +447,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 }
                 mbar_wait(stg_full + sb, sphase);
                 if (tid == 0) TRACE(0, ii, 1);
-                if (P.I_rows || P.stg_tall) {
+                if (P.dbg & 64) {
+                } else if (P.I_rows || P.stg_tall) {
                     const uint32_t tab = smem_u32(smem_raw) + P.tab_off;
                     if (P.stg_tall) build_table_tall(P, it, tab, tid);
                     else build_table(P, it, tab, tid);
@@ -575,6 +590,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 const uint64_t a_desc0 = smem_desc(a_stage, P.a_lbo, 128);
                 const uint64_t b_desc0 = smem_desc(b_base, b_lbo, 128);
                 const int ksteps = P.CC / 4;
+                // warp-converged tap loop; one elected lane issues the tap's
+                // (k-step x tile) MMAs
                 // warp-converged tap loop; one elected lane issues the tap's
                 // (k-step x tile) MMAs
                 if (!(P.dbg & 2))

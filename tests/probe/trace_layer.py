@@ -1,0 +1,20 @@
+"""One traced call of a conv pass (CAPSCONV_TRACE=1 prints CTA 0's per-item timestamps).
+   python tests/probe/trace_layer.py OP B,H,W,C,Cout,KH,KW,s"""
+import os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import torch
+import capsinputs
+import paper_2104_02621_b200.capsconv as cc
+cc.load_library()
+op = sys.argv[1]
+B, H, W, C, Co, KH, KW, s = map(int, sys.argv[2].split(","))
+L = capsinputs.Layer(B, H, W, C, Co, KH, KW, 4, 4, 4, s)
+I = capsinputs.make_input(L, dtype=torch.bfloat16).cuda()
+K = capsinputs.make_kernel(L, dtype=torch.bfloat16).cuda()
+Ho, Wo = cc.output_dims(H, W, KH, KW, s)
+dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), dtype=torch.bfloat16).cuda()
+fn = {"fwd": lambda: cc.fwd(I, K, s), "dI": lambda: cc.bwd_data(dO, K, s, H, W)}[op]
+fn(); torch.cuda.synchronize()
+print("---- traced call", file=sys.stderr)
+fn(); torch.cuda.synchronize()
