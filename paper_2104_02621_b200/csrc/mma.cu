@@ -370,6 +370,55 @@ __device__ __forceinline__ void epi_store16(const ConvMma &P, const Item &it, co
     }
 }
 
+// MMA warp: the taps of one staged chunk.  Descriptors of a tap are computed
+// by the whole (converged) warp; one elected lane then issues the tap's
+// KS k-steps x NTL tiles.  KS = NTL = 0: runtime counts (ks, ntl).
+struct TapIssue {
+    uint64_t a_desc0, b_desc0;
+    uint32_t a_lbo16, b_lbo16, n_tile, idesc, d_base;
+    int offmin, T0;
+    bool first_chunk;
+};
+template <int KS, int NTL>
+__device__ __forceinline__ void mma_taps(const ConvMma &P, const Item &it, const TapIssue &ti, int ks = KS,
+                                         int ntl = NTL) {
+    for (int gg = 0; gg < P.gpi; ++gg) {
+        const int g = it.g + gg;
+        const uint32_t d0 = ti.d_base + (uint32_t)(gg * P.G * P.N_tile);
+        for (int t = P.og_t0[g]; t < P.og_t1[g]; ++t) {
+            const uint64_t a_tap = ti.a_desc0 + ((P.tap_plane[t] * P.plane_bytes +
+                                                  (uint32_t)(P.tap_shift[t] - ti.offmin) * 64u) >> 4);
+            const uint64_t b_tap = ti.b_desc0 + (uint64_t)((t - ti.T0) * (P.CC / 2)) * ti.b_lbo16;
+            const bool first_tap = (ti.first_chunk && t == P.og_t0[g]);
+            if (elect_one()) {
+                if constexpr (KS > 0) {
+#pragma unroll
+                    for (int j = 0; j < KS; ++j)
+#pragma unroll
+                        for (int gi = 0; gi < NTL; ++gi)
+                            mma_bf16_ss(d0 + (uint32_t)gi * ti.n_tile,
+                                        a_tap + 2u * j * ti.a_lbo16 + (uint32_t)gi * ((kTilePix * 64) >> 4),
+                                        b_tap + 2u * j * ti.b_lbo16, ti.idesc, (first_tap && j == 0) ? 0u : 1u);
+                } else {
+                    for (int j = 0; j < ks; ++j) {
+                        const uint64_t bd = b_tap + 2u * j * ti.b_lbo16;
+                        const uint64_t aj = a_tap + 2u * j * ti.a_lbo16;
+                        const uint32_t acc = (first_tap && j == 0) ? 0u : 1u;
+                        uint32_t d = d0;
+                        uint64_t ad = aj;
+                        for (int gi = 0; gi < ntl; ++gi) {
+                            mma_bf16_ss(d, ad, bd, ti.idesc, acc);
+                            d += ti.n_tile;
+                            ad += (kTilePix * 64) >> 4;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_constant__ ConvMma P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
@@ -591,34 +640,20 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 const uint64_t b_desc0 = smem_desc(b_base, b_lbo, 128);
                 const int ksteps = P.CC / 4;
                 // warp-converged tap loop; one elected lane issues the tap's
-                // (k-step x tile) MMAs
-                // warp-converged tap loop; one elected lane issues the tap's
-                // (k-step x tile) MMAs
-                if (!(P.dbg & 2))
-                for (int gg = 0; gg < P.gpi; ++gg) {
-                    const int g = it.g + gg;
-                    const uint32_t d0 = tmem + (uint32_t)((abuf * P.gpi + gg) * P.G * P.N_tile);
-                    for (int t = P.og_t0[g]; t < P.og_t1[g]; ++t) {
-                        const uint64_t a_tap = a_desc0 + ((P.tap_plane[t] * P.plane_bytes +
-                                                           (uint32_t)(P.tap_shift[t] - offmin) * 64u) >> 4);
-                        const uint64_t b_tap = b_desc0 + (((t - T0) * (P.CC / 2) * b_lbo) >> 4);
-                        const bool first_tap = (ch == it.c_begin && t == P.og_t0[g]);
-                        if (elect_one()) {
-                            for (int j = 0; j < ksteps; ++j) {
-                                const uint64_t bd = b_tap + ((2u * j * b_lbo) >> 4);
-                                const uint64_t aj = a_tap + ((2u * j * P.a_lbo) >> 4);
-                                const uint32_t acc = (first_tap && j == 0) ? 0u : 1u;
-                                uint32_t d = d0;
-                                uint64_t ad = aj;
-                                for (int gi = 0; gi < it.ntl; ++gi) {
-                                    mma_bf16_ss(d, ad, bd, idesc, acc);
-                                    d += (uint32_t)P.N_tile;
-                                    ad += (kTilePix * 64) >> 4;
-                                }
-                            }
-                        }
-                        __syncwarp();
-                    }
+                // (k-step x tile) MMAs, fully unrolled for the common shapes
+                if (!(P.dbg & 2)) {
+                    const TapIssue ti{a_desc0, b_desc0, P.a_lbo >> 4, b_lbo >> 4, (uint32_t)P.N_tile, idesc,
+                                      tmem + (uint32_t)(abuf * P.gpi * P.G * P.N_tile), offmin, T0,
+                                      ch == it.c_begin};
+                    const int ntl = it.ntl;
+                    if (ksteps == 1 && ntl == 8) mma_taps<1, 8>(P, it, ti);
+                    else if (ksteps == 1 && ntl == 2) mma_taps<1, 2>(P, it, ti);
+                    else if (ksteps == 2 && ntl == 1) mma_taps<2, 1>(P, it, ti);
+                    else if (ksteps == 2 && ntl == 2) mma_taps<2, 2>(P, it, ti);
+                    else if (ksteps == 2 && ntl == 4) mma_taps<2, 4>(P, it, ti);
+                    else if (ksteps == 2 && ntl == 8) mma_taps<2, 8>(P, it, ti);
+                    else if (ksteps == 4 && ntl == 2) mma_taps<4, 2>(P, it, ti);
+                    else mma_taps<0, 0>(P, it, ti, ksteps, ntl);
                 }
                 if (elect_one()) mma_commit(a_empty + stage);
 
