@@ -23,6 +23,11 @@ static thread_local std::string t_last_error;
 
 void note_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+    static const bool on = getenv("CAPSCONV_NO_PDL") == nullptr;
+    return on;
+}
+
 static capsconv_status_t fail(capsconv_status_t st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 static capsconv_status_t fail(capsconv_status_t st, const char *fmt, ...) {
     char buf[512];

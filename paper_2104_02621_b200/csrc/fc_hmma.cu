@@ -92,6 +92,8 @@ FcPlan fc_plan(const Problem &p) {
 // K[c][c'][d2][d3]; columns past 4*Cout are zero.
 __global__ void __launch_bounds__(256) fc_pack(const __nv_bfloat16 *__restrict__ K, uint32_t *__restrict__ wp,
                                                int ksteps, int NT, int Cout) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)ksteps * NT * 32;
     if (idx >= total) return;
@@ -149,6 +151,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat
                                                                 const uint32_t *__restrict__ wp,
                                                                 float *__restrict__ part, int B, int C, int kslice,
                                                                 int ksteps) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(128) uint8_t fw_smem[];
     uint8_t *ring = fw_smem;
     uint32_t *wsm = reinterpret_cast<uint32_t *>(fw_smem + kFwdStages * kFwdStageBytes);
@@ -247,6 +251,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat
 // O[b][c'][d1][d3] = sum over splits (fixed order) of part[ks][(b, d1)][(c', d3)], rounded to bf16
 __global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ part, __nv_bfloat16 *__restrict__ O,
                                                    int B, int Cout, int ncol, int ksplit) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (row, c')
     const int64_t rows = (int64_t)B * 4;
     if (idx >= rows * Cout) return;
@@ -280,6 +286,8 @@ __global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ par
 // K[c][c'][d2][d3]; c' >= Cout is zero.
 __global__ void __launch_bounds__(256) fc_pack_dgrad(const __nv_bfloat16 *__restrict__ K, uint32_t *__restrict__ wp,
                                                      int ksteps, int NT, int Cout) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)ksteps * NT * 32;
     if (idx >= total) return;
@@ -313,6 +321,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dgrad_kernel(const __nv_bflo
                                                                   const uint32_t *__restrict__ wp,
                                                                   __nv_bfloat16 *__restrict__ dI, int B, int C,
                                                                   int Cout, int ksteps, int NTall, int ntper) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(16) uint32_t wsm[];
     const int nb = blockIdx.x, mb = blockIdx.y;
     const int nt0 = nb * ntper, nt1 = min(NTall, nt0 + ntper);
@@ -426,6 +436,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
                                                                const __nv_bfloat16 *__restrict__ dO,
                                                                float *__restrict__ part, int B, int C, int Cout,
                                                                int bslice, int dbg) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(128) uint8_t dk_smem[];
     uint8_t *ring = dk_smem;   // kDkStages x (4 I rows, then 4 dO rows)
     uint2 *bfr = reinterpret_cast<uint2 *>(dk_smem + kDkStages * kDkStageBytes);   // [2][kDkKs][NT][32] B fragments
@@ -545,6 +557,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
 
 __global__ void __launch_bounds__(256) fc_dk_finalize(const float *__restrict__ part, float *__restrict__ dK,
                                                       int64_t n, int ksplit) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // float4 index, n % 4 == 0
     if (i >= n / 4) return;
     const float4 *p4 = reinterpret_cast<const float4 *>(part);
@@ -576,7 +590,7 @@ cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O,
     uint32_t *wp = static_cast<uint32_t *>(ws);
     float *part = reinterpret_cast<float *>(static_cast<uint8_t *>(ws) + f.wpack_bytes);
     const int64_t npk = (int64_t)f.ksteps * f.NT * 32;
-    fc_pack<<<(unsigned)((npk + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps, f.NT,
+    launch_k(fc_pack, dim3((unsigned)((npk + 255) / 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps, f.NT,
                                                             f.Cout);
     note_launches(1);
     const dim3 grid((unsigned)f.ksplit, (unsigned)f.mblocks);
@@ -587,7 +601,7 @@ cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O,
     case nt:                                                                                                      \
         e = cudaFuncSetAttribute(fc_fwd_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);    \
         if (e != cudaSuccess) return e;                                                                           \
-        fc_fwd_kernel<nt><<<grid, kFcWarps * 32, f.smem, st>>>(Ib, wp, part, f.B, f.C, f.kslice, f.ksteps);        \
+        launch_k(fc_fwd_kernel<nt>, dim3(grid), dim3(kFcWarps * 32), f.smem, st, Ib, wp, part, f.B, f.C, f.kslice, f.ksteps);        \
         break;
         FC_CASE(1) FC_CASE(2) FC_CASE(3) FC_CASE(4) FC_CASE(5) FC_CASE(6) FC_CASE(7) FC_CASE(8)
 #undef FC_CASE
@@ -595,7 +609,7 @@ cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O,
     }
     note_launches(1);
     const int64_t nfin = (int64_t)f.B * 4 * f.Cout;
-    fc_finalize<<<(unsigned)((nfin + 255) / 256), 256, 0, st>>>(part, static_cast<__nv_bfloat16 *>(O), f.B, f.Cout,
+    launch_k(fc_finalize, dim3((unsigned)((nfin + 255) / 256)), dim3(256), 0, st, part, static_cast<__nv_bfloat16 *>(O), f.B, f.Cout,
                                                                 f.NT * 8, f.ksplit);
     note_launches(1);
     return cudaGetLastError();
@@ -648,12 +662,12 @@ cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void 
     if (!f.ok || ws_bytes < f.wpack_bytes) return cudaErrorInvalidValue;
     uint32_t *wp = static_cast<uint32_t *>(ws);
     const int64_t npk = (int64_t)f.ksteps * f.NTall * 32;
-    fc_pack_dgrad<<<(unsigned)((npk + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps,
+    launch_k(fc_pack_dgrad, dim3((unsigned)((npk + 255) / 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps,
                                                                   f.NTall, f.Cout);
     note_launches(1);
     cudaError_t e = cudaFuncSetAttribute(fc_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
     if (e != cudaSuccess) return e;
-    fc_dgrad_kernel<<<dim3((unsigned)f.nblocks, (unsigned)f.mblocks), kFcWarps * 32, f.smem, st>>>(
+    launch_k(fc_dgrad_kernel, dim3(dim3((unsigned)f.nblocks, (unsigned)f.mblocks)), dim3(kFcWarps * 32), f.smem, st, 
         static_cast<const __nv_bfloat16 *>(dO), wp, static_cast<__nv_bfloat16 *>(dI), f.B, f.C, f.Cout, f.ksteps,
         f.NTall, f.ntper);
     note_launches(1);
@@ -714,7 +728,7 @@ cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *d
     case nt:                                                                                                \
         e = cudaFuncSetAttribute(fc_dk_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
         if (e != cudaSuccess) return e;                                                                         \
-        fc_dk_kernel<nt><<<grid, kFcWarps * 32, smem, st>>>(Ib, Ob, part, f.B, f.C, f.Cout, f.bslice, dbg);       \
+        launch_k(fc_dk_kernel<nt>, dim3(grid), dim3(kFcWarps * 32), smem, st, Ib, Ob, part, f.B, f.C, f.Cout, f.bslice, dbg);       \
         break;
         DK_CASE(1) DK_CASE(2) DK_CASE(3) DK_CASE(4) DK_CASE(5) DK_CASE(6) DK_CASE(7) DK_CASE(8)
 #undef DK_CASE
@@ -722,7 +736,7 @@ cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *d
     }
     note_launches(1);
     const int64_t n = (int64_t)f.C * f.Cout * 16;
-    fc_dk_finalize<<<(unsigned)((n / 4 + 255) / 256), 256, 0, st>>>(part, dK, n, f.ksplit);
+    launch_k(fc_dk_finalize, dim3((unsigned)((n / 4 + 255) / 256)), dim3(256), 0, st, part, dK, n, f.ksplit);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -36,6 +36,34 @@ const DeviceInfo &device_info();
 // Counts kernels enqueued by the library (capsconv_launch_count()).
 void note_launches(int n);
 
+// Programmatic dependent launch (PDL) for the kernels of the hot path: the
+// launch may begin while the previous kernel in the stream is still running;
+// every kernel launched this way calls pdl_launch_dependents() on entry and
+// pdl_wait() before its first global-memory access, which blocks until the
+// previous grid has completed and its writes are visible -- stream order is
+// unchanged, only launch latency and CTA placement overlap the predecessor's
+// tail.  Disabled with CAPSCONV_NO_PDL (A/B measurements).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+#endif
+
 // ---------------------------------------------------------------- SIMT path
 size_t simt_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, cudaStream_t st);

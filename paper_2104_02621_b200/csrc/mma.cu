@@ -420,6 +420,8 @@ __device__ __forceinline__ void mma_taps(const ConvMma &P, const Item &it, const
 }
 
 __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_constant__ ConvMma P) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *a_full = bars;
@@ -691,6 +693,8 @@ struct PackArgs {
 };
 
 __global__ void __launch_bounds__(256) pack_weights_kernel(const __grid_constant__ PackArgs A) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     const int kcpc = A.CC / 2;
     const long long total = (long long)A.n_ntiles * A.nchunks * A.ntaps * kcpc * A.N_tile;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -726,6 +730,8 @@ __global__ void __launch_bounds__(256) pack_weights_kernel(const __grid_constant
 
 // ------------------------------------------------------------------ split-K finalize
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ ConvMma P) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     // one thread per (virtual row R = u*4 + d1, output channel)
     const long long rows = (long long)P.Bn * P.Hg * P.Wg * 4;
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1033,7 +1039,7 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
     pl.pack.K = static_cast<const __nv_bfloat16 *>(K);
     pl.pack.dst = w;
     const long long npack = (long long)pl.wpack_bytes / 16;
-    pack_weights_kernel<<<(unsigned)((npack + 255) / 256), 256, 0, st>>>(pl.pack);
+    launch_k(pack_weights_kernel, dim3((unsigned)((npack + 255) / 256)), dim3(256), 0, st, pl.pack);
     note_launches(1);
     static bool attr_set = false;  // per process; the attribute is per function
     if (!attr_set) {
@@ -1047,7 +1053,7 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
         cudaMalloc(&P.trace, 3 * 64 * 4 * sizeof(unsigned long long));
         cudaMemset(P.trace, 0, 3 * 64 * 4 * sizeof(unsigned long long));
     }
-    conv_mma_kernel<<<grid, kConvThreads, P.smem_bytes, st>>>(P);
+    launch_k(conv_mma_kernel, dim3(grid), dim3(kConvThreads), P.smem_bytes, st, P);
     note_launches(1);
     if (tracing) {
         std::vector<unsigned long long> h(3 * 64 * 4);
@@ -1069,7 +1075,7 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
     }
     if (P.ksplit > 1) {
         const long long n = (long long)P.Bn * P.Hg * P.Wg * 4 * P.NCH;
-        finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P);
+        launch_k(finalize_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, P);
         note_launches(1);
     }
     return cudaGetLastError();

@@ -594,6 +594,8 @@ __device__ __forceinline__ void w_load_A(const WgradMma &P, const WLane &L, int 
 }
 
 __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_constant__ WgradMma P) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *stg_full = bars, *stg_empty = bars + 4;
@@ -930,6 +932,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
 // then added in slice order (a fixed summation tree for every launch).
 __global__ void __launch_bounds__(256) w_finalize(const float *__restrict__ part, float *__restrict__ dK, int64_t n,
                                                   int ksplit, int nsl) {
+    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    pdl_wait();                // the previous grid has completed and its writes are visible
     __shared__ float red[256];
     const int E = 256 / nsl;
     const int el = threadIdx.x % E, sl = threadIdx.x / E;
@@ -1288,7 +1292,7 @@ cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK
         cudaMalloc(&P.trace, 3 * 64 * 4 * 8);
         cudaMemset(P.trace, 0, 3 * 64 * 4 * 8);
     }
-    wgrad_kernel<<<grid, kWThreads, P.smem_bytes, st>>>(P);
+    launch_k(wgrad_kernel, dim3(grid), dim3(kWThreads), P.smem_bytes, st, P);
     note_launches(1);
     if (tracing) {
         std::vector<unsigned long long> h(3 * 64 * 4);
@@ -1312,7 +1316,7 @@ cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK
         const int64_t n = (int64_t)P.ntaps * P.C * P.Cout * 16;
         const int nsl = P.ksplit >= 64 ? 8 : P.ksplit >= 32 ? 4 : P.ksplit >= 16 ? 2 : 1;
         const int64_t E = 256 / nsl;
-        w_finalize<<<(unsigned)((n + E - 1) / E), 256, 0, st>>>(P.part, dK, n, P.ksplit, nsl);
+        launch_k(w_finalize, dim3((unsigned)((n + E - 1) / E)), dim3(256), 0, st, P.part, dK, n, P.ksplit, nsl);
         note_launches(1);
     }
     return cudaGetLastError();
