@@ -5,9 +5,15 @@ import collections, csv, json, os, re, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 PROF = os.path.join(ROOT, "profiles")
-CAPS = [("L1_dK", "r1_wgrad_L1_dK.ncu-rep", "wgrad_kernel, nq=3 column shifts as B descriptor offsets, KP=64, 3 loader groups"),
-        ("L3_dK", "r1_wgrad_L3_dK.ncu-rep", "wgrad_kernel (capture predates descriptor-shift mode: nq=1)"),
-        ("L1_fwd", "r1_conv_L1_fwd.ncu-rep", "conv_mma_kernel fwd, G=8 CC=4, row-box staging")]
+# (name, report, launch row in the report, description)
+CAPS = [("L1_dK", "r1b_fc_and_L1dK.ncu-rep", 3,
+         "wgrad_kernel, nq=3 column shifts as B descriptor offsets, KP=64, 3 loader groups (PDL build)"),
+        ("FC_fwd", "r1b_fc_and_L1dK.ncu-rep", 0, "fc_fwd_kernel<5>: mma.sync m16n8k16, cp.async I ring, split-K 18"),
+        ("FC_dI", "r1b_fc_and_L1dK.ncu-rep", 1, "fc_dgrad_kernel: mma.sync, one wave of 3 CTAs/SM"),
+        ("FC_dK", "r1b_fc_and_L1dK.ncu-rep", 2, "fc_dk_kernel<5>: mma.sync, bulk-copy image ring, split-K 9"),
+        ("L1_dK_prev", "r1_wgrad_L1_dK.ncu-rep", 0, "wgrad_kernel, earlier r1 build (before PDL)"),
+        ("L3_dK", "r1_wgrad_L3_dK.ncu-rep", 0, "wgrad_kernel (capture predates descriptor-shift mode: nq=1)"),
+        ("L1_fwd", "r1_conv_L1_fwd.ncu-rep", 0, "conv_mma_kernel fwd, G=8 CC=4, row-box staging")]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -25,16 +31,16 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 def full_summaries():
     out = ["# Round 1 ncu --set full captures (one launch each, --clock-control none, bf16, 1 B200)",
-           "# command: python tests/probe/run_layer.py <op> <layer> 1 under ncu -k regex:<kernel> -s 2 -c 1",
-           "# (single launch, L2 warm from the warm-up launches; shares/stalls matter, not the absolute time)", ""]
+           "# commands: tests/probe/run_layer.py / capture_ops.py under ncu --set full -k regex:<kernels>",
+           "# (cache control on: cold L2; shares/stalls matter, not the absolute time)", ""]
     traffic = {}
-    for name, f, desc in CAPS:
+    for name, f, row, desc in CAPS:
         path = os.path.join(PROF, f)
         if not os.path.exists(path):
             continue
         raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         r = list(csv.reader(raw.splitlines()))
-        h, u, v = r[0], r[1], r[2]
+        h, u, v = r[0], r[1], r[2 + row]
         out.append("[%s]  (profiles/%s)  %s" % (name, f, desc))
         d = {}
         for k in KEYS:
