@@ -239,3 +239,55 @@ def test_stack_step_small_batch(cc, oracle_mod):
     assert_close(to_np(st.grads[0]), dX, den["dI"][0], torch.bfloat16, "stack dX")
     for li in range(len(specs)):
         assert_close(to_np(dKs[li]), rdKs[li], den["dK"][li], torch.bfloat16, "stack dK L%d" % (li + 1))
+
+
+def test_stack_step_graph_matches_serialised(cc):
+    """The config-5 stack step as bench.py times it -- captured once in a CUDA
+    graph (kernels chained by programmatic-dependent-launch edges, no host
+    synchronisation) and replayed -- against the same chain run op by op with
+    a device synchronisation after every call, global batch 1024.  Every
+    kernel is deterministic, so any ordering hazard between consecutive
+    kernels shows up as a bitwise difference."""
+    from paper_2104_02621_b200.stack import CapsStack, LayerSpec
+    specs = [LayerSpec(*l) for l in capsinputs.STACK_LAYERS]
+    si = capsinputs.STACK_INPUT
+    B = capsinputs.STACK_BATCH
+    layers = capsinputs.stack_layers(B, cc.output_dims)
+    Ks = [capsinputs.make_kernel(L, dtype=torch.bfloat16, layer_idx=i).to(DEV) for i, L in enumerate(layers)]
+    X = capsinputs.make_input(layers[0], dtype=torch.bfloat16).to(DEV)
+    hw = [(si["H"], si["W"])]
+    for s in specs:
+        hw.append(cc.output_dims(hw[-1][0], hw[-1][1], s.KH, s.KW, s.stride))
+    dY = capsinputs.make_grad_output((B, hw[-1][0], hw[-1][1], specs[-1].Cout, 4, 4), dtype=torch.bfloat16,
+                                     layer_idx=len(specs)).to(DEV)
+    # serialised reference
+    acts = [X]
+    for li, s in enumerate(specs):
+        acts.append(cc.fwd(acts[-1], Ks[li], s.stride))
+        torch.cuda.synchronize()
+    g, rdK = dY, [None] * len(specs)
+    for li in range(len(specs) - 1, -1, -1):
+        s = specs[li]
+        rdK[li] = cc.bwd_kernel(acts[li], g, s.stride, s.KH, s.KW)
+        torch.cuda.synchronize()
+        g = cc.bwd_data(g, Ks[li], s.stride, hw[li][0], hw[li][1])
+        torch.cuda.synchronize()
+    # graph-captured product step
+    st = CapsStack(specs, si["H"], si["W"], 4, B, Ks, DEV)
+    graph, cs = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        st.step(X, dY)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=cs):
+            st.step(X, dY)
+    torch.cuda.synchronize()
+    for t in [st.out] + st.grads + st.dK:
+        t.fill_(float("nan"))
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(st.out, acts[-1])
+    assert torch.equal(st.grads[0], g)
+    for li in range(len(specs)):
+        assert torch.equal(st.dK[li], rdK[li]), li
