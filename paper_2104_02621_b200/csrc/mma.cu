@@ -91,13 +91,15 @@ __device__ __forceinline__ void conv_in_rows(const ConvMma &P, int v0, int &rA, 
 // Tall-box staging: the window's source rows, image by image.  Segment of
 // image b = rows [yfirst, yhi] (yfirst pulled up so the last box never runs
 // past yhi; a segment occupies max(rows, h_box) staged rows), staged at row
-// offset rowbase.  Every thread walks the same (<= 4) segments.
+// offset rowbase.  Slot i is image ba + i (the planner bounds the window to
+// <= 4 images); slots are statically indexed so the segments stay in registers.
 struct TallSegs {
-    int n;
+    bool ok[4];
     int b[4], yfirst[4], yhi[4], rowbase[4];
 };
 __device__ __forceinline__ void tall_segments(const ConvMma &P, int v0, TallSegs &S) {
-    S.n = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { S.ok[i] = false; S.b[i] = S.yfirst[i] = S.yhi[i] = S.rowbase[i] = 0; }
     const int vtot = P.Bn * P.Hg * P.Wg;
     const int vlo = max(v0, 0), vhi = min(v0 + P.win_px, vtot) - 1;
     if (vhi < vlo) return;
@@ -106,13 +108,14 @@ __device__ __forceinline__ void tall_segments(const ConvMma &P, int v0, TallSegs
     const int ya = (int)P.fd_Wg.div((uint32_t)vlo - (uint32_t)ba * HgWg);
     const int yb = (int)P.fd_Wg.div((uint32_t)vhi - (uint32_t)bb * HgWg);
     int rowbase = 0;
-    for (int b = ba; b <= bb && S.n < 4; ++b) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int b = ba + i;
         const int ylo = b == ba ? ya : 0;
         const int yhi = min(b == bb ? yb : P.Hg - 1, P.src_H - 1);
-        if (yhi < ylo) continue;   // only zero-padding rows of this image
+        if (b > bb || yhi < ylo) continue;   // past the window, or only zero-padding rows of this image
         const int yfirst = max(0, min(ylo, yhi - P.h_box + 1));
-        S.b[S.n] = b; S.yfirst[S.n] = yfirst; S.yhi[S.n] = yhi; S.rowbase[S.n] = rowbase;
-        ++S.n;
+        S.ok[i] = true; S.b[i] = b; S.yfirst[i] = yfirst; S.yhi[i] = yhi; S.rowbase[i] = rowbase;
         rowbase += max(yhi - yfirst + 1, P.h_box);
     }
 }
@@ -126,7 +129,9 @@ __device__ __forceinline__ uint32_t tall_issue(const ConvMma &P, int v0, int ch,
     const uint32_t box_bytes = (uint32_t)P.h_box * P.src_W * px_bytes;
     const int c0 = ch * P.CC * 16;
     uint32_t bytes = 0;
-    for (int k = 0; k < S.n; ++k) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!S.ok[k]) continue;
         const int nb = tall_nbox(P, S, k);
         for (int j = 0; j < nb; ++j) {
             const int ys = j == nb - 1 ? max(S.yfirst[k], S.yhi[k] - P.h_box + 1) : S.yfirst[k] + j * P.h_box;
@@ -156,7 +161,7 @@ __device__ __forceinline__ void build_table_tall(const ConvMma &P, const Item &i
             if (Y < P.src_H && X < P.src_W) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (k < S.n && S.b[k] == (int)b) idx = (S.rowbase[k] + Y - S.yfirst[k]) * P.src_W + X;
+                    if (S.ok[k] && S.b[k] == (int)b) idx = (S.rowbase[k] + Y - S.yfirst[k]) * P.src_W + X;
             }
         }
         asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(tab + (uint32_t)e * 4u), "r"(idx) : "memory");
