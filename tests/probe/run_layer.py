@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import torch
 import capsinputs
 import paper_2104_02621_b200.capsconv as cc
-cc.load_library()
+cc.load_library(os.environ.get("CAPSCONV_LIB"))   # A/B: an alternative build
 op = sys.argv[1]
 B, H, W, C, Co, KH, KW, s = map(int, sys.argv[2].split(","))
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 5
