@@ -98,7 +98,7 @@ struct WgradMma {
     int nstg, nstages;
     uint32_t smem_bytes, tmem_cols;
     unsigned long long *trace;             // debug: globaltimer stamps of CTA 0 [role][stage][4]
-    int dbg;                               // bench-only (wrong results): 1 skip transpose, 4 skip B, 16 skip A
+    int dbg;                               // bench-only (wrong results): 1 skip transpose, 2 skip MMAs, 4 skip B, 16 skip A
     // contiguous staging (1-D bulk copies): dO always; I when stride 1 (not FC)
     const uint8_t *I_ptr, *O_ptr;
     int I_contig;
@@ -845,7 +845,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 const uint32_t a0 = tmem + P.acc_cols + (uint32_t)st * P.abuf_cols;
                 // the warp stays converged; one elected lane issues 4 k-steps at
                 // a time (a long divergent single-lane loop issues far slower)
-                if (P.bdesc) {
+                if (P.dbg & 2) {
+                } else if (P.bdesc) {
                     // accumulator block bi = shift j = nq-1-bi reads F_0 from
                     // pixel bi (descriptor offset); one MMA covers bmat adjacent
                     // blocks through the materialised copies.  Block-major order:
