@@ -291,3 +291,33 @@ def test_stack_step_graph_matches_serialised(cc):
     assert torch.equal(st.grads[0], g)
     for li in range(len(specs)):
         assert torch.equal(st.dK[li], rdK[li]), li
+
+
+FC_RAGGED = [
+    # B, H=W=KH=KW, C, Cout: full-extent (FC) layers on the mma.sync kernels --
+    # ragged batch (split-K / image-slice tails, partial stages), flattened
+    # channel counts that are not multiples of 4 or 64, odd and small Cout
+    (37, 3, 5, 3),
+    (130, 2, 12, 16),
+    (1, 1, 7, 1),
+    (257, 4, 9, 10),
+    (64, 8, 32, 10),
+]
+
+
+@pytest.mark.parametrize("case", FC_RAGGED, ids=lambda c: "x".join(map(str, c)))
+def test_fc_ragged_exact(cc, oracle_mod, case):
+    """Full-extent capsule layers with ragged extents, exact-integer bf16
+    inputs: bitwise equal to the oracle on the library's own path."""
+    B, S, C, Co = case
+    L = capsinputs.Layer(B, S, S, C, Co, S, S, 4, 4, 4, 1)
+    I = capsinputs.make_input(L, "int1", torch.bfloat16)
+    K = capsinputs.make_kernel(L, "int1", torch.bfloat16)
+    dO = capsinputs.make_grad_output(L.o_shape(1, 1), "int1", torch.bfloat16)
+    O, dI, dK = run_all(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), 1)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), 1, S, S)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), 1, S, S)
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
