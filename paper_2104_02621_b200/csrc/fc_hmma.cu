@@ -1,23 +1,28 @@
 // fc_hmma.cu -- the fully-connected capsule layer (R18: a full-extent
 // capsule convolution viewed as 1x1 over C = KH*KW*Cin channels) on warp-level
-// mma.sync tensor-core instructions, reading the natural capsule layout
-// directly into register fragments.
+// mma.sync tensor-core instructions: forward, dI and dK.
 //
 // Why not tcgen05 here: the FC passes are streaming GEMMs (forward: M = B*4,
 // K = 4*C = 8192, N = 4*Cout = 40; 40 flop/byte, HBM-bound at ~260 TFLOP/s,
 // well inside the ~550 TFLOP/s legacy HMMA sustains on B200, tests/probe/
-// hmma_probe.cu).  The m16n8k16 A fragment's k-pairs are (d2, d2+1) of one
-// capsule row -- 4 contiguous bytes of I[b][c][d1][d2] -- so the operand
-// needs no shared-memory staging or D1 repack at all, which is what bounds the
-// tcgen05 path on this layer (producer repack and split-K bookkeeping).
+// hmma_probe.cu).  With the k index inside each 16-step permuted, a thread's
+// whole m16n8k16 A fragment is 16 contiguous bytes of the capsule layout, so
+// the operand needs no D1 repack, which is what bounds the tcgen05 path on
+// this layer (producer repack and split-K bookkeeping).
 //
-//   O[b, c', d1, d3] = sum_{c, d2} I[b, c, d1, d2] * K[c, c', d2, d3]
-//   rows m = (b, d1), k = (c, d2), columns n = (c', d3)        (R18)
+//   O[b, c', d1, d3]  = sum_{c, d2}   I[b, c, d1, d2] * K[c, c', d2, d3]     rows (b, d1),  k (c, d2)
+//   dI[b, c, d1, d2]  = sum_{c', d3}  dO[b, c', d1, d3] * K[c, c', d2, d3]   rows (b, d1),  k (c', d3)
+//   dK[c, c', d2, d3] = sum_{b, d1}   I[b, c, d1, d2] * dO[b, c', d1, d3]    rows (c, d2),  k (b, d1)
+//                                                            (Alg. 4, R18)
 //
-// Work: CTA = (K split ks, block of 8 warps x 2 m-tiles); each warp keeps
-// 2 x ceil(N/8) accumulator fragments over its K range; the K slice of the
-// weights (prepacked in fragment order) sits in shared memory.  Split
-// partials are summed in a fixed order by fc_finalize (deterministic).
+// fwd: CTA = (K split, 64 images); the CTA's I rows stream through a 4-stage
+// cp.async ring, the K slice of the weights (prepacked in fragment order)
+// sits in shared memory.  dI: CTA = (column block, 64 images), dO fragments
+// in registers, weights of the column block in shared memory.  dK: CTA =
+// (image slice, 64 channels), I and dO rows of 8 images per stage by 1-D bulk
+// copies on an mbarrier ring, capsule-column fragments built with PRMT.
+// Split partials are summed in a fixed order by the finalize kernels
+// (deterministic).  DESIGN.md 5.3c has the measurements.
 #include <cuda_bf16.h>
 
 #include <algorithm>
