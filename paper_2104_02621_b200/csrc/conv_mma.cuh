@@ -102,6 +102,7 @@ struct ConvMma {
     int n_igroups;             // ceil(n_mtiles / G)
     int n_items;
     FastDiv fd_units;          // 8-byte pieces per pixel in a chunk = 4*CC
+    FastDiv fd_ksplit, fd_nnt, fd_nig;   // item decode: ksplit, n_ntiles, n_igroups
     // ---- shared memory plan
     int win_px;                // window pixels (max over groups, even)
     uint32_t a_lbo;            // win_px*4*16 + 16 (bank stagger)

@@ -40,16 +40,17 @@ struct Item {
 };
 
 __device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
+    // every role decodes every item: host-computed reciprocals, no runtime division
     Item it;
-    int r = item;
-    it.ks = r % P.ksplit; r /= P.ksplit;
-    it.nt = r % P.n_ntiles; r /= P.n_ntiles;
-    it.ig = r % P.n_igroups;
-    it.g = (r / P.n_igroups) * P.gpi;   // first output group of the item
+    uint32_t r = (uint32_t)item, q;
+    q = P.fd_ksplit.div(r); it.ks = (int)(r - q * (uint32_t)P.ksplit); r = q;
+    q = P.fd_nnt.div(r);    it.nt = (int)(r - q * (uint32_t)P.n_ntiles); r = q;
+    q = P.fd_nig.div(r);    it.ig = (int)(r - q * (uint32_t)P.n_igroups);
+    it.g = (int)q * P.gpi;   // first output group of the item
     it.tile0 = it.ig * P.G;
     it.ntl = min(P.G, P.n_mtiles - it.tile0);
-    it.c_begin = it.ks * P.nchunks / P.ksplit;
-    it.c_end = (it.ks + 1) * P.nchunks / P.ksplit;
+    it.c_begin = (int)P.fd_ksplit.div((uint32_t)(it.ks * P.nchunks));
+    it.c_end = (int)P.fd_ksplit.div((uint32_t)((it.ks + 1) * P.nchunks));
     return it;
 }
 
@@ -1013,6 +1014,9 @@ Plan make_plan(const Problem &p, bool dgrad) {
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_units.init((uint32_t)(2 * P.CC));
+    P.fd_ksplit.init((uint32_t)P.ksplit);
+    P.fd_nnt.init((uint32_t)P.n_ntiles);
+    P.fd_nig.init((uint32_t)P.n_igroups);
 
     pl.wpack_bytes = align256((size_t)P.n_ntiles * P.nchunks * P.ntaps * (P.CC / 2) * P.N_tile * 16);
     pl.part_bytes = P.ksplit > 1 ? align256((size_t)P.ksplit * P.n_mtiles * 128 * P.n_ntiles * P.N_tile * 4) : 0;
