@@ -54,6 +54,11 @@ __device__ __forceinline__ Item decode_item(const ConvMma &P, int item) {
     return it;
 }
 
+// floor(a / d) for any sign of a, with a host-computed reciprocal of d
+__device__ __forceinline__ int fd_floor(const FastDiv &fd, int a) {
+    return a >= 0 ? (int)fd.div((uint32_t)a) : -(int)fd.div((uint32_t)(-a) + fd.d - 1u);
+}
+
 #define TRACE(role, idx, ev)                                                                      \
     do {                                                                                          \
         if (P.trace && blockIdx.x == 0 && (idx) < 64)                                             \
@@ -69,7 +74,7 @@ __device__ __forceinline__ int window_v0(const ConvMma &P, const Item &it) {
     return it.tile0 * kTilePix + P.ib_offmin[it.g];
 }
 __device__ __forceinline__ int staging_off(const ConvMma &P, int v0) {
-    return P.stg_batch_mode ? 0 : v0 - floor_div(v0, P.Wg) * P.Wg;
+    return P.stg_batch_mode ? 0 : v0 - fd_floor(P.fd_Wg, v0) * P.Wg;
 }
 
 // rows mode: global input rows [rA, rB] covering the window [v0, v0 + win_px)
@@ -200,9 +205,9 @@ __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &
                 bytes += (uint32_t)P.BB * px_bytes;
             }
         } else {
-            const int Ra = floor_div(v0, P.Wg), Rb = floor_div(v0 + len - 1, P.Wg);
+            const int Ra = fd_floor(P.fd_Wg, v0), Rb = fd_floor(P.fd_Wg, v0 + len - 1);
             for (int R = Ra; R <= Rb; ++R) {
-                const int b = floor_div(R, P.Hg);
+                const int b = fd_floor(P.fd_Hg, R);
                 const int Y = R - b * P.Hg;
                 tma::load4d(base + (uint32_t)((R - Ra) * P.Wg) * px_bytes, &P.tmap, c0, P.pl_ox[k] - P.src_pad,
                             P.pl_s * Y + P.pl_oy[k] - P.src_pad, b, mbar);
@@ -226,7 +231,7 @@ __device__ __forceinline__ uint32_t staging_bytes(const ConvMma &P, const Item &
     if (P.stg_batch_mode) {
         per_plane = (uint32_t)((P.win_px + P.BB - 1) / P.BB) * P.BB * px_bytes;
     } else {
-        const int Ra = floor_div(v0, P.Wg), Rb = floor_div(v0 + P.win_px - 1, P.Wg);
+        const int Ra = fd_floor(P.fd_Wg, v0), Rb = fd_floor(P.fd_Wg, v0 + P.win_px - 1);
         per_plane = (uint32_t)((Rb - Ra + 1) * P.Wg) * px_bytes;
     }
     return per_plane * P.npl;
@@ -487,9 +492,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         }
         int stage = 0, sb = 0;
         uint32_t phase = 0, sphase = 0;
-        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+        for (int item = blockIdx.x, ii = 0; item < P.n_items; item += gridDim.x, ++ii) {
             const Item it = decode_item(P, item);
-            const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
             for (int ch = it.c_begin; ch < it.c_end; ++ch) {
                 if (tid == 0) TRACE(0, ii, 0);
                 mbar_wait(a_empty + stage, phase ^ 1);
@@ -532,9 +536,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         const uint32_t HgWg = (uint32_t)(P.Hg * P.Wg);
         int abuf = 0;
         uint32_t aphase = 0;
-        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+        for (int item = blockIdx.x, ii = 0; item < P.n_items; item += gridDim.x, ++ii) {
             const Item it = decode_item(P, item);
-            const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
             if (row == 0) TRACE(2, ii, 0);
             mbar_wait(acc_full + abuf, aphase);
             if (row == 0) TRACE(2, ii, 1);
@@ -625,9 +628,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
         int abuf = 0;
         uint32_t aphase = 0;
         if (P.b_resident) mbar_wait(b_res, 0);
-        for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+        for (int item = blockIdx.x, ii = 0; item < P.n_items; item += gridDim.x, ++ii) {
             const Item it = decode_item(P, item);
-            const int ii = (item - (int)blockIdx.x) / (int)gridDim.x;
             if (lane == 0) TRACE(1, ii, 0);
             mbar_wait(acc_empty + abuf, aphase ^ 1);
             if (lane == 0) TRACE(1, ii, 1);
@@ -1012,6 +1014,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
     while (cols < (uint32_t)(2 * P.gpi * P.G * P.N_tile)) cols <<= 1;
     P.tmem_cols = cols;
     P.fd_Wg.init((uint32_t)P.Wg);
+    P.fd_Hg.init((uint32_t)P.Hg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_units.init((uint32_t)(2 * P.CC));
     P.fd_ksplit.init((uint32_t)P.ksplit);
