@@ -78,7 +78,7 @@ struct ConvMma {
     int src_H, src_W;          // source tensor spatial extents (pitch)
     int src_vH, src_vW;        // valid source region (mapped coordinates)
     int Hg, Wg;                // virtual grid per image
-    FastDiv fd_Wg, fd_HgWg, fd_Hg;
+    FastDiv fd_Wg, fd_HgWg, fd_Hg, fd_hbox;
     int npl, pl_s;             // source planes and their stride
     int pl_oy[4], pl_ox[4];
     // ---- taps (sorted by output group)

@@ -126,7 +126,7 @@ __device__ __forceinline__ void tall_segments(const ConvMma &P, int v0, TallSegs
     }
 }
 __device__ __forceinline__ int tall_nbox(const ConvMma &P, const TallSegs &S, int k) {
-    return max(1, (S.yhi[k] - S.yfirst[k] + P.h_box) / P.h_box);
+    return max(1, (int)P.fd_hbox.div((uint32_t)(S.yhi[k] - S.yfirst[k] + P.h_box)));
 }
 __device__ __forceinline__ uint32_t tall_issue(const ConvMma &P, int v0, int ch, uint32_t stg, uint32_t mbar, bool issue) {
     TallSegs S;
@@ -1015,6 +1015,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
     P.tmem_cols = cols;
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_Hg.init((uint32_t)P.Hg);
+    P.fd_hbox.init((uint32_t)std::max(1, P.h_box));
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_units.init((uint32_t)(2 * P.CC));
     P.fd_ksplit.init((uint32_t)P.ksplit);
