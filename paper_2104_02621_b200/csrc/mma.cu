@@ -218,24 +218,6 @@ __device__ __forceinline__ uint32_t issue_staging(const ConvMma &P, const Item &
     return bytes;
 }
 
-__device__ __forceinline__ uint32_t staging_bytes(const ConvMma &P, const Item &it) {
-    if (P.stg_tall) return tall_issue(P, window_v0(P, it), 0, 0, 0, false);
-    if (P.I_rows) {
-        int rA, rB;
-        conv_in_rows(P, window_v0(P, it), rA, rB);
-        return rB >= rA ? (uint32_t)(rB - rA + 1) * P.Win * P.CS * 32u : 0u;
-    }
-    const int v0 = window_v0(P, it);
-    const uint32_t px_bytes = (uint32_t)P.CC * 32u;
-    uint32_t per_plane;
-    if (P.stg_batch_mode) {
-        per_plane = (uint32_t)((P.win_px + P.BB - 1) / P.BB) * P.BB * px_bytes;
-    } else {
-        const int Ra = fd_floor(P.fd_Wg, v0), Rb = fd_floor(P.fd_Wg, v0 + P.win_px - 1);
-        per_plane = (uint32_t)((Rb - Ra + 1) * P.Wg) * px_bytes;
-    }
-    return per_plane * P.npl;
-}
 
 
 // Producers: repack the staged natural layout [pixel][c][d1][d2] into the
@@ -609,9 +591,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     const uint32_t stg = stg0 + sb * P.stg_bytes;
                     const uint32_t mb = smem_u32(stg_full + sb);
                     if (!(P.dbg & 1)) {
-                        // arm with the exact byte count, then issue the copies
-                        mbar_arrive_expect_tx(stg_full + sb, staging_bytes(P, it));
-                        issue_staging(P, it, ch, stg, mb);
+                        // issue the copies, then arm with their byte count (the transaction
+                        // count may go transiently negative; the phase cannot complete
+                        // before this arrival) -- one walk over the staging plan
+                        const uint32_t bytes = issue_staging(P, it, ch, stg, mb);
+                        mbar_arrive_expect_tx(stg_full + sb, bytes);
                     } else {
                         mbar_arrive(stg_full + sb);
                     }
