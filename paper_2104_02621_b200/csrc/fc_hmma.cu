@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
     __syncthreads();
     // thread 0: stage ss <- images b_lo + kDkImg*ss .. (valid ones only; the rest are masked in the fragments)
     auto issue = [&](int ss) {
-        if (ss >= nst || (dbg & 1)) return;
+        if (ss >= nst || (kProbes && (dbg & 1))) return;
         uint8_t *st = ring + (ss % kDkStages) * kDkStageBytes;
         const int ni = min(kDkImg, nimg - kDkImg * ss);
         mbar_arrive_expect_tx(&full[ss % kDkStages], (uint32_t)ni * (nc + Cout) * 32u);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
         }
     };
     auto wait_stage = [&](int ss) {
-        if (ss < nst && !(dbg & 1)) mbar_wait(&full[ss % kDkStages], (uint32_t)(ss / kDkStages) & 1u);
+        if (ss < nst && !(kProbes && (dbg & 1))) mbar_wait(&full[ss % kDkStages], (uint32_t)(ss / kDkStages) & 1u);
     };
     if (threadIdx.x == 0)
         for (int s0 = 0; s0 < kDkStages - 1; ++s0) issue(s0);
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
         __syncthreads();   // B(ss) extracted; every thread is done with stage ss-1 (and waited for ss, ss+1)
         if (threadIdx.x == 0) issue(ss + kDkStages - 1);
         extract_b(ss + 1);
-        if (dbg & 2) continue;
+        if (kProbes && (dbg & 2)) continue;
 #pragma unroll
         for (int j = 0; j < kDkKs; ++j) {
         const int k = ss * kDkKs + j;
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256) fc_dk_finalize(const float *__restrict__ 
 }  // namespace
 
 bool fc_hmma_fwd_supported(const Problem &p) {
-    static const bool off = getenv("CAPSCONV_NO_FC_HMMA") != nullptr;
+    static const bool off = probe_env("CAPSCONV_NO_FC_HMMA") != nullptr;
     return !off && fc_plan(p).ok;
 }
 
@@ -604,7 +604,7 @@ cudaError_t fc_hmma_fwd(const Problem &p, const void *I, const void *K, void *O,
     switch (f.NT) {
 #define FC_CASE(nt)                                                                                               \
     case nt:                                                                                                      \
-        e = cudaFuncSetAttribute(fc_fwd_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);    \
+        e = smem_optin(reinterpret_cast<const void *>(fc_fwd_kernel<nt>), (int)f.smem);    \
         if (e != cudaSuccess) return e;                                                                           \
         launch_k(fc_fwd_kernel<nt>, dim3(grid), dim3(kFcWarps * 32), f.smem, st, Ib, wp, part, f.B, f.C, f.kslice, f.ksteps);        \
         break;
@@ -652,7 +652,7 @@ FcDgPlan fc_dg_plan(const Problem &p) {
 }  // namespace
 
 bool fc_hmma_dgrad_supported(const Problem &p) {
-    static const bool off = getenv("CAPSCONV_NO_FC_HMMA") != nullptr;
+    static const bool off = probe_env("CAPSCONV_NO_FC_HMMA") != nullptr;
     return !off && fc_dg_plan(p).ok;
 }
 
@@ -670,7 +670,7 @@ cudaError_t fc_hmma_dgrad(const Problem &p, const void *dO, const void *K, void 
     launch_k(fc_pack_dgrad, dim3((unsigned)((npk + 255) / 256)), dim3(256), 0, st, static_cast<const __nv_bfloat16 *>(K), wp, f.ksteps,
                                                                   f.NTall, f.Cout);
     note_launches(1);
-    cudaError_t e = cudaFuncSetAttribute(fc_dgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
+    cudaError_t e = smem_optin(reinterpret_cast<const void *>(fc_dgrad_kernel), (int)f.smem);
     if (e != cudaSuccess) return e;
     launch_k(fc_dgrad_kernel, dim3(dim3((unsigned)f.nblocks, (unsigned)f.mblocks)), dim3(kFcWarps * 32), f.smem, st, 
         static_cast<const __nv_bfloat16 *>(dO), wp, static_cast<__nv_bfloat16 *>(dI), f.B, f.C, f.Cout, f.ksteps,
@@ -709,7 +709,7 @@ FcDkPlan fc_dk_plan(const Problem &p) {
 }  // namespace
 
 bool fc_hmma_dk_supported(const Problem &p) {
-    static const bool off = getenv("CAPSCONV_NO_FC_HMMA") != nullptr;
+    static const bool off = probe_env("CAPSCONV_NO_FC_HMMA") != nullptr;
     return !off && fc_dk_plan(p).ok;
 }
 
@@ -726,12 +726,12 @@ cudaError_t fc_hmma_dk(const Problem &p, const void *I, const void *dO, float *d
     const dim3 grid((unsigned)f.ksplit, (unsigned)f.mblocks);
     const __nv_bfloat16 *Ib = static_cast<const __nv_bfloat16 *>(I), *Ob = static_cast<const __nv_bfloat16 *>(dO);
     const uint32_t smem = kDkStages * kDkStageBytes + kDkBfrBytes + kDkStages * 8;
-    static const int dbg = getenv("CAPSCONV_FC_DBG") ? atoi(getenv("CAPSCONV_FC_DBG")) : 0;   // probe only
+    static const int dbg = probe_env("CAPSCONV_FC_DBG") ? atoi(probe_env("CAPSCONV_FC_DBG")) : 0;   // probe only
     cudaError_t e = cudaSuccess;
     switch (f.NT) {
 #define DK_CASE(nt)                                                                                         \
     case nt:                                                                                                \
-        e = cudaFuncSetAttribute(fc_dk_kernel<nt>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        e = smem_optin(reinterpret_cast<const void *>(fc_dk_kernel<nt>), (int)smem);     \
         if (e != cudaSuccess) return e;                                                                         \
         launch_k(fc_dk_kernel<nt>, dim3(grid), dim3(kFcWarps * 32), smem, st, Ib, Ob, part, f.B, f.C, f.Cout, f.bslice, dbg);       \
         break;

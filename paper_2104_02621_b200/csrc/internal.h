@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 
 #include "capsconv.h"
 
@@ -35,6 +36,24 @@ const DeviceInfo &device_info();
 
 // Counts kernels enqueued by the library (capsconv_launch_count()).
 void note_launches(int n);
+
+// Diagnostic knobs (planner overrides, switches that skip loads / MMAs /
+// stores, timing traces, the PDL A/B switch) exist only in probe builds
+// (-DCAPSCONV_PROBES, tests/probe/); the product library never reads the
+// environment, so no variable can change its results or make a call
+// synchronise.
+#ifdef CAPSCONV_PROBES
+constexpr bool kProbes = true;
+inline const char *probe_env(const char *name) { return getenv(name); }
+#else
+constexpr bool kProbes = false;
+inline const char *probe_env(const char *) { return nullptr; }
+#endif
+
+// Opt `func` in to `bytes` of dynamic shared memory on the CURRENT device
+// (the attribute is per function and per device).  Thread-safe; the driver
+// call is made once per (function, device, larger size).
+cudaError_t smem_optin(const void *func, int bytes);
 
 // Programmatic dependent launch (PDL) for the kernels of the hot path: the
 // launch may begin while the previous kernel in the stream is still running;

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -61,7 +62,7 @@ __device__ __forceinline__ int fd_floor(const FastDiv &fd, int a) {
 
 #define TRACE(role, idx, ev)                                                                      \
     do {                                                                                          \
-        if (P.trace && blockIdx.x == 0 && (idx) < 64)                                             \
+        if (kProbes && P.trace && blockIdx.x == 0 && (idx) < 64)                                             \
             P.trace[((role) * 64 + (idx)) * 4 + (ev)] = gtime();                                  \
     } while (0)
 
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 }
                 mbar_wait(stg_full + sb, sphase);
                 if (tid == 0) TRACE(0, ii, 1);
-                if (P.dbg & 64) {
+                if (kProbes && (P.dbg & 64)) {
                 } else if (P.I_rows || P.stg_tall) {
                     const uint32_t tab = smem_u32(smem_raw) + P.tab_off;
                     if (P.stg_tall) build_table_tall(P, it, tab, tid);
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     asm volatile("bar.sync 1, %0;\n" ::"r"(kProducerThreads) : "memory");
                     repack_rows(P, stg0 + sb * P.stg_bytes, tab, a_stage, tid);
                     asm volatile("bar.sync 1, %0;\n" ::"r"(kProducerThreads) : "memory");   // table reuse
-                } else if (!(P.dbg & 1)) {
+                } else if (!(kProbes && (P.dbg & 1))) {
                     repack_window(P, it, stg0 + sb * P.stg_bytes, a_stage, tid);
                 }
                 fence_proxy_async_smem();
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
             // the two warps of this lane quarter -- both stay busy even for
             // one tile per item (G = 1)
             const int nch = (P.N_tile + 31) / 32;
-            const int nunits = (P.dbg & 32) ? 0 : P.gpi * it.ntl * nch;
+            const int nunits = (kProbes && (P.dbg & 32)) ? 0 : P.gpi * it.ntl * nch;
             int cur_t = -1;
             int u = 0, d1 = row & 3;
             bool valid = false;
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 {
                     float va[16], vb[16];
                     const bool two = n0 + 16 < P.N_tile;
-                    if (!(P.dbg & 16)) {
+                    if (!(kProbes && (P.dbg & 16))) {
                         tmem_ld16(tcol + n0, va);
                         if (two) tmem_ld16(tcol + n0 + 16, vb);
                         tmem_wait_ld();
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
 #pragma unroll
                         for (int e = 0; e < 16; ++e) va[e] = vb[e] = (float)e;
                     }
-                    if (!(P.dbg & 4)) {
+                    if (!(kProbes && (P.dbg & 4))) {
                         epi_store16(P, it, va, n0, u, d1, valid, opix);
                         if (two) epi_store16(P, it, vb, n0 + 16, u, d1, valid, opix);
                     }
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                     mbar_wait(stg_empty + sb, sphase ^ 1);
                     const uint32_t stg = stg0 + sb * P.stg_bytes;
                     const uint32_t mb = smem_u32(stg_full + sb);
-                    if (!(P.dbg & 1)) {
+                    if (!(kProbes && (P.dbg & 1))) {
                         // issue the copies, then arm with their byte count (the transaction
                         // count may go transiently negative; the phase cannot complete
                         // before this arrival) -- one walk over the staging plan
@@ -635,7 +636,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_
                 const int ksteps = P.CC / 4;
                 // warp-converged tap loop; one elected lane issues the tap's
                 // (k-step x tile) MMAs, fully unrolled for the common shapes
-                if (!(P.dbg & 2)) {
+                if (!(kProbes && (P.dbg & 2))) {
                     const TapIssue ti{a_desc0, b_desc0, P.a_lbo >> 4, b_lbo >> 4, (uint32_t)P.N_tile, idesc,
                                       tmem + (uint32_t)(abuf * P.gpi * P.G * P.N_tile), offmin, T0,
                                       ch == it.c_begin};
@@ -865,7 +866,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
         for (int t = 0; t < P.ntaps; ++t) { offmin_all = std::min(offmin_all, tshift[t]); mx = std::max(mx, tshift[t]); }
         span_all = mx - offmin_all;
     }
-    static const int no_merge = getenv("CAPSCONV_NO_MERGE") ? 1 : 0;
+    static const int no_merge = probe_env("CAPSCONV_NO_MERGE") ? 1 : 0;
     const long long vtotal = (long long)P.Bn * P.Hg * P.Wg;
     if (vtotal * 4 >= (1ll << 31) || (long long)P.src_H * P.src_W * P.Bn >= (1ll << 31)) return pl;
 
@@ -884,7 +885,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
     bool found = false;
     ConvMma best;
     long long best_score = -1;
-    static const int force_g = getenv("CAPSCONV_FORCE_G") ? atoi(getenv("CAPSCONV_FORCE_G")) : 0;
+    static const int force_g = probe_env("CAPSCONV_FORCE_G") ? atoi(probe_env("CAPSCONV_FORCE_G")) : 0;
     const int gpis[2] = {P.nog, 1};
     for (int gq = (P.nog > 1 && !no_merge) ? 0 : 1; gq < 2; ++gq) {
     const int gpi = gpis[gq];
@@ -892,7 +893,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
     for (int G : {8, 4, 2, 1}) {
         if (force_g && G != force_g) continue;
         for (int cc : ccs) {
-            static const int force_cc = getenv("CAPSCONV_FORCE_CC") ? atoi(getenv("CAPSCONV_FORCE_CC")) : 0;
+            static const int force_cc = probe_env("CAPSCONV_FORCE_CC") ? atoi(probe_env("CAPSCONV_FORCE_CC")) : 0;
             if (force_cc && cc != force_cc) continue;
             const int nchunks = P.CSpad / cc;
             int ksplit = 1;
@@ -928,7 +929,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
             if (!batch_mode && !rows_mode && P.Wg * s > 256) continue;
             const int BB = std::min(win_px, 256);
             // tall boxes: unit-stride source planes outside batch/rows mode
-            static const int no_tall = getenv("CAPSCONV_NO_TALL") ? 1 : 0;
+            static const int no_tall = probe_env("CAPSCONV_NO_TALL") ? 1 : 0;
             // (only when a virtual-row box is small: <= 2.5 KB per TMA op is
             // op-rate bound, measured: L3 dI 146 -> 99 us; 3 KB rows are not)
             const bool tall_ok = !batch_mode && !rows_mode && P.pl_s == 1 && !no_tall && P.src_W <= 256 &&
@@ -941,7 +942,7 @@ Plan make_plan(const Problem &p, bool dgrad) {
             // batch mode (fully-connected view) is a streaming GEMM: deeper
             // staging keeps more HBM bytes in flight per SM
             const int max_nstg = batch_mode ? kMaxStg : 2;
-            static const int force_h = getenv("CAPSCONV_TALL_H") ? atoi(getenv("CAPSCONV_TALL_H")) : -1;
+            static const int force_h = probe_env("CAPSCONV_TALL_H") ? atoi(probe_env("CAPSCONV_TALL_H")) : -1;
             for (int h : {8, 4, 2, 1, 0}) {            // h = 0: one virtual row per box
                 if (force_h >= 0 && h > 0 && h != force_h) continue;   // (row boxes stay the fallback)
                 if (h > 0 && (!tall_ok || h > P.src_H || nseg > 4)) continue;
@@ -1022,7 +1023,7 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
                      cudaStream_t st) {
     ConvMma &P = pl.P;
     if (ws_bytes < pl.wpack_bytes + pl.part_bytes) return cudaErrorInvalidValue;
-    static const int dbg_bits = getenv("CAPSCONV_MMA_DBG") ? atoi(getenv("CAPSCONV_MMA_DBG")) : 0;
+    static const int dbg_bits = probe_env("CAPSCONV_MMA_DBG") ? atoi(probe_env("CAPSCONV_MMA_DBG")) : 0;
     P.dbg = dbg_bits;
     uint8_t *w = static_cast<uint8_t *>(ws);
     P.src = static_cast<const __nv_bfloat16 *>(src);
@@ -1038,13 +1039,10 @@ cudaError_t run_plan(Plan &pl, const void *src, const void *K, void *out, void *
     const long long npack = (long long)pl.wpack_bytes / 16;
     launch_k(pack_weights_kernel, dim3((unsigned)((npack + 255) / 256)), dim3(256), 0, st, pl.pack);
     note_launches(1);
-    static bool attr_set = false;  // per process; the attribute is per function
-    if (!attr_set) {
-        cudaFuncSetAttribute(conv_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit);
-        attr_set = true;
-    }
+    cudaError_t ea = smem_optin(reinterpret_cast<const void *>(conv_mma_kernel), (int)kSmemLimit);
+    if (ea != cudaSuccess) return ea;
     const int grid = std::min(P.n_items, device_info().num_sms);
-    static const bool tracing = getenv("CAPSCONV_TRACE") != nullptr;
+    static const bool tracing = probe_env("CAPSCONV_TRACE") != nullptr;
     P.trace = nullptr;
     if (tracing) {
         cudaMalloc(&P.trace, 3 * 64 * 4 * sizeof(unsigned long long));
@@ -1091,18 +1089,21 @@ struct PlanKey {
     }
 };
 
-const Plan &cached_plan(const Problem &p, bool dgrad) {
+// Entries are immutable and shared: a caller keeps its plan alive while another
+// thread evicts or inserts (the returned pointer never dangles).
+std::shared_ptr<const Plan> cached_plan(const Problem &p, bool dgrad) {
     static std::mutex mu;
-    static std::vector<std::pair<PlanKey, Plan>> cache;
+    static std::vector<std::pair<PlanKey, std::shared_ptr<const Plan>>> cache;
     const DeviceInfo &di = device_info();
     PlanKey k{dgrad ? 1 : 0, (int)p.dt, di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.pad}};
     std::lock_guard<std::mutex> lock(mu);
     for (auto &kv : cache)
         if (kv.first == k) return kv.second;
     if (cache.size() > 256) cache.clear();
-    cache.emplace_back(k, make_plan(p, dgrad));
-    const Plan &pl = cache.back().second;
-    if (getenv("CAPSCONV_DEBUG") && pl.ok) {
+    cache.emplace_back(k, std::make_shared<const Plan>(make_plan(p, dgrad)));
+    std::shared_ptr<const Plan> sp = cache.back().second;
+    const Plan &pl = *sp;
+    if (probe_env("CAPSCONV_DEBUG") && pl.ok) {
         const ConvMma &P = pl.P;
         fprintf(stderr,
                 "[capsconv] mma plan: %s CS=%d NCH=%d Hg=%d Wg=%d npl=%d nog=%d taps=%d N_tile=%d n_ntiles=%d CC=%d "
@@ -1112,7 +1113,7 @@ const Plan &cached_plan(const Problem &p, bool dgrad) {
                 P.nchunks, P.ksplit, P.G, P.n_mtiles, P.n_items, P.win_px, P.nstages, P.b_resident, P.smem_bytes,
                 P.tmem_cols, P.nstg, P.stg_cap_px, P.stg_batch_mode, P.gpi, P.stg_tall ? P.h_box : 0);
     }
-    return pl;
+    return sp;
 }
 
 }  // namespace
@@ -1121,21 +1122,21 @@ bool mma_supported(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return fc_hmma_dk_supported(p) || wgrad_supported(p);
     if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return true;
     if (op == CAPSCONV_OP_BWD_DATA && fc_hmma_dgrad_supported(p)) return true;
-    return cached_plan(p, op == CAPSCONV_OP_BWD_DATA).ok;
+    return cached_plan(p, op == CAPSCONV_OP_BWD_DATA)->ok;
 }
 
 size_t mma_workspace_bytes(capsconv_op_t op, const Problem &p) {
     if (op == CAPSCONV_OP_BWD_KERNEL) return fc_hmma_dk_supported(p) ? fc_hmma_dk_workspace(p) : wgrad_workspace_bytes(p);
     if (op == CAPSCONV_OP_FWD && fc_hmma_fwd_supported(p)) return fc_hmma_fwd_workspace(p);
     if (op == CAPSCONV_OP_BWD_DATA && fc_hmma_dgrad_supported(p)) return fc_hmma_dgrad_workspace(p);
-    const Plan &pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
-    return pl.ok ? pl.wpack_bytes + pl.part_bytes : 0;
+    std::shared_ptr<const Plan> pl = cached_plan(p, op == CAPSCONV_OP_BWD_DATA);
+    return pl->ok ? pl->wpack_bytes + pl->part_bytes : 0;
 }
 
 cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
     if (fc_hmma_fwd_supported(p)) return fc_hmma_fwd(p, I, K, O, ws, ws_bytes, st);
-    Plan pl = cached_plan(p, false);
+    Plan pl = *cached_plan(p, false);
     if (!pl.ok) return cudaErrorNotSupported;
     return run_plan(pl, I, K, O, ws, ws_bytes, st);
 }
@@ -1143,7 +1144,7 @@ cudaError_t mma_fwd(const Problem &p, const void *I, const void *K, void *O, voi
 cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, void *ws, size_t ws_bytes,
                          cudaStream_t st) {
     if (fc_hmma_dgrad_supported(p)) return fc_hmma_dgrad(p, dO, K, dI, ws, ws_bytes, st);
-    Plan pl = cached_plan(p, true);
+    Plan pl = *cached_plan(p, true);
     if (!pl.ok) return cudaErrorNotSupported;
     return run_plan(pl, dO, K, dI, ws, ws_bytes, st);
 }

@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -130,7 +131,7 @@ struct WgradMma {
 };
 #define WTRACE(role, idx, ev)                                                              \
     do {                                                                                   \
-        if (P.trace && blockIdx.x == 0 && (idx) < 64) P.trace[((role) * 64 + (idx)) * 4 + (ev)] = gtime(); \
+        if (kProbes && P.trace && blockIdx.x == 0 && (idx) < 64) P.trace[((role) * 64 + (idx)) * 4 + (ev)] = gtime(); \
     } while (0)
 
 __device__ __forceinline__ void wdecode(const WgradMma &P, int item, int &mt, int &ks, int &p0, int &p1) {
@@ -746,14 +747,14 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 if (tid == 0) WTRACE(1, si, 1);
                 if (P.I_rows) w_build_table(P, G, v0, tab, gtid, gsize);
                 w_build_btab(P, v0, btab, gtid, gsize);
-                if (!(P.dbg & 1)) w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, gtid, gsize);
+                if (!(kProbes && (P.dbg & 1))) w_transpose_stage(stg0 + sb * P.stg_bytes, P.stgI_bytes, gtid, gsize);
                 named_bar_sync(1 + lg, gsize);
                 mbar_wait(op_empty + st, ph ^ 1);
                 fence_after_sync();
                 if (tid == 0) WTRACE(1, si, 2);
                 const uint32_t stg = stg0 + sb * P.stg_bytes;
-                if (!(P.dbg & 4)) w_load_B(P, stg, btab, op0 + st * P.b_bytes, gtid, bpstep);
-                if (P.dbg & 16) {
+                if (!(kProbes && (P.dbg & 4))) w_load_B(P, stg, btab, op0 + st * P.b_bytes, gtid, bpstep);
+                if (kProbes && (P.dbg & 16)) {
                 } else if (P.I_rows)
                     w_load_A_rows(P, L, stg, tab, zero8, tmem + P.acc_cols + (uint32_t)st * P.abuf_cols, q, part,
                                   nparts);
@@ -845,7 +846,7 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
                 const uint32_t a0 = tmem + P.acc_cols + (uint32_t)st * P.abuf_cols;
                 // the warp stays converged; one elected lane issues 4 k-steps at
                 // a time (a long divergent single-lane loop issues far slower)
-                if (P.dbg & 2) {
+                if (kProbes && (P.dbg & 2)) {
                 } else if (P.bdesc) {
                     // accumulator block bi = shift j = nq-1-bi reads F_0 from
                     // pixel bi (descriptor offset); one MMA covers bmat adjacent
@@ -1018,8 +1019,8 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     // descriptor offsets and each copy is its own N = 4*Cout MMA (the
     // accumulators, nq*4*Cout columns per tile, only have to fit TMEM);
     // otherwise the copies are materialised side by side in one N <= 256 MMA.
-    static const int force_nq1 = getenv("CAPSCONV_WG_NQ1") ? 1 : 0;
-    static const int bdesc_env = getenv("CAPSCONV_WG_BDESC") ? atoi(getenv("CAPSCONV_WG_BDESC")) : -1;
+    static const int force_nq1 = probe_env("CAPSCONV_WG_NQ1") ? 1 : 0;
+    static const int bdesc_env = probe_env("CAPSCONV_WG_BDESC") ? atoi(probe_env("CAPSCONV_WG_BDESC")) : -1;
     P.KWv = fc ? 1 : (int)p.KW;
     P.nq = 1;
     P.bdesc = 0;
@@ -1032,7 +1033,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
         }
     }
     {
-        static const int bmat_env = getenv("CAPSCONV_WG_BMAT") ? atoi(getenv("CAPSCONV_WG_BMAT")) : 0;
+        static const int bmat_env = probe_env("CAPSCONV_WG_BMAT") ? atoi(probe_env("CAPSCONV_WG_BMAT")) : 0;
         P.bmat = 1;
         // measured (tests/probe/ab.sh CAPSCONV_WG_BMAT 2 1): two copies are
         // slower on every stack layer (the bigger B costs pipeline depth), so
@@ -1098,7 +1099,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     const int nsm = device_info().num_sms;
     P.CBO = std::min(16, P.Cout);
     const int nbO = cdiv(P.Cout, P.CBO);
-    static const int force_tg = getenv("CAPSCONV_WG_TG") ? atoi(getenv("CAPSCONV_WG_TG")) : 0;
+    static const int force_tg = probe_env("CAPSCONV_WG_TG") ? atoi(probe_env("CAPSCONV_WG_TG")) : 0;
     bool found = false;
     // tiles per CTA group: as many as TMEM holds (shared staged window), then
     // pixels per stage and pipeline depths that fit shared memory
@@ -1137,7 +1138,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
         }
         P.CBI = std::min(16, gmax_ci);
         const int nbI = cdiv(gmax_ci, P.CBI);
-        static const int force_kp = getenv("CAPSCONV_WG_KP") ? atoi(getenv("CAPSCONV_WG_KP")) : 0;
+        static const int force_kp = probe_env("CAPSCONV_WG_KP") ? atoi(probe_env("CAPSCONV_WG_KP")) : 0;
         for (int KP : {128, 96, 64, 32, 16}) {
             if (force_kp ? KP != force_kp : KP > 64) continue;
             const uint32_t acc = (uint32_t)(TG * P.N_tile);
@@ -1161,7 +1162,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
             const uint32_t tab_stride = btab_off + (((uint32_t)(KP + P.nq) * 4u + 15u) & ~15u);
             // (A buffers, staging buffers): equal counts first, so that the
             // loader can run that many stage groups concurrently
-            static const int cmode = getenv("CAPSCONV_WG_CMODE") ? atoi(getenv("CAPSCONV_WG_CMODE")) : 0;
+            static const int cmode = probe_env("CAPSCONV_WG_CMODE") ? atoi(probe_env("CAPSCONV_WG_CMODE")) : 0;
             // (A buffers, staging buffers): equal counts first, so that the
             // loader runs that many stage groups concurrently; 3/3 (three
             // groups of 5-6 warps) measured best where it fits (L1 dK 152 ->
@@ -1201,7 +1202,7 @@ WPlan make_wplan(const Problem &p, bool allow_nq) {
     P.fd_Wg.init((uint32_t)P.Wg);
     P.fd_HgWg.init((uint32_t)(P.Hg * P.Wg));
     P.fd_uppO.init((uint32_t)(2 * P.Cout));
-    static const int lg_env = getenv("CAPSCONV_WG_LG") ? atoi(getenv("CAPSCONV_WG_LG")) : 0;
+    static const int lg_env = probe_env("CAPSCONV_WG_LG") ? atoi(probe_env("CAPSCONV_WG_LG")) : 0;
     P.lgroups = 1;
     // groups of 4 or 8 warps (every group covers the four lane quarters).
     // NG must divide both buffer counts: then a buffer is always used by the
@@ -1232,9 +1233,10 @@ struct WKey {
     }
 };
 
-const WPlan &cached_wplan(const Problem &p) {
+// Entries are immutable and shared (see cached_plan in mma.cu).
+std::shared_ptr<const WPlan> cached_wplan(const Problem &p) {
     static std::mutex mu;
-    static std::vector<std::pair<WKey, WPlan>> cache;
+    static std::vector<std::pair<WKey, std::shared_ptr<const WPlan>>> cache;
     const DeviceInfo &di = device_info();
     WKey k{di.device, di.num_sms, {p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.pad}};
     if (p.dt != CAPSCONV_BF16) k.e[7] = -1;
@@ -1244,9 +1246,10 @@ const WPlan &cached_wplan(const Problem &p) {
     if (cache.size() > 256) cache.clear();
     WPlan w = make_wplan(p, true);
     if (!w.ok) w = make_wplan(p, false);   // column shifts do not fit TMEM/smem: one tap per slot
-    cache.emplace_back(k, w);
-    const WPlan &pl = cache.back().second;
-    if (getenv("CAPSCONV_DEBUG") && pl.ok) {
+    cache.emplace_back(k, std::make_shared<const WPlan>(w));
+    std::shared_ptr<const WPlan> sp = cache.back().second;
+    const WPlan &pl = *sp;
+    if (probe_env("CAPSCONV_DEBUG") && pl.ok) {
         const WgradMma &P = pl.P;
         fprintf(stderr,
                 "[capsconv] wgrad plan: C=%d Cout=%d Hg=%d Wg=%d taps=%d mtiles=%d TG=%d groups=%d N_tile=%d KP=%d "
@@ -1254,21 +1257,21 @@ const WPlan &cached_wplan(const Problem &p) {
                 P.C, P.Cout, P.Hg, P.Wg, P.ntaps, P.n_mtiles, P.TG, P.n_groups, P.N_tile, P.KP, P.ksplit, P.n_items,
                 P.capI, P.capO, P.nstg, P.nstages, P.smem_bytes, P.acc_cols, P.abuf_cols, P.nq, P.bdesc);
     }
-    return pl;
+    return sp;
 }
 
 }  // namespace
 
-bool wgrad_supported(const Problem &p) { return cached_wplan(p).ok; }
+bool wgrad_supported(const Problem &p) { return cached_wplan(p)->ok; }
 
 size_t wgrad_workspace_bytes(const Problem &p) {
-    const WPlan &pl = cached_wplan(p);
-    return pl.ok ? pl.part_bytes : 0;
+    std::shared_ptr<const WPlan> pl = cached_wplan(p);
+    return pl->ok ? pl->part_bytes : 0;
 }
 
 cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
                       cudaStream_t st) {
-    WPlan pl = cached_wplan(p);
+    WPlan pl = *cached_wplan(p);
     if (!pl.ok || ws_bytes < pl.part_bytes) return cudaErrorNotSupported;
     WgradMma &P = pl.P;
     const int boxw = P.batch_mode ? 1 : P.Wg;
@@ -1280,14 +1283,11 @@ cudaError_t wgrad_run(const Problem &p, const void *I, const void *dO, float *dK
     P.part = P.ksplit > 1 ? static_cast<float *>(ws) : dK;
     P.I_ptr = static_cast<const uint8_t *>(I);
     P.O_ptr = static_cast<const uint8_t *>(dO);
-    P.dbg = getenv("CAPSCONV_WG_DBG") ? atoi(getenv("CAPSCONV_WG_DBG")) : 0;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmemLimit);
-        attr = true;
-    }
+    P.dbg = probe_env("CAPSCONV_WG_DBG") ? atoi(probe_env("CAPSCONV_WG_DBG")) : 0;
+    cudaError_t ea = smem_optin(reinterpret_cast<const void *>(wgrad_kernel), (int)kWSmemLimit);
+    if (ea != cudaSuccess) return ea;
     const int grid = std::min(P.n_items, device_info().num_sms);
-    static const bool tracing = getenv("CAPSCONV_TRACE") != nullptr;
+    static const bool tracing = probe_env("CAPSCONV_TRACE") != nullptr;
     P.trace = nullptr;
     if (tracing) {
         cudaMalloc(&P.trace, 3 * 64 * 4 * 8);

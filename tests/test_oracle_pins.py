@@ -403,6 +403,49 @@ def test_stack_depth1_and_fd(oracle_mod):
         assert abs(fd - dKs[0][idx]) <= 1e-6 * max(1.0, abs(fd))
 
 
+def test_stack_bf16_boundaries_chain(oracle_mod):
+    """Reading R13: with bf16_boundaries the oracle stack rounds each layer's
+    forward output and each propagated dI to bf16 (RNE) -- and nothing else.
+    Pinned against a hand-composed 2-layer chain built from independent
+    pieces: torch conv2d in fp64 on the F1 view (autograd for dI, dK) and
+    torch's IEEE bfloat16 cast.  Inputs are small dyadic rationals (multiples
+    of 1/4, dY of 1/64), so every fp64 sum is exact and the roundings are the
+    only inexact steps."""
+    g = np.random.default_rng(2024)
+    q = lambda shape: g.integers(-4, 5, size=shape) / 4.0
+    X = q((2, 9, 9, 3, 4, 4))
+    K1 = q((3, 3, 3, 5, 4, 4))
+    K2 = q((3, 3, 5, 2, 4, 4))
+    bf = lambda t: t.detach().to(torch.bfloat16).to(torch.float64)
+
+    def layer(I, K, s, dO=None):
+        It, Kt, O = _conv2d_view(I, K, s)
+        if dO is None:
+            return O.detach()
+        O.backward(torch.as_tensor(dO))
+        return It.grad, Kt.grad
+
+    a1 = bf(layer(X, K1, 1))                       # rounded activation
+    y = bf(layer(a1.numpy(), K2, 2))
+    dY = g.integers(-100, 101, size=tuple(y.shape)) / 64.0   # more significant bits than bf16 keeps
+    dI2, dK2 = layer(a1.numpy(), K2, 2, dY)        # dK from the rounded activation
+    dI2 = bf(dI2)                                  # rounded propagated gradient
+    dX, dK1 = layer(X, K1, 1, dI2.numpy())
+    dX = bf(dX)
+
+    acts, rdX, rdKs, _ = oracle_mod.stack_fwd_bwd(X, [K1, K2], [1, 2], dY, True)
+    np.testing.assert_array_equal(acts[1], a1.numpy())
+    np.testing.assert_array_equal(acts[2], y.numpy())
+    np.testing.assert_array_equal(rdX, dX.numpy())
+    np.testing.assert_array_equal(rdKs[1], dK2.numpy())   # dK itself is NOT rounded (fp32 output)
+    np.testing.assert_array_equal(rdKs[0], dK1.numpy())
+    # non-vacuous: the roundings change the activation, the gradients and dK1
+    acts0, rdX0, rdKs0, _ = oracle_mod.stack_fwd_bwd(X, [K1, K2], [1, 2], dY, False)
+    assert not np.array_equal(acts0[1], acts[1])
+    assert not np.array_equal(rdX0, rdX)
+    assert not np.array_equal(rdKs0[0], rdKs[0])
+
+
 # ---------------------------------------------------------------- zero padding (SURVEY NEXT-2)
 # Pinned to the (already pinned) unpadded oracle run on an explicitly
 # zero-padded input -- numpy's pad, not the oracle's own index arithmetic --

@@ -57,8 +57,9 @@ def check_layer(cc, oracle_mod, L, dtype, kind="uniform"):
     assert O.dtype == dtype and dI.dtype == dtype and dK.dtype == torch.float32
     e = (assert_close(to_np(O), rO, aO, dtype, "fwd"),
          assert_close(to_np(dI), rdI, adI, dtype, "bwd_data"),
-         # dK is stored in fp32: the fp32 bar applies to its accumulation
-         assert_close(to_np(dK), rdK, adK, torch.float32 if dtype == torch.float32 else dtype, "bwd_kernel"))
+         # dK is accumulated and stored in fp32 from exactly representable
+         # products (bf16 x bf16 is exact in fp32): the fp32 bar applies
+         assert_close(to_np(dK), rdK, adK, torch.float32, "bwd_kernel"))
     return e
 
 
@@ -193,12 +194,13 @@ def _stack_layers():
     return capsinputs.stack_layers(capsinputs.STACK_BATCH, oracle.output_dims)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
 @pytest.mark.parametrize("li", [0, 1, 2, 3], ids=["L1", "L2", "L3", "FC"])
-def test_stack_layers_full_batch_exact(cc, oracle_mod, li):
+def test_stack_layers_full_batch_exact(cc, oracle_mod, li, dtype):
     """Each layer of the config-5 stack at global batch 1024 (the sizes bench.py
-    times), exact-integer inputs in {-1, 0, 1}: bitwise equal to the oracle."""
+    times), exact-integer inputs in {-1, 0, 1}: bitwise equal to the oracle --
+    bf16 on the tensor-core path, fp32 on the exact-fp32 (SIMT) path."""
     L = _stack_layers()[li]
-    dtype = torch.bfloat16
     I = capsinputs.make_input(L, "int1", dtype, layer_idx=li)
     K = capsinputs.make_kernel(L, "int1", dtype, layer_idx=li)
     Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
@@ -210,9 +212,11 @@ def test_stack_layers_full_batch_exact(cc, oracle_mod, li):
     assert np.abs(rdK).max() < 2 ** 24
     # the benchmarked configuration runs on the tensor-core path, every pass
     ext = (L.B, L.H, L.W, L.C, L.Cout, L.KH, L.KW, L.D1, L.D2, L.D3, L.stride)
-    assert [cc.select_path(op, dtype, ext) for op in (0, 1, 2)] == [cc.PATH_MMA] * 3
-    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
-    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    want = cc.PATH_MMA if dtype == torch.bfloat16 else cc.PATH_SIMT
+    assert [cc.select_path(op, dtype, ext) for op in (0, 1, 2)] == [want] * 3
+    rnd = oracle_mod.round_bf16 if dtype == torch.bfloat16 else (lambda x: x)
+    np.testing.assert_array_equal(to_np(O), rnd(rO))
+    np.testing.assert_array_equal(to_np(dI), rnd(rdI))
     np.testing.assert_array_equal(to_np(dK), rdK)
 
 
