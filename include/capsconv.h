@@ -97,6 +97,21 @@ typedef enum {
     CAPSCONV_OP_BWD_KERNEL = 2
 } capsconv_op_t;
 
+/* Memory layout of the capsule tensors I, dI, O, dO (K and dK always use
+ * [KH][KW][C][Cout][D2][D3]).
+ *   NATURAL  I [B][H][W][C][D1][D2],  O [B][Ho][Wo][Cout][D1][D3]  (the order
+ *            of BASELINE.json's formula; every call without a layout argument)
+ *   ROWS     I [B][H][W][D1][C][D2],  O [B][Ho][Wo][D1][Cout][D3]  ("D1-outer":
+ *            row d1 of all C capsules of a pixel is contiguous).  Memory order
+ *            is invisible to the mathematics (reading R3; the
+ *            paper's Algorithm 2 is itself channel-major);
+ *            this one lets TMA stage tensor-core operands with no repack
+ *            (DESIGN.md §5.5), so chained layers should keep it. */
+typedef enum {
+    CAPSCONV_LAYOUT_NATURAL = 0,
+    CAPSCONV_LAYOUT_ROWS = 1
+} capsconv_layout_t;
+
 typedef enum {
     CAPSCONV_PATH_AUTO = 0,   /* library's choice (only valid as an override) */
     CAPSCONV_PATH_SIMT = 1,   /* register-blocked small-matmul kernels (FFMA, fp32 accumulate) */
@@ -221,6 +236,44 @@ CAPSCONV_API capsconv_status_t capsconv_bwd_data_slices(capsconv_dtype_t dt,
 CAPSCONV_API capsconv_status_t capsconv_bwd_kernel_slices(capsconv_dtype_t dt,
         int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
         int64_t KH, int64_t KW, int64_t S, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+        const void *I, const void *dO, float *dK,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+/* ---- Layout-generic forms.  Each call below is its `_pad` namesake with a
+ * capsconv_layout_t argument for I, dI, O and dO (see above); everything
+ * else -- extents, padding, dtypes, ownership, stream semantics, errors --
+ * is unchanged, and CAPSCONV_LAYOUT_NATURAL is exactly the `_pad` call.
+ * An unknown layout value is CAPSCONV_ERR_DTYPE.  In the ROWS layout the
+ * library runs its TMA-fed tensor-core kernels when they take the problem
+ * (bf16, 4x4 capsules, C and Cout multiples of 4, pad 0, 16-byte aligned
+ * pointers); any other valid problem runs the natural-layout path between
+ * two on-device permutations held in the workspace (query the size with
+ * capsconv_workspace_bytes_ex), so every valid call has a path. */
+CAPSCONV_API capsconv_status_t capsconv_workspace_bytes_ex(capsconv_op_t op, capsconv_dtype_t dt,
+        capsconv_layout_t layout, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        size_t *bytes);
+
+CAPSCONV_API capsconv_status_t capsconv_select_path_ex(capsconv_op_t op, capsconv_dtype_t dt,
+        capsconv_layout_t layout, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        capsconv_path_t *path);
+
+CAPSCONV_API capsconv_status_t capsconv_fwd_ex(capsconv_dtype_t dt, capsconv_layout_t layout,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        const void *I, const void *K, void *O,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+CAPSCONV_API capsconv_status_t capsconv_bwd_data_ex(capsconv_dtype_t dt, capsconv_layout_t layout,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+        const void *dO, const void *K, void *dI,
+        void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
+
+CAPSCONV_API capsconv_status_t capsconv_bwd_kernel_ex(capsconv_dtype_t dt, capsconv_layout_t layout,
+        int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
+        int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
         const void *I, const void *dO, float *dK,
         void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
 

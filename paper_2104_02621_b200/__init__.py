@@ -12,6 +12,8 @@ from .capsconv import (  # noqa: F401
     OP_FWD,
     PATH_AUTO,
     PATH_MMA,
+    LAYOUT_NATURAL,
+    LAYOUT_ROWS,
     PATH_SIMT,
     bwd_data,
     bwd_data_slices,

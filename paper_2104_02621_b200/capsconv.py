@@ -6,9 +6,11 @@ convolution runs inside libcapsconv's kernels.  PyTorch provides device
 memory and streams (plumbing).  There is no CPU fallback: if the library is
 missing or the tensors are not CUDA tensors, these functions raise.
 
-Layouts (Algorithm 2):
-  I, dI : (B, H, W, C, D1, D2)      K : (KH, KW, C, Cout, D2, D3)
-  O, dO : (B, Ho, Wo, Cout, D1, D3) dK: like K, always float32
+Layouts (Algorithm 2), chosen per call with
+``layout=``:
+  "natural" I, dI : (B, H, W, C, D1, D2)   O, dO : (B, Ho, Wo, Cout, D1, D3)
+  "rows"    I, dI : (B, H, W, D1, C, D2)   O, dO : (B, Ho, Wo, D1, Cout, D3)
+  K : (KH, KW, C, Cout, D2, D3) and dK (always float32) in both.
 """
 from __future__ import annotations
 
@@ -24,6 +26,8 @@ LIB_PATH = os.path.join(_PKG, "libcapsconv.so")
 
 OP_FWD, OP_BWD_DATA, OP_BWD_KERNEL = 0, 1, 2
 PATH_AUTO, PATH_SIMT, PATH_MMA = 0, 1, 2
+LAYOUT_NATURAL, LAYOUT_ROWS = 0, 1
+_LAYOUTS = {"natural": LAYOUT_NATURAL, "rows": LAYOUT_ROWS, LAYOUT_NATURAL: LAYOUT_NATURAL, LAYOUT_ROWS: LAYOUT_ROWS}
 _DT = {torch.float32: 0, torch.bfloat16: 1}
 
 _lock = threading.Lock()
@@ -61,6 +65,14 @@ def load_library(path: Optional[str] = None):
         lib.capsconv_select_path_pad.argtypes = [ctypes.c_int, ctypes.c_int] + ext12 + [ctypes.POINTER(ctypes.c_int)]
         for name in ("capsconv_fwd_pad", "capsconv_bwd_data_pad", "capsconv_bwd_kernel_pad"):
             getattr(lib, name).argtypes = [ctypes.c_int] + ext12 + [vp, vp, vp, vp, sz, vp]
+        ci = ctypes.c_int
+        lib.capsconv_workspace_bytes_ex.argtypes = [ci, ci, ci] + ext12 + [ctypes.POINTER(sz)]
+        lib.capsconv_select_path_ex.argtypes = [ci, ci, ci] + ext12 + [ctypes.POINTER(ci)]
+        for name in ("capsconv_fwd_ex", "capsconv_bwd_data_ex", "capsconv_bwd_kernel_ex"):
+            getattr(lib, name).argtypes = [ci, ci] + ext12 + [vp, vp, vp, vp, sz, vp]
+        for name in ("capsconv_workspace_bytes_ex", "capsconv_select_path_ex", "capsconv_fwd_ex",
+                     "capsconv_bwd_data_ex", "capsconv_bwd_kernel_ex"):
+            getattr(lib, name).restype = ci
         lib.capsconv_workspace_bytes_slices.argtypes = [ctypes.c_int, ctypes.c_int] + [i64] * 12 + [ctypes.POINTER(sz)]
         for name in ("capsconv_fwd_slices", "capsconv_bwd_data_slices", "capsconv_bwd_kernel_slices"):
             getattr(lib, name).argtypes = [ctypes.c_int] + [i64] * 12 + [vp, vp, vp, vp, sz, vp]
@@ -129,14 +141,21 @@ def _ext12(ext):
     return ext + (0,) if len(ext) == 11 else ext
 
 
-def workspace_bytes(op: int, dtype, ext) -> int:
+def _layout(layout) -> int:
+    if layout not in _LAYOUTS:
+        raise ValueError("layout must be 'natural' or 'rows', got %r" % (layout,))
+    return _LAYOUTS[layout]
+
+
+def workspace_bytes(op: int, dtype, ext, layout="natural") -> int:
     ext = _ext12(ext)
-    key = (op, dtype, ext, _device_key())
+    lay = _layout(layout)
+    key = (op, dtype, ext, lay, _device_key())
     v = _ws_size_cache.get(key)
     if v is None:
         lib = load_library()
         out = ctypes.c_size_t()
-        _check(lib.capsconv_workspace_bytes_pad(op, _dt(dtype), *ext, ctypes.byref(out)), "workspace_bytes")
+        _check(lib.capsconv_workspace_bytes_ex(op, _dt(dtype), lay, *ext, ctypes.byref(out)), "workspace_bytes")
         v = _ws_size_cache[key] = out.value
     return v
 
@@ -145,10 +164,11 @@ def _device_key():
     return torch.cuda.current_device() if torch.cuda.is_available() else -1
 
 
-def select_path(op: int, dtype, ext) -> int:
+def select_path(op: int, dtype, ext, layout="natural") -> int:
     lib = load_library()
     out = ctypes.c_int()
-    _check(lib.capsconv_select_path_pad(op, _dt(dtype), *_ext12(ext), ctypes.byref(out)), "select_path")
+    _check(lib.capsconv_select_path_ex(op, _dt(dtype), _layout(layout), *_ext12(ext), ctypes.byref(out)),
+           "select_path")
     return out.value
 
 
@@ -184,70 +204,83 @@ def _need_cuda(*ts):
     return dev
 
 
-def _call(name: str, op: int, dtype, ext, a, b, out, stream: Optional[torch.cuda.Stream]):
+def _call(name: str, op: int, dtype, ext, a, b, out, stream: Optional[torch.cuda.Stream], layout=LAYOUT_NATURAL):
     lib = load_library()
     s = stream if stream is not None else torch.cuda.current_stream(out.device)
     handle = s.cuda_stream
     ext = _ext12(ext)
-    need = workspace_bytes(op, dtype, ext)
+    need = workspace_bytes(op, dtype, ext, layout)
     ws = _workspace(need, out.device, handle)
-    fn = getattr(lib, name + "_pad")
+    fn = getattr(lib, name + "_ex")
     with torch.cuda.device(out.device):
-        st = fn(_dt(dtype), *ext, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+        st = fn(_dt(dtype), _layout(layout), *ext, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr() if ws is not None else 0),
                 ctypes.c_size_t(need), ctypes.c_void_p(handle))
     _check(st, name)
     return out
 
 
+def _split(t, layout):
+    """(B, H, W, C, D1, D2) of a capsule tensor in either layout."""
+    if _layout(layout) == LAYOUT_ROWS:
+        B, H, W, D1, C, D2 = t.shape
+    else:
+        B, H, W, C, D1, D2 = t.shape
+    return B, H, W, C, D1, D2
+
+
+def _shape(B, H, W, C, D1, D2, layout):
+    return (B, H, W, D1, C, D2) if _layout(layout) == LAYOUT_ROWS else (B, H, W, C, D1, D2)
+
+
 def fwd(I: torch.Tensor, K: torch.Tensor, stride: int = 1, out: Optional[torch.Tensor] = None,
-        stream: Optional[torch.cuda.Stream] = None, pad: int = 0) -> torch.Tensor:
-    """O = capsule_conv(I, K, stride) (capsconv_fwd); pad > 0: symmetric zero
-    padding of H and W (capsconv_fwd_pad)."""
+        stream: Optional[torch.cuda.Stream] = None, pad: int = 0, layout="natural") -> torch.Tensor:
+    """O = capsule_conv(I, K, stride) (capsconv_fwd_ex); pad > 0: symmetric zero
+    padding of H and W; layout: "natural" or "rows" (capsconv.h)."""
     dev = _need_cuda(I, K)
     if I.dim() != 6 or K.dim() != 6:
-        raise ValueError("I must be (B,H,W,C,D1,D2) and K (KH,KW,C,Cout,D2,D3)")
-    B, H, W, C, D1, D2 = I.shape
+        raise ValueError("I must be (B,H,W,C,D1,D2) [natural] / (B,H,W,D1,C,D2) [rows] and K (KH,KW,C,Cout,D2,D3)")
+    B, H, W, C, D1, D2 = _split(I, layout)
     KH, KW, C2, Cout, D2b, D3 = K.shape
     if C2 != C or D2b != D2 or I.dtype != K.dtype:
         raise ValueError("I %s and K %s disagree" % (tuple(I.shape), tuple(K.shape)))
     Ho, Wo = output_dims(H, W, KH, KW, stride, pad)
-    shape = (B, Ho, Wo, Cout, D1, D3)
+    shape = _shape(B, Ho, Wo, Cout, D1, D3, layout)
     if out is None:
         out = torch.empty(shape, dtype=I.dtype, device=dev)
     elif tuple(out.shape) != shape or out.dtype != I.dtype:
         raise ValueError("out has the wrong shape/dtype")
     ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
-    return _call("capsconv_fwd", OP_FWD, I.dtype, ext, I, K, out, stream)
+    return _call("capsconv_fwd", OP_FWD, I.dtype, ext, I, K, out, stream, layout)
 
 
 def bwd_data(dO: torch.Tensor, K: torch.Tensor, stride: int, H: int, W: int,
              out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
-             pad: int = 0) -> torch.Tensor:
-    """dI (capsconv_bwd_data)."""
+             pad: int = 0, layout="natural") -> torch.Tensor:
+    """dI (capsconv_bwd_data_ex)."""
     dev = _need_cuda(dO, K)
-    B, Ho, Wo, Cout, D1, D3 = dO.shape
+    B, Ho, Wo, Cout, D1, D3 = _split(dO, layout)
     KH, KW, C, Cout2, D2, D3b = K.shape
     if Cout2 != Cout or D3b != D3 or dO.dtype != K.dtype:
         raise ValueError("dO %s and K %s disagree" % (tuple(dO.shape), tuple(K.shape)))
     if output_dims(H, W, KH, KW, stride, pad) != (Ho, Wo):
         raise ValueError("dO spatial extent does not match H, W, K, stride and pad")
-    shape = (B, H, W, C, D1, D2)
+    shape = _shape(B, H, W, C, D1, D2, layout)
     if out is None:
         out = torch.empty(shape, dtype=dO.dtype, device=dev)
     elif tuple(out.shape) != shape or out.dtype != dO.dtype:
         raise ValueError("out has the wrong shape/dtype")
     ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
-    return _call("capsconv_bwd_data", OP_BWD_DATA, dO.dtype, ext, dO, K, out, stream)
+    return _call("capsconv_bwd_data", OP_BWD_DATA, dO.dtype, ext, dO, K, out, stream, layout)
 
 
 def bwd_kernel(I: torch.Tensor, dO: torch.Tensor, stride: int, KH: int, KW: int,
                out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
-               pad: int = 0) -> torch.Tensor:
-    """dK in float32 (capsconv_bwd_kernel)."""
+               pad: int = 0, layout="natural") -> torch.Tensor:
+    """dK in float32 (capsconv_bwd_kernel_ex)."""
     dev = _need_cuda(I, dO)
-    B, H, W, C, D1, D2 = I.shape
-    B2, Ho, Wo, Cout, D1b, D3 = dO.shape
+    B, H, W, C, D1, D2 = _split(I, layout)
+    B2, Ho, Wo, Cout, D1b, D3 = _split(dO, layout)
     if B2 != B or D1b != D1 or I.dtype != dO.dtype:
         raise ValueError("I %s and dO %s disagree" % (tuple(I.shape), tuple(dO.shape)))
     if output_dims(H, W, KH, KW, stride, pad) != (Ho, Wo):
@@ -258,7 +291,7 @@ def bwd_kernel(I: torch.Tensor, dO: torch.Tensor, stride: int, KH: int, KW: int,
     elif tuple(out.shape) != shape or out.dtype != torch.float32:
         raise ValueError("out must be float32 of the kernel's shape")
     ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
-    return _call("capsconv_bwd_kernel", OP_BWD_KERNEL, I.dtype, ext, I, dO, out, stream)
+    return _call("capsconv_bwd_kernel", OP_BWD_KERNEL, I.dtype, ext, I, dO, out, stream, layout)
 
 
 # ------------------------------------------------------------ S-slice capsules (R22)

@@ -3,6 +3,7 @@
 //
 // Every argument is validated before anything is enqueued, so a non-OK
 // status other than CAPSCONV_ERR_CUDA leaves all buffers untouched.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -87,8 +88,10 @@ static bool mul_ok(int64_t a, int64_t b, int64_t *out) {
 
 static capsconv_status_t make_problem(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,
                                       int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
-                                      int64_t s, int64_t pad, Problem *p) {
+                                      int64_t s, int64_t pad, Problem *p, int layout = CAPSCONV_LAYOUT_NATURAL) {
     if (dt != CAPSCONV_F32 && dt != CAPSCONV_BF16) return fail(CAPSCONV_ERR_DTYPE, "unknown dtype %d", (int)dt);
+    if (layout != CAPSCONV_LAYOUT_NATURAL && layout != CAPSCONV_LAYOUT_ROWS)
+        return fail(CAPSCONV_ERR_DTYPE, "unknown layout %d", layout);
     if (s < 1) return fail(CAPSCONV_ERR_STRIDE, "stride %lld < 1", (long long)s);
     if (pad < 0 || pad > (1 << 20)) return fail(CAPSCONV_ERR_SHAPE, "padding %lld out of [0, 2^20]", (long long)pad);
     const int64_t ext[] = {B, H, W, C, Cout, KH, KW, D1, D2, D3};
@@ -103,6 +106,7 @@ static capsconv_status_t make_problem(capsconv_dtype_t dt, int64_t B, int64_t H,
     p->KH = KH; p->KW = KW; p->D1 = D1; p->D2 = D2; p->D3 = D3; p->s = s; p->pad = pad;
     p->Ho = (H + 2 * pad - KH) / s + 1;
     p->Wo = (W + 2 * pad - KW) / s + 1;
+    p->layout = layout;
     // Element counts (and their byte sizes) must fit comfortably in int64.
     int64_t n = 1;
     const int64_t in_f[] = {B, H, W, C, D1, D2, 8};
@@ -122,14 +126,50 @@ static capsconv_status_t make_problem(capsconv_dtype_t dt, int64_t B, int64_t H,
     return CAPSCONV_OK;
 }
 
+// ---- rows layout (D1-outer): the TMA-fed tensor-core kernels when they take
+// the problem, else the natural-layout path between two permutations.
+static bool rows_mma(capsconv_op_t op, const Problem &p) {
+    if (p.layout != CAPSCONV_LAYOUT_ROWS || g_path_override.load() == CAPSCONV_PATH_SIMT) return false;
+    if (rows_fc_supported(op, p)) return true;
+    return op == CAPSCONV_OP_BWD_KERNEL ? rows_wgrad_supported(p) : rows_conv_supported(op, p);
+}
+static size_t rows_mma_ws(capsconv_op_t op, const Problem &p) {
+    if (rows_fc_supported(op, p)) return rows_fc_workspace_bytes(op, p);
+    return op == CAPSCONV_OP_BWD_KERNEL ? rows_wgrad_workspace_bytes(p) : rows_conv_workspace_bytes(op, p);
+}
+static Problem natural_of(const Problem &p) {
+    Problem q = p;
+    q.layout = CAPSCONV_LAYOUT_NATURAL;
+    return q;
+}
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+// fallback workspace: [natural copy of the first operand][natural copy of the
+// second operand or of the output][the natural path's own workspace]
+static size_t rows_fb_a(capsconv_op_t op, const Problem &p) {
+    return align256((size_t)(op == CAPSCONV_OP_BWD_DATA ? p.n_out() : p.n_in()) * p.elem());
+}
+static size_t rows_fb_b(capsconv_op_t op, const Problem &p) {
+    return align256((size_t)(op == CAPSCONV_OP_BWD_DATA ? p.n_in() : p.n_out()) * p.elem());
+}
+
 static capsconv_path_t choose_path(capsconv_op_t op, const Problem &p) {
     const int ov = g_path_override.load();
     if (ov == CAPSCONV_PATH_SIMT) return CAPSCONV_PATH_SIMT;
+    if (p.layout == CAPSCONV_LAYOUT_ROWS) {
+        if (rows_mma(op, p)) return CAPSCONV_PATH_MMA;
+        return choose_path(op, natural_of(p));
+    }
     if (mma_supported(op, p)) return CAPSCONV_PATH_MMA;
     return CAPSCONV_PATH_SIMT;
 }
 
 static size_t workspace_for(capsconv_op_t op, const Problem &p) {
+    if (p.layout == CAPSCONV_LAYOUT_ROWS) {
+        const size_t fb = rows_fb_a(op, p) + rows_fb_b(op, p) + workspace_for(op, natural_of(p));
+        if (!rows_mma(op, p)) return fb;
+        // misaligned pointers take the fallback: cover both
+        return std::max(rows_mma_ws(op, p), fb);
+    }
     if (choose_path(op, p) == CAPSCONV_PATH_MMA) {
         // The MMA path falls back to SIMT for misaligned pointers, so the
         // workspace covers both.
@@ -159,7 +199,48 @@ static capsconv_status_t finish(cudaError_t e, const char *what) {
 // Path choice + launch for a validated problem (the body shared by the
 // plain, padded and S-slice entry points).
 static cudaError_t dispatch(capsconv_op_t op, const Problem &p, const void *a, const void *b, void *out, void *ws,
+                            size_t ws_bytes, cudaStream_t cs);
+
+// Rows-layout call: a = I (fwd, dK) or dO (dI); b = K (fwd, dI) or dO (dK).
+static cudaError_t dispatch_rows(capsconv_op_t op, const Problem &p, const void *a, const void *b, void *out,
+                                 void *ws, size_t ws_bytes, cudaStream_t cs) {
+    const size_t need = rows_mma(op, p) ? rows_mma_ws(op, p) : 0;
+    if (rows_mma(op, p) && aligned16(a) && aligned16(b) && aligned16(out) && (need == 0 || aligned16(ws))) {
+        if (rows_fc_supported(op, p)) return rows_fc_run(op, p, a, b, out, ws, ws_bytes, cs);
+        if (op == CAPSCONV_OP_BWD_KERNEL)
+            return rows_wgrad_run(p, a, b, static_cast<float *>(out), ws, ws_bytes, cs);
+        return rows_conv_run(op, p, a, b, out, ws, ws_bytes, cs);
+    }
+    const Problem q = natural_of(p);
+    uint8_t *w8 = static_cast<uint8_t *>(ws);
+    const size_t na = rows_fb_a(op, p), nb = rows_fb_b(op, p);
+    if (ws_bytes < na + nb) return cudaErrorInvalidValue;
+    void *wa = w8, *wb = w8 + na, *wr = w8 + na + nb;
+    const size_t rest = ws_bytes - na - nb;
+    const int64_t pin = p.B * p.H * p.W, pout = p.B * p.Ho * p.Wo;
+    cudaError_t e;
+    switch (op) {
+        case CAPSCONV_OP_FWD:
+            e = permute_layout(p.dt, a, wa, pin, p.C, p.D1, p.D2, 0, cs);
+            if (e == cudaSuccess) e = dispatch(op, q, wa, b, wb, wr, rest, cs);
+            if (e == cudaSuccess) e = permute_layout(p.dt, wb, out, pout, p.Cout, p.D1, p.D3, 1, cs);
+            return e;
+        case CAPSCONV_OP_BWD_DATA:
+            e = permute_layout(p.dt, a, wa, pout, p.Cout, p.D1, p.D3, 0, cs);
+            if (e == cudaSuccess) e = dispatch(op, q, wa, b, wb, wr, rest, cs);
+            if (e == cudaSuccess) e = permute_layout(p.dt, wb, out, pin, p.C, p.D1, p.D2, 1, cs);
+            return e;
+        default:
+            e = permute_layout(p.dt, a, wa, pin, p.C, p.D1, p.D2, 0, cs);
+            if (e == cudaSuccess) e = permute_layout(p.dt, b, wb, pout, p.Cout, p.D1, p.D3, 0, cs);
+            if (e == cudaSuccess) e = dispatch(op, q, wa, wb, out, wr, rest, cs);
+            return e;
+    }
+}
+
+static cudaError_t dispatch(capsconv_op_t op, const Problem &p, const void *a, const void *b, void *out, void *ws,
                             size_t ws_bytes, cudaStream_t cs) {
+    if (p.layout == CAPSCONV_LAYOUT_ROWS) return dispatch_rows(op, p, a, b, out, ws, ws_bytes, cs);
     const size_t need = workspace_for(op, p);
     const bool mma = choose_path(op, p) == CAPSCONV_PATH_MMA && aligned16(a) && aligned16(b) && aligned16(out) &&
                      (need == 0 || aligned16(ws));
@@ -259,28 +340,83 @@ capsconv_status_t capsconv_set_path_override(capsconv_path_t path) {
     return CAPSCONV_OK;
 }
 
-#define CAPSCONV_PROLOGUE(OP, A, B_, OUT)                                                                     \
-    Problem p;                                                                                                \
-    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p);           \
-    if (st) return st;                                                                                        \
-    if (!(A) || !(B_) || !(OUT)) return fail(CAPSCONV_ERR_NULL, "a tensor pointer is NULL");                  \
-    const size_t need = workspace_for(OP, p);                                                                 \
-    if (workspace_bytes < need)                                                                               \
-        return fail(CAPSCONV_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);     \
-    if (need && !workspace) return fail(CAPSCONV_ERR_NULL, "workspace is NULL but %zu bytes are required", need); \
-    st = check_device();                                                                                      \
-    if (st) return st;                                                                                        \
-    cudaStream_t cs = (cudaStream_t)stream;                                                                   \
-    const bool mma = choose_path(OP, p) == CAPSCONV_PATH_MMA && aligned16(A) && aligned16(B_) &&             \
-                     aligned16(OUT) && (need == 0 || aligned16(workspace));
+capsconv_status_t capsconv_workspace_bytes_ex(capsconv_op_t op, capsconv_dtype_t dt, capsconv_layout_t layout,
+                                              int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t KH,
+                                              int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
+                                              int64_t pad, size_t *bytes) {
+    if (!bytes) return fail(CAPSCONV_ERR_NULL, "bytes pointer is NULL");
+    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
+    Problem p;
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p, (int)layout);
+    if (st) return st;
+    *bytes = workspace_for(op, p);
+    return CAPSCONV_OK;
+}
+
+capsconv_status_t capsconv_select_path_ex(capsconv_op_t op, capsconv_dtype_t dt, capsconv_layout_t layout, int64_t B,
+                                          int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t KH, int64_t KW,
+                                          int64_t D1, int64_t D2, int64_t D3, int64_t stride, int64_t pad,
+                                          capsconv_path_t *path) {
+    if (!path) return fail(CAPSCONV_ERR_NULL, "path pointer is NULL");
+    if (op < CAPSCONV_OP_FWD || op > CAPSCONV_OP_BWD_KERNEL) return fail(CAPSCONV_ERR_DTYPE, "unknown op %d", (int)op);
+    Problem p;
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p, (int)layout);
+    if (st) return st;
+    *path = choose_path(op, p);
+    return CAPSCONV_OK;
+}
+
+// Validation (all of it before any launch), then the path dispatch.
+static capsconv_status_t run_op(capsconv_op_t op, capsconv_dtype_t dt, capsconv_layout_t layout, int64_t B,
+                                int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1,
+                                int64_t D2, int64_t D3, int64_t stride, int64_t pad, const void *a, const void *b,
+                                void *out, void *workspace, size_t workspace_bytes, capsconv_stream_t stream,
+                                const char *what) {
+    Problem p;
+    capsconv_status_t st = make_problem(dt, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, &p, (int)layout);
+    if (st) return st;
+    if (!a || !b || !out) return fail(CAPSCONV_ERR_NULL, "a tensor pointer is NULL");
+    const size_t need = workspace_for(op, p);
+    if (workspace_bytes < need)
+        return fail(CAPSCONV_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+    if (need && !workspace) return fail(CAPSCONV_ERR_NULL, "workspace is NULL but %zu bytes are required", need);
+    st = check_device();
+    if (st) return st;
+    return finish(dispatch(op, p, a, b, out, workspace, workspace_bytes, (cudaStream_t)stream), what);
+}
+
+capsconv_status_t capsconv_fwd_ex(capsconv_dtype_t dt, capsconv_layout_t layout, int64_t B, int64_t H, int64_t W,
+                                  int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
+                                  int64_t stride, int64_t pad, const void *I, const void *K, void *O, void *workspace,
+                                  size_t workspace_bytes, capsconv_stream_t stream) {
+    return run_op(CAPSCONV_OP_FWD, dt, layout, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, I, K, O, workspace,
+                  workspace_bytes, stream, "capsconv_fwd");
+}
+
+capsconv_status_t capsconv_bwd_data_ex(capsconv_dtype_t dt, capsconv_layout_t layout, int64_t B, int64_t H,
+                                       int64_t W, int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1,
+                                       int64_t D2, int64_t D3, int64_t stride, int64_t pad, const void *dO,
+                                       const void *K, void *dI, void *workspace, size_t workspace_bytes,
+                                       capsconv_stream_t stream) {
+    return run_op(CAPSCONV_OP_BWD_DATA, dt, layout, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, dO, K, dI,
+                  workspace, workspace_bytes, stream, "capsconv_bwd_data");
+}
+
+capsconv_status_t capsconv_bwd_kernel_ex(capsconv_dtype_t dt, capsconv_layout_t layout, int64_t B, int64_t H,
+                                         int64_t W, int64_t C, int64_t Cout, int64_t KH, int64_t KW, int64_t D1,
+                                         int64_t D2, int64_t D3, int64_t stride, int64_t pad, const void *I,
+                                         const void *dO, float *dK, void *workspace, size_t workspace_bytes,
+                                         capsconv_stream_t stream) {
+    return run_op(CAPSCONV_OP_BWD_KERNEL, dt, layout, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, I, dO, dK,
+                  workspace, workspace_bytes, stream, "capsconv_bwd_kernel");
+}
 
 capsconv_status_t capsconv_fwd_pad(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
                                    int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3, int64_t stride,
                                    int64_t pad, const void *I, const void *K, void *O, void *workspace,
                                    size_t workspace_bytes, capsconv_stream_t stream) {
-    CAPSCONV_PROLOGUE(CAPSCONV_OP_FWD, I, K, O)
-    cudaError_t e = mma ? mma_fwd(p, I, K, O, workspace, workspace_bytes, cs) : simt_fwd(p, I, K, O, cs);
-    return finish(e, "capsconv_fwd");
+    return capsconv_fwd_ex(dt, CAPSCONV_LAYOUT_NATURAL, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, I, K, O,
+                           workspace, workspace_bytes, stream);
 }
 
 capsconv_status_t capsconv_fwd(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
@@ -295,10 +431,8 @@ capsconv_status_t capsconv_bwd_data_pad(capsconv_dtype_t dt, int64_t B, int64_t 
                                         int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
                                         int64_t stride, int64_t pad, const void *dO, const void *K, void *dI,
                                         void *workspace, size_t workspace_bytes, capsconv_stream_t stream) {
-    CAPSCONV_PROLOGUE(CAPSCONV_OP_BWD_DATA, dO, K, dI)
-    cudaError_t e =
-        mma ? mma_bwd_data(p, dO, K, dI, workspace, workspace_bytes, cs) : simt_bwd_data(p, dO, K, dI, cs);
-    return finish(e, "capsconv_bwd_data");
+    return capsconv_bwd_data_ex(dt, CAPSCONV_LAYOUT_NATURAL, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, dO, K,
+                                dI, workspace, workspace_bytes, stream);
 }
 
 capsconv_status_t capsconv_bwd_data(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Cout,
@@ -313,10 +447,8 @@ capsconv_status_t capsconv_bwd_kernel_pad(capsconv_dtype_t dt, int64_t B, int64_
                                           int64_t Cout, int64_t KH, int64_t KW, int64_t D1, int64_t D2, int64_t D3,
                                           int64_t stride, int64_t pad, const void *I, const void *dO, float *dK,
                                           void *workspace, size_t workspace_bytes, capsconv_stream_t stream) {
-    CAPSCONV_PROLOGUE(CAPSCONV_OP_BWD_KERNEL, I, dO, dK)
-    cudaError_t e = mma ? mma_bwd_kernel(p, I, dO, dK, workspace, workspace_bytes, cs)
-                        : simt_bwd_kernel(p, I, dO, dK, workspace, workspace_bytes, cs);
-    return finish(e, "capsconv_bwd_kernel");
+    return capsconv_bwd_kernel_ex(dt, CAPSCONV_LAYOUT_NATURAL, B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad, I,
+                                  dO, dK, workspace, workspace_bytes, stream);
 }
 
 capsconv_status_t capsconv_bwd_kernel(capsconv_dtype_t dt, int64_t B, int64_t H, int64_t W, int64_t C,

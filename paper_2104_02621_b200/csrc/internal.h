@@ -17,6 +17,7 @@ struct Problem {
     int64_t B, H, W, C, Cout, KH, KW, D1, D2, D3, s;
     int64_t pad;   // symmetric zero padding of H and W (0: the paper's valid convolution)
     int64_t Ho, Wo;
+    int layout = CAPSCONV_LAYOUT_NATURAL;   // capsconv_layout_t of I, dI, O, dO
 
     size_t elem() const { return dt == CAPSCONV_BF16 ? 2 : 4; }
     int64_t n_in() const { return B * H * W * C * D1 * D2; }
@@ -118,6 +119,24 @@ cudaError_t mma_bwd_data(const Problem &p, const void *dO, const void *K, void *
                          void *ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t mma_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK,
                            void *ws, size_t ws_bytes, cudaStream_t st);
+
+// D1-outer ("rows") layout: tcgen05 kernels fed by TMA only (rows_*.cu)
+bool rows_wgrad_supported(const Problem &p);
+size_t rows_wgrad_workspace_bytes(const Problem &p);
+cudaError_t rows_wgrad_run(const Problem &p, const void *I, const void *dO, float *dK, void *ws, size_t ws_bytes,
+                           cudaStream_t st);
+bool rows_conv_supported(capsconv_op_t op, const Problem &p);
+size_t rows_conv_workspace_bytes(capsconv_op_t op, const Problem &p);
+cudaError_t rows_conv_run(capsconv_op_t op, const Problem &p, const void *src, const void *K, void *out, void *ws,
+                          size_t ws_bytes, cudaStream_t st);
+bool rows_fc_supported(capsconv_op_t op, const Problem &p);
+size_t rows_fc_workspace_bytes(capsconv_op_t op, const Problem &p);
+cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const void *b, void *out, void *ws,
+                        size_t ws_bytes, cudaStream_t st);
+// capsule-row permutation between the layouts: [npix][C][D1][D2] <-> [npix][D1][C][D2]
+// (to_rows = 1: natural -> rows).  Used by the rows-layout fallback path.
+cudaError_t permute_layout(capsconv_dtype_t dt, const void *src, void *dst, int64_t npix, int64_t C, int64_t D1,
+                           int64_t D2, int to_rows, cudaStream_t st);
 
 // tcgen05 kernel gradient (wgrad.cu)
 bool wgrad_supported(const Problem &p);

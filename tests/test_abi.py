@@ -136,3 +136,29 @@ def test_python_binding_refuses_cpu_tensors(cc):
     K = torch.zeros(4, 4, 1, 1, 3, 3)
     with pytest.raises(ValueError):
         cc.fwd(I, K, 1)
+
+
+def test_layout_argument(cc):
+    """capsconv_*_ex: an unknown layout is CAPSCONV_ERR_DTYPE before anything
+    else; both layouts have a path for every valid problem, and the rows
+    layout's fallback reserves workspace for its two permuted copies."""
+    lib = _raw(cc)
+    fake = ctypes.c_void_p(0x1000)
+    ext12 = EXT_OK + (0,)
+    for fn in (lib.capsconv_fwd_ex, lib.capsconv_bwd_data_ex, lib.capsconv_bwd_kernel_ex):
+        fn.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_int64] * 12 + [ctypes.c_void_p] * 4 + \
+            [ctypes.c_size_t, ctypes.c_void_p]
+        assert fn(1, 2, *ext12, fake, fake, fake, None, 0, None) == 4
+        assert b"layout" in lib.capsconv_last_error()
+    for op in (cc.OP_FWD, cc.OP_BWD_DATA, cc.OP_BWD_KERNEL):
+        for dt in (torch.float32, torch.bfloat16):
+            for ext in [(64, 32, 32, 8, 8, 3, 3, 4, 4, 4, 1), (3, 7, 5, 3, 2, 2, 3, 2, 5, 3, 3)]:
+                assert cc.select_path(op, dt, ext, "rows") in (cc.PATH_SIMT, cc.PATH_MMA)
+    # fp32 rows problems run the natural path between permutations
+    ext = (2, 9, 9, 3, 5, 3, 3, 4, 4, 4, 1)
+    nat = cc.workspace_bytes(cc.OP_FWD, torch.float32, ext)
+    rows = cc.workspace_bytes(cc.OP_FWD, torch.float32, ext, "rows")
+    n_in, n_out = 2 * 9 * 9 * 3 * 16 * 4, 2 * 7 * 7 * 5 * 16 * 4
+    assert rows >= nat + n_in + n_out
+    with pytest.raises(ValueError):
+        cc.workspace_bytes(cc.OP_FWD, torch.float32, ext, "columns")

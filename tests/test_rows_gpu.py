@@ -1,0 +1,138 @@
+"""GPU parity of the D1-outer ("rows") layout: libcapsconv through its C ABI
+(capsconv_*_ex, layout CAPSCONV_LAYOUT_ROWS) against the CPU oracle.
+
+Inputs are generated in the natural layout (capsinputs), permuted to
+(B, H, W, D1, C, D2) for the call and the results permuted back, so the
+oracle is untouched.  The rows layout runs its own TMA-fed tensor-core
+kernels where they apply (bf16, 4x4 capsules) and the natural path between
+two permutations otherwise; both are covered.  Full-size stack layers are
+checked bit-exactly on exact-integer inputs (every sum is an integer below
+2^24, bf16 outputs must equal RNE_bf16(exact))."""
+import numpy as np
+import pytest
+import torch
+
+import capsinputs
+from helpers import TOL, assert_close, to_np
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def cc():
+    from paper_2104_02621_b200 import _build
+    _build.build()
+    import paper_2104_02621_b200.capsconv as cc
+    cc.load_library()
+    yield cc
+    cc.set_path_override(cc.PATH_AUTO)
+
+
+def to_rows(t):      # natural (B,H,W,C,D1,D2) -> rows (B,H,W,D1,C,D2)
+    return t.permute(0, 1, 2, 4, 3, 5).contiguous()
+
+
+def from_rows(t):    # rows -> natural
+    return t.permute(0, 1, 2, 4, 3, 5).contiguous()
+
+
+def run_rows(cc, L, I, K, dO):
+    Id, Kd, dOd = to_rows(I.to(DEV)), K.to(DEV), to_rows(dO.to(DEV))
+    O = cc.fwd(Id, Kd, L.stride, layout="rows")
+    dI = cc.bwd_data(dOd, Kd, L.stride, L.H, L.W, layout="rows")
+    dK = cc.bwd_kernel(Id, dOd, L.stride, L.KH, L.KW, layout="rows")
+    torch.cuda.synchronize()
+    return from_rows(O), from_rows(dI), dK
+
+
+def ext_of(L):
+    return (L.B, L.H, L.W, L.C, L.Cout, L.KH, L.KW, L.D1, L.D2, L.D3, L.stride)
+
+
+SMALL = [
+    # B, H, W, C, Cout, KH, KW, D1, D2, D3, s
+    (2, 9, 11, 4, 8, 3, 3, 4, 4, 4, 1),
+    (3, 10, 9, 8, 8, 3, 3, 4, 4, 4, 2),
+    (2, 8, 8, 32, 12, 8, 8, 4, 4, 4, 1),
+    (1, 12, 40, 8, 8, 3, 3, 4, 4, 4, 1),
+    (5, 7, 7, 16, 32, 3, 3, 4, 4, 4, 2),
+    (3, 13, 6, 4, 16, 2, 3, 4, 4, 4, 3),
+    (2, 6, 5, 2, 3, 2, 3, 2, 3, 5, 1),
+    (4, 11, 11, 8, 16, 1, 1, 4, 4, 4, 1),
+    (2, 34, 17, 8, 8, 3, 3, 4, 4, 4, 1),
+    (3, 12, 12, 16, 16, 5, 5, 4, 4, 4, 1),
+    (2, 9, 9, 8, 4, 3, 3, 4, 4, 4, 1),
+]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+def test_rows_small_random(cc, oracle_mod, case, dtype):
+    L = capsinputs.Layer(*case)
+    I = capsinputs.make_input(L, "uniform", dtype)
+    K = capsinputs.make_kernel(L, "uniform", dtype)
+    Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "uniform", dtype)
+    O, dI, dK = run_rows(cc, L, I, K, dO)
+    rO, aO = oracle_mod.fwd(to_np(I), to_np(K), L.stride)
+    rdI, adI = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
+    rdK, adK = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
+    assert_close(to_np(O), rO, aO, dtype, "rows fwd")
+    assert_close(to_np(dI), rdI, adI, dtype, "rows bwd_data")
+    assert_close(to_np(dK), rdK, adK, torch.float32, "rows bwd_kernel")
+
+
+@pytest.mark.parametrize("case", SMALL[:6], ids=lambda c: "x".join(map(str, c)))
+def test_rows_small_exact(cc, oracle_mod, case):
+    """Exact-integer bf16 inputs: bitwise (order-independent sums)."""
+    L = capsinputs.Layer(*case)
+    dt = torch.bfloat16
+    I = capsinputs.make_input(L, "int", dt)
+    K = capsinputs.make_kernel(L, "int", dt)
+    Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "int", dt)
+    O, dI, dK = run_rows(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), L.stride)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
+
+
+def _stack_layers():
+    import oracle
+    return capsinputs.stack_layers(capsinputs.STACK_BATCH, oracle.output_dims)
+
+
+@pytest.mark.parametrize("li", [0, 1, 2, 3], ids=["L1", "L2", "L3", "FC"])
+def test_rows_stack_layers_full_batch_exact(cc, oracle_mod, li):
+    """Each config-5 stack layer at batch 1024 in the rows layout (the launch
+    configuration bench.py times), exact-integer inputs in {-1, 0, 1}."""
+    L = _stack_layers()[li]
+    dt = torch.bfloat16
+    I = capsinputs.make_input(L, "int1", dt, layer_idx=li)
+    K = capsinputs.make_kernel(L, "int1", dt, layer_idx=li)
+    Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "int1", dt, layer_idx=li)
+    O, dI, dK = run_rows(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), L.stride)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
+    assert np.abs(rdK).max() < 2 ** 24
+    if li < 3:
+        assert cc.select_path(cc.OP_BWD_KERNEL, dt, ext_of(L), "rows") == cc.PATH_MMA
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
+
+
+def test_rows_deterministic(cc):
+    L = _stack_layers()[0]
+    I = to_rows(capsinputs.make_input(L, dtype=torch.bfloat16).to(DEV))
+    dO = torch.randn(L.B, 22, 22, 4, L.Cout, 4, device=DEV).to(torch.bfloat16)
+    a = cc.bwd_kernel(I, dO, 1, 3, 3, layout="rows")
+    b = cc.bwd_kernel(I, dO, 1, 3, 3, layout="rows")
+    assert torch.equal(a, b)
