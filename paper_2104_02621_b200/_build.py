@@ -13,6 +13,10 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libcapsconv.so")
+# probe flavour (tests/probe/ only): same sources with -DCAPSCONV_PROBES, which
+# compiles in the diagnostic knobs (skip switches, planner overrides, traces)
+PROBE_LIB = os.path.join(PKG, "libcapsconv_probe.so")
+PROBE_BUILD = os.path.join(PKG, "build_probe")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -29,16 +33,16 @@ def _deps():
         [os.path.join(INCLUDE, "capsconv.h"), os.path.abspath(__file__)]
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+def _compile(src: str, verbose: bool, probes: bool = False) -> str:
+    obj = os.path.join(PROBE_BUILD if probes else BUILD, os.path.basename(src) + ".o")
+    cmd = [NVCC] + ARCH + FLAGS + (["-DCAPSCONV_PROBES"] if probes else []) + ["-c", src, "-o", obj]
     if src.endswith(".cu") and verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -49,24 +53,26 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every CUDA / C++ source under csrc/ and link libcapsconv.so."""
-    if not force and not needs_build():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, probes: bool = False) -> str:
+    """Compile every CUDA / C++ source under csrc/ and link libcapsconv.so
+    (probes=True: the diagnostic flavour libcapsconv_probe.so)."""
+    lib = PROBE_LIB if probes else LIB
+    if not force and not needs_build(lib):
+        return lib
+    os.makedirs(PROBE_BUILD if probes else BUILD, exist_ok=True)
     srcs = _sources()
     with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    tmp = LIB + ".tmp.%d" % os.getpid()
+        objs = list(ex.map(lambda s: _compile(s, verbose, probes), srcs))
+    tmp = lib + ".tmp.%d" % os.getpid()
     # -fvisibility=hidden + extern "C" with default visibility (see capsconv.h users):
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, probes="--probes" in sys.argv))

@@ -89,7 +89,74 @@ struct RowsWgrad {
     int nstg;
     uint32_t smem_bytes;
     long long nK;
+    int dbg;                       // probe builds only: 1 skip MMAs, 2 skip TMA loads, 4 skip the k-loop
 };
+
+// MMA issue of one work item: NG accumulator groups, descriptors built once
+// per item and advanced by constant offsets (descriptor units of 16 bytes),
+// so every operand lives in uniform registers; two k-steps per elected region.
+template <int NG>
+__device__ __forceinline__ void rw_mma_item(const RowsWgrad &P, const RwSet &S, uint32_t stg0, uint64_t *full,
+                                            uint64_t *empty, int t0, int t1, int &sb, uint32_t &ph) {
+    uint64_t ad[NG], bd[NG];
+    uint32_t dc[NG], id[NG];
+    const int ng = min(NG, S.ngroups);
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const RwGroup &G = S.g[g < ng ? g : 0];
+        ad[g] = rows::sdesc(stg0 + S.buf[G.ibuf].off + (uint32_t)(G.p0 * P.Wpb + G.acol) * P.pxA, P.lboA, P.sboA,
+                            2 * P.Ea);
+        bd[g] = rows::sdesc(stg0 + S.buf[G.obuf].off, P.lboB, P.sboB, 2 * P.Eb);
+        dc[g] = G.dcol;
+        id[g] = G.idesc;
+    }
+    const uint32_t rowa = ((uint32_t)(P.s * P.Wpb) * P.pxA) >> 4;   // one output row, A
+    const uint32_t rowb = ((uint32_t)P.Wv * P.pxO) >> 4;
+    const uint32_t ka = P.pxA >> 2, kb = P.pxO >> 2;                  // one k-step = 4 pixels
+    const uint32_t sstr = P.stage_stride >> 4;
+    const int nkx = P.nkx;
+    uint32_t acc = 0;
+    for (int t = t0; t < t1; ++t) {
+        const int img = t / P.nYst, Y0 = (t - img * P.nYst) * P.R;
+        const int Reff = min(P.R, P.Ho - Y0);
+        mbar_wait(full + sb, ph);
+        fence_after_sync();
+        const uint32_t so = (uint32_t)sb * sstr;
+        if (!(kProbes && (P.dbg & 4))) {
+            for (int yl = 0; yl < Reff; ++yl) {
+                const uint32_t oa0 = so + (uint32_t)yl * rowa, ob0 = so + (uint32_t)yl * rowb;
+                int kx = 0;
+                for (; kx + 2 <= nkx; kx += 2) {
+                    if (!(kProbes && (P.dbg & 1)) && elect_one()) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const uint32_t oa = oa0 + (uint32_t)(kx + u) * ka, ob = ob0 + (uint32_t)(kx + u) * kb;
+#pragma unroll
+                            for (int g = 0; g < NG; ++g)
+                                if (g < ng)
+                                    rows::mma_ss(dc[g], ad[g] + oa, bd[g] + ob, id[g], (acc | (uint32_t)u));
+                        }
+                    }
+                    __syncwarp();
+                    acc = 1;
+                }
+                if (kx < nkx) {
+                    if (!(kProbes && (P.dbg & 1)) && elect_one()) {
+                        const uint32_t oa = oa0 + (uint32_t)kx * ka, ob = ob0 + (uint32_t)kx * kb;
+#pragma unroll
+                        for (int g = 0; g < NG; ++g)
+                            if (g < ng) rows::mma_ss(dc[g], ad[g] + oa, bd[g] + ob, id[g], acc);
+                    }
+                    __syncwarp();
+                    acc = 1;
+                }
+            }
+        }
+        if (elect_one()) mma_commit(empty + sb);
+        __syncwarp();
+        if (++sb == P.nstg) { sb = 0; ph ^= 1; }
+    }
+}
 
 __global__ void __launch_bounds__(kRwThreads, 1) rows_wgrad_kernel(const __grid_constant__ RowsWgrad P) {
     pdl_launch_dependents();
@@ -133,6 +200,11 @@ __global__ void __launch_bounds__(kRwThreads, 1) rows_wgrad_kernel(const __grid_
                     mbar_wait(empty + sb, ph ^ 1);
                     const uint32_t stg = stg0 + (uint32_t)sb * P.stage_stride;
                     const uint32_t mb = smem_u32(full + sb);
+                    if (kProbes && (P.dbg & 2)) {
+                        mbar_arrive(full + sb);
+                        if (++sb == P.nstg) { sb = 0; ph ^= 1; }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(full + sb, S.stage_bytes);
                     for (int i = 0; i < S.nbufs; ++i) {
                         const RwBuf &bf = S.buf[i];
@@ -157,34 +229,12 @@ __global__ void __launch_bounds__(kRwThreads, 1) rows_wgrad_kernel(const __grid_
             const int t1 = (int)((long long)(ks + 1) * P.n_st / P.ksplit);
             mbar_wait(acc_empty, aph ^ 1);
             fence_after_sync();
-            uint32_t acc = 0;
-            for (int t = t0; t < t1; ++t) {
-                const int img = t / P.nYst, Y0 = (t - img * P.nYst) * P.R;
-                const int Reff = min(P.R, P.Ho - Y0);
-                mbar_wait(full + sb, ph);
-                fence_after_sync();
-                const uint32_t stg = stg0 + (uint32_t)sb * P.stage_stride;
-                for (int yl = 0; yl < Reff; ++yl) {
-                    for (int kx = 0; kx < P.nkx; ++kx) {
-                        const uint32_t offa = (uint32_t)((P.s * yl) * P.Wpb + 4 * kx) * P.pxA;
-                        const uint32_t offb = (uint32_t)(yl * P.Wv + 4 * kx) * P.pxO;
-                        if (elect_one()) {
-                            for (int g = 0; g < S.ngroups; ++g) {
-                                const RwGroup &G = S.g[g];
-                                const uint32_t a = stg + S.buf[G.ibuf].off + offa +
-                                                   (uint32_t)(G.p0 * P.Wpb + G.acol) * P.pxA;
-                                const uint32_t b = stg + S.buf[G.obuf].off + offb;
-                                rows::mma_ss(tmem + G.dcol, rows::sdesc(a, P.lboA, P.sboA, 2 * P.Ea),
-                                             rows::sdesc(b, P.lboB, P.sboB, 2 * P.Eb), G.idesc, acc);
-                            }
-                        }
-                        __syncwarp();
-                        acc = 1;
-                    }
-                }
-                if (elect_one()) mma_commit(empty + sb);
-                __syncwarp();
-                if (++sb == P.nstg) { sb = 0; ph ^= 1; }
+            switch (S.ngroups) {
+                case 1: rw_mma_item<1>(P, S, stg0, full, empty, t0, t1, sb, ph); break;
+                case 2: rw_mma_item<2>(P, S, stg0, full, empty, t0, t1, sb, ph); break;
+                case 3: rw_mma_item<3>(P, S, stg0, full, empty, t0, t1, sb, ph); break;
+                case 4: rw_mma_item<4>(P, S, stg0, full, empty, t0, t1, sb, ph); break;
+                default: rw_mma_item<8>(P, S, stg0, full, empty, t0, t1, sb, ph); break;
             }
             if (elect_one()) mma_commit(acc_full);
             __syncwarp();
@@ -236,19 +286,38 @@ __global__ void __launch_bounds__(kRwThreads, 1) rows_wgrad_kernel(const __grid_
     if (warp == 1) tmem_dealloc_dyn(0u, 512);
 }
 
-// dK[e] = sum_k part[k][e], fixed order (float4 per thread).
-__global__ void rw_finalize(const float *__restrict__ part, float *__restrict__ dK, long long n4, long long nK,
-                            int ksplit) {
+// dK[e] = sum_k part[k][e] in a fixed order: a block owns 32 float4 columns;
+// warp w sums splits w, w + 16, w + 32, ... (independent loads in flight),
+// then the 16 warp partials are added in warp order.  Deterministic.
+constexpr int kFinWarps = 16;
+__global__ void __launch_bounds__(kFinWarps * 32) rw_finalize(const float *__restrict__ part, float *__restrict__ dK,
+                                                              long long n4, long long nK, int ksplit) {
     pdl_launch_dependents();
     pdl_wait();
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n4) return;
-    float4 acc = reinterpret_cast<const float4 *>(part)[i];
-    for (int k = 1; k < ksplit; ++k) {
-        const float4 v = reinterpret_cast<const float4 *>(part + (size_t)k * (size_t)nK)[i];
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    __shared__ float4 red[kFinWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long i = (long long)blockIdx.x * 32 + lane;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n4) {
+        const float4 *p = reinterpret_cast<const float4 *>(part) + i;
+        const long long st4 = nK / 4;
+        int k = w;
+#pragma unroll 4
+        for (; k < ksplit; k += kFinWarps) {
+            const float4 v = __ldg(p + (size_t)k * (size_t)st4);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
     }
-    reinterpret_cast<float4 *>(dK)[i] = acc;
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && i < n4) {
+        float4 r = red[0][lane];
+        for (int j = 1; j < kFinWarps; ++j) {
+            const float4 v = red[j][lane];
+            r.x += v.x; r.y += v.y; r.z += v.z; r.w += v.w;
+        }
+        reinterpret_cast<float4 *>(dK)[i] = r;
+    }
 }
 
 struct RwPlan {
@@ -365,7 +434,8 @@ RwPlan make_rw_plan(const Problem &p) {
     };
     int best_R = 0, best_nstg = 0;
     uint32_t best_stride = 0;
-    for (int nstg = 3; nstg >= 1 && !best_R; --nstg) {
+    const int force_nstg = probe_env("CAPSCONV_RW_NSTG") ? atoi(probe_env("CAPSCONV_RW_NSTG")) : 0;
+    for (int nstg = force_nstg ? force_nstg : 3; nstg >= 1 && !best_R; --nstg) {
         for (int R = std::min(P.Ho, 64); R >= 1; --R) {
             const int rowsI = s * (R - 1) + KH;
             if (rowsI > 256 || R > 256) continue;
@@ -450,6 +520,7 @@ cudaError_t rows_wgrad_run(const Problem &p, const void *I, const void *dO, floa
         !rows::make_rows_map5(&P.tmO, dO, P.B, P.Ho, P.Wo, 4 * P.Cout, P.Eb, P.Wv, P.R, 1, 1))
         return cudaErrorInvalidValue;
     P.part = P.ksplit > 1 ? static_cast<float *>(ws) : dK;
+    P.dbg = probe_env("CAPSCONV_RW_DBG") ? atoi(probe_env("CAPSCONV_RW_DBG")) : 0;
     cudaError_t e = smem_optin(reinterpret_cast<const void *>(rows_wgrad_kernel), (int)P.smem_bytes);
     if (e != cudaSuccess) return e;
     const int grid = std::min(P.n_items, device_info().num_sms);
@@ -458,7 +529,7 @@ cudaError_t rows_wgrad_run(const Problem &p, const void *I, const void *dO, floa
     note_launches(1);
     if (P.ksplit > 1) {
         const long long n4 = P.nK / 4;
-        e = launch_k(rw_finalize, dim3((unsigned)((n4 + 255) / 256)), dim3(256), 0, st,
+        e = launch_k(rw_finalize, dim3((unsigned)((n4 + 31) / 32)), dim3(kFinWarps * 32), 0, st,
                      static_cast<const float *>(P.part), dK, n4, P.nK, P.ksplit);
         if (e != cudaSuccess) return e;
         note_launches(1);
