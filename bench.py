@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce on the compute stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
+    ap.add_argument("--layout", default="rows", choices=["rows", "natural"],
+                    help="capsule-tensor layout of the stack's activations (include/capsconv.h)")
     return ap.parse_args()
 
 
@@ -307,13 +309,17 @@ def main():
         h, w = pkg.output_dims(h, w, sp.KH, sp.KW, sp.stride, sp.pad)
     L0 = capsinputs.Layer(B=gbatch, H=H, W=W, C=specs[0].C, Cout=specs[0].Cout, KH=specs[0].KH, KW=specs[0].KW,
                           D1=D, D2=D, D3=D, stride=specs[0].stride)
-    X_host = capsinputs.make_input(L0, dtype=dtype, batch_offset=lo, batch=batch).pin_memory()
+    X_host = capsinputs.make_input(L0, dtype=dtype, batch_offset=lo, batch=batch)
     dY_host = capsinputs.make_grad_output((gbatch, h, w, specs[-1].Cout, D, D), dtype=dtype, layer_idx=len(specs),
-                                          batch_offset=lo, batch=batch).pin_memory()
+                                          batch_offset=lo, batch=batch)
+    if args.layout == "rows":   # the same synthetic tensors stored D1-outer: (B, H, W, D1, C, D2)
+        X_host = X_host.permute(0, 1, 2, 4, 3, 5).contiguous()
+        dY_host = dY_host.permute(0, 1, 2, 4, 3, 5).contiguous()
+    X_host, dY_host = X_host.pin_memory(), dY_host.pin_memory()
     X = X_host.to(dev)
     dY = dY_host.to(dev)
 
-    st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap)
+    st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap, layout=args.layout)
     gflops = st.step_flops(batch=gbatch)          # whole-job algorithmic flops per step
     peaks = load_peaks()
 
@@ -502,6 +508,7 @@ def main():
                        "layers": ["%dx%d s%d%s %d->%d" % (s.KH, s.KW, s.stride, " p%d" % s.pad if s.pad else "", s.C,
                                                           s.Cout) for s in specs],
                        "input": "%dx%dx%d capsules %dx%d" % (H, W, specs[0].C, D, D),
+                       "layout": args.layout,
                        "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
                        "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None,
                        "launch": ("one CUDA-graph replay of the captured step (%d libcapsconv kernels)" % launches_per_step)

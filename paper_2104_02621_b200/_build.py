@@ -42,7 +42,8 @@ def needs_build(lib: str = LIB) -> bool:
 
 def _compile(src: str, verbose: bool, probes: bool = False) -> str:
     obj = os.path.join(PROBE_BUILD if probes else BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC] + ARCH + FLAGS + (["-DCAPSCONV_PROBES"] if probes else []) + ["-c", src, "-o", obj]
+    extra = os.environ.get("CAPSCONV_EXTRA_FLAGS", "").split() if probes else []
+    cmd = [NVCC] + ARCH + FLAGS + (["-DCAPSCONV_PROBES"] if probes else []) + extra + ["-c", src, "-o", obj]
     if src.endswith(".cu") and verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

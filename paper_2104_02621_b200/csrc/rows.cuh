@@ -51,6 +51,15 @@ __device__ __forceinline__ void tma_load5d(uint32_t dst, const CUtensorMap *m, i
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(mbar)
         : "memory");
 }
+// 4-D tile load over a merged-row view (E, 4, Ws, B*Hs).
+__device__ __forceinline__ void tma_load4d_rows(uint32_t dst, const CUtensorMap *m, int c0, int c1, int c2, int c3,
+                                                uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load3d(uint32_t dst, const CUtensorMap *m, int c0, int c1, int c2,
                                            uint32_t mbar) {
     asm volatile(
@@ -72,6 +81,24 @@ __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, 
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// The same MMA issued by one elected lane of a converged warp: the whole
+// warp runs the (uniform) issue loop, so descriptors stay in uniform
+// registers and each MMA costs an elect + a predicated UTCHMMA.
+__device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_ld16x(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -100,6 +127,11 @@ bool make_rows_map5(CUtensorMap *map, const void *base, int64_t B, int64_t Hs, i
 //   map2: a row-major [rows][E] bf16 matrix, box (ce, br), swizzle 2*ce bytes
 //         (ce = 16/32/64), or no swizzle when swz == 0 (then ce*2 must be 16).
 bool make_rows_map2(CUtensorMap *map, const void *base, int64_t rows, int64_t E, int ce, int br, int swz);
+//   map4m: dims (E, 4, Ws, rows) -- a rows tensor with all B*Hs pixel rows
+//          merged (dense: image stride = Hs row strides), box (ce, 4, bx, by),
+//          element strides (1, 1, es, es)
+bool make_rows_map4m(CUtensorMap *map, const void *base, int64_t rows, int64_t Ws, int64_t E, int ce, int bx, int by,
+                     int es);
 //   map4: dims (E, 4, P, B) -- a rows tensor viewed with all P = H*W pixels of
 //         an image flattened -- box (ce, 4, 1, bb): one pixel position of bb
 //         images (the fully-connected view, R18).

@@ -125,29 +125,13 @@ __device__ __forceinline__ void rw_mma_item(const RowsWgrad &P, const RwSet &S, 
         if (!(kProbes && (P.dbg & 4))) {
             for (int yl = 0; yl < Reff; ++yl) {
                 const uint32_t oa0 = so + (uint32_t)yl * rowa, ob0 = so + (uint32_t)yl * rowb;
-                int kx = 0;
-                for (; kx + 2 <= nkx; kx += 2) {
-                    if (!(kProbes && (P.dbg & 1)) && elect_one()) {
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const uint32_t oa = oa0 + (uint32_t)(kx + u) * ka, ob = ob0 + (uint32_t)(kx + u) * kb;
-#pragma unroll
-                            for (int g = 0; g < NG; ++g)
-                                if (g < ng)
-                                    rows::mma_ss(dc[g], ad[g] + oa, bd[g] + ob, id[g], (acc | (uint32_t)u));
-                        }
-                    }
-                    __syncwarp();
-                    acc = 1;
-                }
-                if (kx < nkx) {
-                    if (!(kProbes && (P.dbg & 1)) && elect_one()) {
-                        const uint32_t oa = oa0 + (uint32_t)kx * ka, ob = ob0 + (uint32_t)kx * kb;
+                for (int kx = 0; kx < nkx; ++kx) {
+                    const uint32_t oa = oa0 + (uint32_t)kx * ka, ob = ob0 + (uint32_t)kx * kb;
+                    if (!(kProbes && (P.dbg & 1))) {
 #pragma unroll
                         for (int g = 0; g < NG; ++g)
-                            if (g < ng) rows::mma_ss(dc[g], ad[g] + oa, bd[g] + ob, id[g], acc);
+                            if (g < ng) rows::mma_ss_elect(dc[g], ad[g] + oa, bd[g] + ob, id[g], acc);
                     }
-                    __syncwarp();
                     acc = 1;
                 }
             }

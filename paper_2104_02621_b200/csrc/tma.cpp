@@ -71,6 +71,20 @@ bool make_rows_map5(CUtensorMap *map, const void *base, int64_t B, int64_t Hs, i
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_rows_map4m(CUtensorMap *map, const void *base, int64_t rows, int64_t Ws, int64_t E, int ce, int bx, int by,
+                     int es) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || ce * 2 > 128 || bx > 256 || by > 256 || bx < 1 || by < 1) return false;
+    const cuuint64_t el = 2;
+    cuuint64_t dims[4] = {(cuuint64_t)E, 4, (cuuint64_t)Ws, (cuuint64_t)rows};
+    cuuint64_t strides[3] = {(cuuint64_t)E * el, (cuuint64_t)(4 * E) * el, (cuuint64_t)(Ws * 4 * E) * el};
+    cuuint32_t box[4] = {(cuuint32_t)ce, 4, (cuuint32_t)bx, (cuuint32_t)by};
+    cuuint32_t estr[4] = {1, 1, (cuuint32_t)es, (cuuint32_t)es};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz_enum(ce * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_rows_map2(CUtensorMap *map, const void *base, int64_t rows, int64_t E, int ce, int br, int swz) {
     EncodeTiledFn fn = encode_fn();
     if (!fn || br > 256 || br < 1) return false;

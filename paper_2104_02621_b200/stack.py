@@ -44,10 +44,14 @@ def shard_range(global_batch: int, rank: int, world: int):
 
 class CapsStack:
     def __init__(self, specs: Sequence[LayerSpec], H: int, W: int, D: int, batch: int, weights: List[torch.Tensor],
-                 device, ops=None, group=None, overlap: bool = True):
+                 device, ops=None, group=None, overlap: bool = True, layout: str = "natural"):
         if ops is None:
             from . import capsconv as ops
         self.ops = ops
+        # capsule-tensor layout of the activations and gradients: "natural"
+        # (B,H,W,C,D1,D2) or "rows" (B,H,W,D1,C,D2), see include/capsconv.h
+        self.layout = layout
+        self._lk = {} if layout == "natural" else {"layout": layout}
         self.specs = list(specs)
         self.device = torch.device(device)
         self.dtype = weights[0].dtype
@@ -65,12 +69,12 @@ class CapsStack:
         # static buffers (stable pointers: the step can be captured in a CUDA graph).
         # acts[0] is the caller's input itself when it already has the layer-0
         # layout (no copy); the static buffer is only used otherwise.
-        self.acts = [torch.empty((batch, h, w, sp.C, D, D), dtype=self.dtype, device=self.device)
+        self.acts = [torch.empty(self.caps_shape(batch, h, w, sp.C), dtype=self.dtype, device=self.device)
                      for (h, w), sp in zip(self.hw[:-1], self.specs)]
         self._acts0 = self.acts[0]
         last = self.specs[-1]
         h, w = self.hw[-1]
-        self.out = torch.empty((batch, h, w, last.Cout, D, D), dtype=self.dtype, device=self.device)
+        self.out = torch.empty(self.caps_shape(batch, h, w, last.Cout), dtype=self.dtype, device=self.device)
         self.grads = [torch.empty_like(a) for a in self.acts]           # dI of every layer
         # dK is fp32 for fp32/bf16 operands (libcapsconv's contract); wider
         # operand types (test backends) keep their own precision
@@ -78,6 +82,11 @@ class CapsStack:
         self.dK = [torch.empty(k.shape, dtype=kdt, device=self.device) for k in self.K]
         self.comm_stream = torch.cuda.Stream(self.device) if self.overlap else None
         self.events = [torch.cuda.Event() for _ in self.K] if self.overlap else None
+
+    def caps_shape(self, b, h, w, c):
+        """Shape of a capsule tensor of this stack's layout."""
+        D = self.D
+        return (b, h, w, D, c, D) if self.layout == "rows" else (b, h, w, c, D, D)
 
     # ------------------------------------------------------------ flops / bytes
     def layer_flops(self, li: int, batch: Optional[int] = None) -> int:
@@ -103,7 +112,7 @@ class CapsStack:
         self._bind_input(x)
         for li, sp in enumerate(self.specs):
             dst = self.acts[li + 1] if li + 1 < len(self.specs) else self.out
-            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst, pad=sp.pad)
+            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst, pad=sp.pad, **self._lk)
         return self.out
 
     def backward(self, dy: torch.Tensor, timer=None) -> List[torch.Tensor]:
@@ -113,7 +122,7 @@ class CapsStack:
             sp = self.specs[li]
             h, w = self.hw[li]
             if timer: timer.begin(li, "dK")
-            self.ops.bwd_kernel(self.acts[li], g, sp.stride, sp.KH, sp.KW, out=self.dK[li], pad=sp.pad)
+            self.ops.bwd_kernel(self.acts[li], g, sp.stride, sp.KH, sp.KW, out=self.dK[li], pad=sp.pad, **self._lk)
             if timer: timer.end(li, "dK")
             if self.world > 1:
                 if self.overlap:
@@ -124,7 +133,7 @@ class CapsStack:
                 else:
                     dist.all_reduce(self.dK[li], op=dist.ReduceOp.SUM, group=self.group)
             if timer: timer.begin(li, "dI")
-            self.ops.bwd_data(g, self.K[li], sp.stride, h, w, out=self.grads[li], pad=sp.pad)
+            self.ops.bwd_data(g, self.K[li], sp.stride, h, w, out=self.grads[li], pad=sp.pad, **self._lk)
             if timer: timer.end(li, "dI")
             g = self.grads[li]
         if self.world > 1 and self.overlap:
@@ -139,6 +148,6 @@ class CapsStack:
         for li, sp in enumerate(self.specs):
             dst = self.acts[li + 1] if li + 1 < len(self.specs) else self.out
             timer.begin(li, "fwd")
-            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst, pad=sp.pad)
+            self.ops.fwd(self.acts[li], self.K[li], sp.stride, out=dst, pad=sp.pad, **self._lk)
             timer.end(li, "fwd")
         return self.backward(dy, timer)

@@ -20,7 +20,10 @@ def main():
     layouts = sys.argv[3].split(",") if len(sys.argv) > 3 else ["natural", "rows"]
     if os.environ.get("PROBE"):
         from paper_2104_02621_b200 import _build
-        pkg.load_library(_build.PROBE_LIB)   # diagnostic flavour (-DCAPSCONV_PROBES)
+        lib = _build.PROBE_LIB
+        if os.environ.get("PROBE_LIB"):
+            lib = os.path.join(os.path.dirname(_build.PROBE_LIB), os.environ["PROBE_LIB"])
+        pkg.load_library(lib)   # diagnostic flavour (-DCAPSCONV_PROBES)
     else:
         pkg.load_library()
     dev = "cuda:0"

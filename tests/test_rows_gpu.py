@@ -122,8 +122,9 @@ def test_rows_stack_layers_full_batch_exact(cc, oracle_mod, li):
     rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
     rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
     assert np.abs(rdK).max() < 2 ** 24
-    if li < 3:
-        assert cc.select_path(cc.OP_BWD_KERNEL, dt, ext_of(L), "rows") == cc.PATH_MMA
+    if li < 3:   # the conv layers run the rows-layout tensor-core kernels on every pass
+        for op in (cc.OP_FWD, cc.OP_BWD_DATA, cc.OP_BWD_KERNEL):
+            assert cc.select_path(op, dt, ext_of(L), "rows") == cc.PATH_MMA, op
     np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
     np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
     np.testing.assert_array_equal(to_np(dK), rdK)

@@ -29,8 +29,14 @@ def load_probe():
     lib = ctypes.CDLL(LIB)
     lib.rows_probe.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 10
     lib.rows_probe.restype = ctypes.c_int
-    lib.rows_bench.argtypes = [ctypes.c_int] * 6
+    lib.rows_bench.argtypes = [ctypes.c_int] * 8
     lib.rows_bench.restype = ctypes.c_double
+    lib.sync_bench.argtypes = [ctypes.c_int] * 3
+    lib.sync_bench.restype = ctypes.c_double
+    lib.tile_bench.argtypes = [ctypes.c_int] * 7
+    lib.tile_bench.restype = ctypes.c_double
+    lib.tmem_bw.argtypes = [ctypes.c_int] * 2
+    lib.tmem_bw.restype = ctypes.c_double
     return lib
 
 
@@ -93,12 +99,38 @@ def test_rows_layout(probe, case):
 
 
 if __name__ == "__main__":
+    import sys
     lib = load_probe()
+    if "--sync" in sys.argv:
+        for mode, name in ((0, "commit->wait round trip"), (1, "commit issue"), (2, "mbarrier hand-off x2")):
+            for nb in (1, 148):
+                print("sync %-24s blocks %3d: %.1f cycles" % (name, nb, lib.sync_bench(mode, 2000, nb)))
+        sys.exit(0)
+    if "--tmem" in sys.argv:
+        for nw in (1, 4, 8, 16):
+            print("tmem read nwarps %2d: %.1f bytes/cycle/SM" % (nw, lib.tmem_bw(nw, 2000)))
+        sys.exit(0)
+    if "--tile" in sys.argv:
+        for N in (96, 128):
+            for per in (6, 24):
+                for bmode in (0, 4):
+                    cyc = lib.tile_bench(N, 400, per, 4, 1, 1, bmode)
+                    print("tile N %3d per %2d bmode %d: %.1f cycles/MMA" % (N, per, bmode, cyc))
+        sys.exit(0)
+    if "--align" in sys.argv:
+        for mode, swz in ((0, 64), (2, 64), (2, 128), (1, 64)):
+            for N in (96, 192):
+                for aoff in (0, 256):
+                    for walk in (0, 256):
+                        cyc = lib.rows_bench(mode, swz, N, 4096, 1, 148, aoff, walk)
+                        print("align mode %d swz %3d N %3d aoff %4d walk %4d: %.1f cycles/MMA" % (
+                            mode, swz, N, aoff, walk, cyc))
+        sys.exit(0)
     for c in CASES:
         got, ref = run_case(lib, *c)
         print("case", c, "max |diff| = %.3g" % float((got - ref).abs().max()))
     for mode, swz in ((0, 64), (0, 128), (1, 64), (1, 128)):
         for N in (32, 64, 96, 128, 192, 256):
             for nacc in (1, 2):
-                cyc = lib.rows_bench(mode, swz, N, 4096, nacc, 148)
+                cyc = lib.rows_bench(mode, swz, N, 4096, nacc, 148, 0, 0)
                 print("bench mode %d swz %d N %3d nacc %d: %.1f cycles/MMA" % (mode, swz, N, nacc, cyc))
