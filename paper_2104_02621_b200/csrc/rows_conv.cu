@@ -97,6 +97,7 @@ struct RowsConv {
     int Hout, Wout, Eout;          // output tensor extents, elements per capsule row
     int ngrp;                      // epilogue groups in use (divides nacc: a slot always has one group)
     int pair;                      // MMA warp issues two tiles at a time (nacc == 4)
+    int cstage;                    // one source chunk per pipeline stage (wide K, one tile per item)
     int prog;                      // compile-time MMA program (tap groups x k-steps), see the dispatch
     int dmax;                      // largest lane offset of any output
     int xl;                        // hand-off lanes per quarter (largest sum of an output's deltas)
@@ -178,6 +179,23 @@ __device__ __forceinline__ void rc_issue_u(uint32_t alo, uint32_t ahi, uint32_t 
     }
 }
 
+// Chunk-staged issue: the stage holds one source chunk (kpc k-steps) of the
+// window; its B k-steps start at ks0; the very first MMA overwrites.
+template <int NM, int KPC>
+__device__ __forceinline__ void rc_issue_uc(uint32_t alo, uint32_t ahi, uint32_t dslot, const uint32_t (&aoff)[NM],
+                                            uint32_t blo0, uint32_t bhi, uint32_t bst, uint32_t wst, uint32_t dcol,
+                                            uint32_t idesc, uint32_t ks0, bool first) {
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+#pragma unroll
+        for (int kk = 0; kk < KPC; ++kk) {
+            const uint64_t ad = ((uint64_t)ahi << 32) | (uint64_t)(alo + aoff[m] + 2u * (uint32_t)kk);
+            const uint64_t bd = ((uint64_t)bhi << 32) | (uint64_t)(blo0 + (uint32_t)m * wst + (ks0 + (uint32_t)kk) * bst);
+            rows::mma_ss_elect(dslot + dcol, ad, bd, idesc, (first && m == 0 && kk == 0) ? 0u : 1u);
+        }
+    }
+}
+
 template <int NM, int KPC, int NCH>
 __device__ __forceinline__ void rc_mma_loop(const RowsConv &P, uint32_t stg0, uint32_t wsm, uint64_t *full,
                                             uint64_t *empty, uint64_t *accf, uint64_t *acce) {
@@ -207,6 +225,36 @@ __device__ __forceinline__ void rc_mma_loop(const RowsConv &P, uint32_t stg0, ui
     const unsigned long long cstart = kProbes ? clock64() : 0;
     int sb = 0, slot = 0;
     uint32_t ph = 0, aph = 0;
+    if constexpr (kU && NCH > 1) {
+        if (P.cstage) {
+            // one chunk per stage, one tile per item: acquire the tile's slot,
+            // then accumulate chunk by chunk as the stages arrive
+            for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
+                int t0, t1, Ra, nrows;
+                rc_window(P, it, t0, t1, Ra, nrows);
+                mbar_wait(acce + slot, aph ^ 1);
+                fence_after_sync();
+                const int v0 = t0 * P.T + P.smin;
+                const uint32_t dslot = (uint32_t)slot * P.ND;
+                for (int ci = 0; ci < NCH; ++ci) {
+                    mbar_wait(full + sb, ph);
+                    fence_after_sync();
+                    const uint32_t stg = stg0 + (uint32_t)sb * P.stage_bytes;
+                    const uint64_t at =
+                        rows::sdesc(stg + (uint32_t)(v0 + P.sAmin - Ra * P.Wg) * P.pxS, 16u, sbo_a, swz);
+                    rc_issue_uc<NM, KPC>((uint32_t)at, (uint32_t)(at >> 32), dslot, aoff, blo[0], bhi, bst[0], wst,
+                                         dcol[0], idesc[0], (uint32_t)(ci * KPC), ci == 0);
+                    if (elect_one()) mma_commit(empty + sb);
+                    __syncwarp();
+                    if (++sb == P.nstg) { sb = 0; ph ^= 1; }
+                }
+                if (elect_one()) mma_commit(accf + slot);
+                __syncwarp();
+                if (++slot == P.nacc) { slot = 0; aph ^= 1; }
+            }
+            return;
+        }
+    }
     for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
         int t0, t1, Ra, nrows;
         rc_window(P, it, t0, t1, Ra, nrows);
@@ -546,6 +594,37 @@ __global__ void __launch_bounds__(kRcThreads, 1) rows_conv_kernel(const __grid_c
             for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
                 int t0, t1, Ra, nrows;
                 rc_window(P, it, t0, t1, Ra, nrows);
+                if (P.cstage) {
+                    // one stage per source chunk (rows of the window, this chunk's columns)
+                    const uint32_t rowb = (uint32_t)P.Wg * P.pxS;
+                    for (int ci = 0; ci < P.nch; ++ci) {
+                        mbar_wait(empty + sb, ph ^ 1);
+                        const uint32_t stg = stg0 + (uint32_t)sb * P.stage_bytes;
+                        const uint32_t mb = smem_u32(full + sb);
+                        mbar_arrive_expect_tx(full + sb, (uint32_t)(nrows * P.npl) * rowb);
+                        int r = 0;
+                        while (r < nrows) {
+                            const int R = Ra + r;
+                            const int img = R >= 0 ? R / P.Hg : -((-R + P.Hg - 1) / P.Hg);
+                            const int Y = R - img * P.Hg;
+                            const int len = min(P.Hg - Y, nrows - r);
+                            int k = 0;
+                            for (; k + P.hb <= len; k += P.hb)
+                                for (int pl = 0; pl < P.npl; ++pl)
+                                    rows::tma_load5d(stg + (uint32_t)pl * P.plane_bytes + (uint32_t)(r + k) * rowb,
+                                                     &P.tmH, ci * P.Ea, 0, P.pl_ox[pl], P.es * (Y + k) + P.pl_oy[pl],
+                                                     img, mb);
+                            for (; k < len; ++k)
+                                for (int pl = 0; pl < P.npl; ++pl)
+                                    rows::tma_load5d(stg + (uint32_t)pl * P.plane_bytes + (uint32_t)(r + k) * rowb,
+                                                     &P.tmS, ci * P.Ea, 0, P.pl_ox[pl], P.es * (Y + k) + P.pl_oy[pl],
+                                                     img, mb);
+                            r += len;
+                        }
+                        if (++sb == P.nstg) { sb = 0; ph ^= 1; }
+                    }
+                    continue;
+                }
                 mbar_wait(empty + sb, ph ^ 1);
                 if (kProbes && (P.dbg & 2)) {
                     mbar_arrive(full + sb);
@@ -940,6 +1019,24 @@ RcPlan make_rc_plan(const Problem &p, bool dgrad) {
                 }
             }
         }
+    }
+    if ((!bestG || best_nstg < 2) && P.nch > 1 && !P.merged && P.nmma == 9) {
+        // wide K (several source chunks): stage one chunk at a time, one tile per item
+        const int span_px = 32 + P.sAspan;
+        const int rows = span_px / P.Wg + 2;
+        const uint32_t plane_b = (uint32_t)rows * P.Wg * P.pxS;
+        const uint32_t stage_b = ((plane_b * (uint32_t)P.npl) + 1023u) & ~1023u;
+        for (int nstg = 4; nstg >= 2; --nstg)
+            if (1024ull + P.stg_off + (uint64_t)nstg * stage_b <= kRcSmemLimit) {
+                bestG = 1; best_nstg = nstg; best_stage = stage_b;
+                P.rows_max = rows;
+                P.hb = std::max(1, std::min(rows, 16));
+                P.plane_bytes = plane_b;
+                P.chunk_bytes = (uint32_t)P.npl * plane_b;
+                P.cstage = 1;
+                P.pair = 0;
+                break;
+            }
     }
     if (!bestG) return pl;
     P.G = bestG;
