@@ -1161,11 +1161,4 @@ cudaError_t rows_conv_run(capsconv_op_t op, const Problem &p, const void *src, c
     return cudaGetLastError();
 }
 
-bool rows_fc_supported(capsconv_op_t, const Problem &) { return false; }
-size_t rows_fc_workspace_bytes(capsconv_op_t, const Problem &) { return 0; }
-cudaError_t rows_fc_run(capsconv_op_t, const Problem &, const void *, const void *, void *, void *, size_t,
-                        cudaStream_t) {
-    return cudaErrorNotSupported;
-}
-
 }  // namespace capsconv

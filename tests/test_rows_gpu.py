@@ -122,9 +122,37 @@ def test_rows_stack_layers_full_batch_exact(cc, oracle_mod, li):
     rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
     rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
     assert np.abs(rdK).max() < 2 ** 24
-    if li < 3:   # the conv layers run the rows-layout tensor-core kernels on every pass
-        for op in (cc.OP_FWD, cc.OP_BWD_DATA, cc.OP_BWD_KERNEL):
-            assert cc.select_path(op, dt, ext_of(L), "rows") == cc.PATH_MMA, op
+    # every layer runs the rows-layout tensor-core kernels on every pass
+    for op in (cc.OP_FWD, cc.OP_BWD_DATA, cc.OP_BWD_KERNEL):
+        assert cc.select_path(op, dt, ext_of(L), "rows") == cc.PATH_MMA, op
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
+
+
+FC_CASES = [
+    # B, S (= H = W = KH = KW), C, Cout: full-extent (fully-connected) layers on
+    # the rows-layout GEMMs -- ragged batch tiles, several pixels, Cout < 16
+    (64, 8, 32, 10),
+    (37, 4, 32, 16),
+    (96, 2, 64, 10),
+    (32, 3, 32, 4),
+]
+
+
+@pytest.mark.parametrize("case", FC_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_rows_fc_exact(cc, oracle_mod, case):
+    B, S, C, Co = case
+    L = capsinputs.Layer(B, S, S, C, Co, S, S, 4, 4, 4, 1)
+    dt = torch.bfloat16
+    I = capsinputs.make_input(L, "int1", dt)
+    K = capsinputs.make_kernel(L, "int1", dt)
+    dO = capsinputs.make_grad_output(L.o_shape(1, 1), "int1", dt)
+    assert cc.select_path(cc.OP_FWD, dt, ext_of(L), "rows") == cc.PATH_MMA
+    O, dI, dK = run_rows(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), 1)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), 1, S, S)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), 1, S, S)
     np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
     np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
     np.testing.assert_array_equal(to_np(dK), rdK)
