@@ -14,6 +14,13 @@ CAPS = [("L1_dK", "r1b_fc_and_L1dK.ncu-rep", 3,
         ("L1_dK_prev", "r1_wgrad_L1_dK.ncu-rep", 0, "wgrad_kernel, earlier r1 build (before PDL)"),
         ("L3_dK", "r1_wgrad_L3_dK.ncu-rep", 0, "wgrad_kernel (capture predates descriptor-shift mode: nq=1)"),
         ("L1_fwd", "r1_conv_L1_fwd.ncu-rep", 0, "conv_mma_kernel fwd, G=8 CC=4, row-box staging")]
+# Round 2: rows layout (D1-outer), tests/probe/prof_r2.sh (run_rows_layer.py <layer> <op> 3, -s 2 -c 1)
+CAPS_R2 = [("L1_dI", "r2_L1_dI.ncu-rep", 0, "rows_conv_kernel dI (flipped-kernel conv of dO padded by 2), N=32 per tap"),
+           ("L1_fwd", "r2_L1_fwd.ncu-rep", 0, "rows_conv_kernel fwd, virtual-grid shifted windows, N=32 per tap"),
+           ("L1_dK", "r2_L1_dK.ncu-rep", 0, "rows_wgrad_kernel, row-walk slots (p) x atoms (q), MN-major I^T / dO"),
+           ("L2_fwd", "r2_L2_fwd.ncu-rep", 0, "rows_conv_kernel fwd stride 2 (merged phase planes), N=64"),
+           ("L3_dI", "r2_L3_dI.ncu-rep", 0, "rows_conv_kernel dI, chunk-staged source (cstage), N=64"),
+           ("L4_dI", "r2_L4_dI.ncu-rep", 0, "rows_fc_kernel mode 1 (FC dI GEMM, N=256 tiles, direct bf16 stores)")]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
@@ -29,12 +36,14 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def full_summaries():
-    out = ["# Round 1 ncu --set full captures (one launch each, --clock-control none, bf16, 1 B200)",
-           "# commands: tests/probe/run_layer.py / capture_ops.py under ncu --set full -k regex:<kernels>",
-           "# (cache control on: cold L2; shares/stalls matter, not the absolute time)", ""]
-    traffic = {}
-    for name, f, row, desc in CAPS:
+def full_summaries(caps, rnd, traffic):
+    out = ["# Round %d ncu --set full captures (one launch each, --clock-control none, bf16, 1 B200)" % rnd,
+           "# commands: " + ("tests/probe/run_layer.py / capture_ops.py" if rnd == 1 else "tests/probe/prof_r2.sh") +
+           " under ncu --set full -k regex:<kernel>",
+           "# (cache control on: cold L2; shares/stalls matter, not the absolute time; dram writes still dirty",
+           "#  in the 126 MB L2 when the kernel ends are not counted, so writes can read below the algorithmic bytes)",
+           ""]
+    for name, f, row, desc in caps:
         path = os.path.join(PROF, f)
         if not os.path.exists(path):
             continue
@@ -50,17 +59,14 @@ def full_summaries():
                 d[k] = (float(v[i].replace(",", "")), u[i])
         tb = int(d["dram__bytes_read.sum"][0] * SCALE[d["dram__bytes_read.sum"][1]] +
                  d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]])
-        traffic[name] = tb
+        traffic[name if rnd == 2 else "r1_" + name] = tb
         out.append("  %-80s %d" % ("dram read+write bytes per launch", tb))
         out.append("")
-    open(os.path.join(PROF, "r1_ncu_full_summary.txt"), "w").write("\n".join(out) + "\n")
-    traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the ncu --set full "
-                        "captures in profiles/ (tests/probe/profile_summary.py)")
-    json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    open(os.path.join(PROF, "r%d_ncu_full_summary.txt" % rnd), "w").write("\n".join(out) + "\n")
 
 
-def launches():
-    rows = [r for r in csv.reader(open(os.path.join(PROF, "r1_stack_launches.csv"))) if len(r) > 5]
+def launches(rnd, cmd):
+    rows = [r for r in csv.reader(open(os.path.join(PROF, "r%d_stack_launches.csv" % rnd))) if len(r) > 5]
     h, data = rows[0], rows[1:]
     iK, iV, iU = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     agg, tot = collections.OrderedDict(), 0.0
@@ -71,16 +77,23 @@ def launches():
         a[0] += 1
         a[1] += val
         tot += val
-    out = ["# r1 launch list: ncu --metrics gpu__time_duration.sum --clock-control none",
-           "# command: python bench.py --steps 3 --warmup 3 --no-cpu-baseline (eager warm-up steps, graph capture,",
+    out = ["# r%d launch list: ncu --metrics gpu__time_duration.sum --clock-control none" % rnd,
+           "# command: python bench.py %s --no-cpu-baseline (eager warm-up steps, graph capture," % cmd,
            "#          graph replays, L2 flush fills); ncu times are cold-cache and serialised: compare SHARES",
            "launches %d, total %.1f us" % (len(data), tot / 1e3)]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         out.append("%-22s n=%4d total=%9.1f us share=%5.1f%% avg=%7.1f us" % (k, n, t / 1e3, 100 * t / tot, t / n / 1e3))
-    open(os.path.join(PROF, "r1_stack_launches_summary.txt"), "w").write("\n".join(out) + "\n")
+    open(os.path.join(PROF, "r%d_stack_launches_summary.txt" % rnd), "w").write("\n".join(out) + "\n")
     print("\n".join(out))
 
 
 if __name__ == "__main__":
-    full_summaries()
-    launches()
+    traffic = {}
+    full_summaries(CAPS, 1, traffic)
+    full_summaries(CAPS_R2, 2, traffic)
+    traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the ncu --set full "
+                        "captures in profiles/ (tests/probe/profile_summary.py); unprefixed keys: round 2 "
+                        "(rows layout, the kernels bench.py times); r1_*: round-1 natural-layout kernels")
+    json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    launches(1, "--steps 3 --warmup 3")
+    launches(2, "--steps 2 --warmup 1")
