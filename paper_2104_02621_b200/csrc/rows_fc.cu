@@ -9,7 +9,7 @@
 //         B = K packed K-major; split-K, fp32 partials, fixed-order finalize.
 //   dI    dI[(b,d1), (p,c,d2)]     = sum_{(c',d3)} dO[b,d1,(c',d3)] K[p,c,c',d2,d3]
 //         A = dO rows K-major (K = Cout*D3, TMA zero fill to the k-step), B = K^T
-//         packed; one k-block, N = 256 tiles, bf16 straight to dI.
+//         packed; one k-block, N = 256 tiles, bf16 through swizzled staging + TMA stores.
 //   dK    dK[(p,c,d2), (c',d3)]    = sum_{(b,d1)} I[b,p,d1,(c,d2)] dO[b,d1,(c',d3)]
 //         A = I^T MN-major (two 64-element atoms per tile), B = dO MN-major;
 //         split-K over images, fp32 partials, fixed-order finalize into dK.
@@ -38,6 +38,7 @@ constexpr uint32_t kFcSmemLimit = 227 * 1024;
 struct RowsFc {
     alignas(64) CUtensorMap tmA;   // fwd/dK: I as (E, 4, P, B); dI: dO as (EO, B*4)
     alignas(64) CUtensorMap tmB;   // dK: dO as (EO, B*4)
+    alignas(64) CUtensorMap tmO;   // dI: dI as (E, 4, P, B), SWIZZLE_128B boxes (64, 4, 1, 8) for the stores
     int mode;                      // 0 fwd, 1 dI, 2 dK
     int B, P, E, EO, Cout, C;
     int N;                         // MMA N
@@ -50,6 +51,7 @@ struct RowsFc {
     const uint8_t *wpack;          // fwd: [chunk][N rows][128 B swizzled]; dI: [n][128 B swizzled]
     float *part;                   // fwd / dK: [ksplit][M][N] fp32 partials
     __nv_bfloat16 *out;            // dI output
+    uint32_t epi_off;              // dI: per-warp store staging (2 x 4 KB per epilogue warp) from stg0
     uint32_t smem_bytes;
 };
 
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
         // ------------------------------------------------------------ epilogue
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        int slot = 0;
+        int slot = 0, ebi = 0;
         uint32_t aph = 0;
         for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
             int mt, nt, ks;
@@ -187,28 +189,42 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
             fence_after_sync();
             const uint32_t tb = ((uint32_t)(q * 32) << 16) + (uint32_t)slot * 256u;
             if (P.mode == 1) {
-                // rows (b, d1) of dI; columns (p_local, c, d2): P.E elements per pixel p
-                const int b = 32 * mt + (row >> 2), d1 = row & 3;
-                const bool ok = b < P.B;
-                for (int c0 = 0; c0 < P.N; c0 += 32) {
-                    float v[32];
-                    rows::tmem_ld32(tb + (uint32_t)c0, v);
+                // rows (b, d1) of dI, 8 images x 4 d1 per warp; columns (p, c, d2).  Each
+                // 64-column chunk (one pixel p, 64 elements of E) is converted to bf16,
+                // written to a per-warp SWIZZLE_128B staging box (row = lane, 16-byte
+                // chunk j at j ^ (lane & 7): conflict-free) and stored by one TMA
+                // (64, 4, 1, 8) box; two staging buffers alternate.
+                const uint32_t ebuf = stg0 + P.epi_off + (uint32_t)q * 8192u;
+                const int b0 = 32 * mt + 8 * q;
+                for (int c0 = 0; c0 < P.N; c0 += 64) {
+                    float v[64];
+                    rows::tmem_ld32(tb + (uint32_t)c0, *reinterpret_cast<float(*)[32]>(v));
+                    rows::tmem_ld32(tb + (uint32_t)c0 + 32u, *reinterpret_cast<float(*)[32]>(v + 32));
                     tmem_wait_ld();
-                    const int n = nt * P.N + c0, p = n / P.E, e = n - p * P.E;
-                    if (ok) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(
-                            P.out + ((((size_t)b * P.P + p) * 4 + d1) * (size_t)P.E + e));
+                    const uint32_t buf = ebuf + (uint32_t)(ebi & 1) * 4096u;
+                    if (lane == 0) rows::bulk_wait_read<1>();
+                    __syncwarp();
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            uint32_t w[4];
+                    for (int j = 0; j < 8; ++j) {
+                        uint32_t w[4];
 #pragma unroll
-                            for (int c = 0; c < 4; ++c) {
-                                __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * g + 2 * c], v[8 * g + 2 * c + 1]);
-                                w[c] = *reinterpret_cast<uint32_t *>(&h);
-                            }
-                            dst[g] = make_uint4(w[0], w[1], w[2], w[3]);
+                        for (int c = 0; c < 4; ++c) {
+                            __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * j + 2 * c], v[8 * j + 2 * c + 1]);
+                            w[c] = *reinterpret_cast<uint32_t *>(&h);
                         }
+                        const uint32_t a = buf + (uint32_t)lane * 128u + (uint32_t)((j ^ (lane & 7)) * 16);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(w[0]), "r"(w[1]),
+                                     "r"(w[2]), "r"(w[3])
+                                     : "memory");
                     }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    const int n = nt * P.N + c0, p = n / P.E, e = n - p * P.E;
+                    if (lane == 0 && b0 < P.B) {
+                        rows::tma_store4d(&P.tmO, buf, e, 0, p, b0);
+                        rows::bulk_commit();
+                    }
+                    ++ebi;
                 }
             } else {
                 // fp32 partial rows [ks][M][N]
@@ -227,6 +243,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
             if (lane == 0) mbar_arrive(acce + slot);
             if (++slot == P.nacc) { slot = 0; aph ^= 1; }
         }
+        if (P.mode == 1 && lane == 0) rows::bulk_wait_all();
     }
     fence_before_sync();
     __syncthreads();
@@ -362,11 +379,13 @@ FcPlan make_fc_plan(const Problem &p, int mode) {
             if (P.kst % k == 0 && P.nmt * k <= 2 * nsm) P.ksplit = k;
     }
     P.stage_bytes = (P.a_bytes + P.b_bytes + 1023u) & ~1023u;
-    P.nstg = std::min(8, (int)((kFcSmemLimit - 2048u) / P.stage_bytes));
+    const uint32_t epi = mode == 1 ? 4u * 8192u : 0u;
+    P.nstg = std::min(8, (int)((kFcSmemLimit - 2048u - epi) / P.stage_bytes));
     if (P.nstg < 2) return pl;
     P.nacc = 2;
     P.n_items = P.nmt * P.nnt * P.ksplit;
-    P.smem_bytes = 2048u + (uint32_t)P.nstg * P.stage_bytes;
+    P.epi_off = (uint32_t)P.nstg * P.stage_bytes;
+    P.smem_bytes = 2048u + P.epi_off + epi;
     if (mode != 1) pl.part_bytes = (size_t)P.ksplit * P.nmt * 128 * P.N * 4;
     pl.ok = true;
     return pl;
@@ -414,7 +433,9 @@ cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const
         if (!rows::make_rows_map4(&P.tmA, a, P.B, P.P, P.E, 64, 1, 32)) return cudaErrorInvalidValue;
     } else if (mode == 1) {
         // a = dO, b = K
-        if (!rows::make_rows_map2(&P.tmA, a, (int64_t)P.B * 4, P.EO, 32, 128, 64)) return cudaErrorInvalidValue;
+        if (!rows::make_rows_map2(&P.tmA, a, (int64_t)P.B * 4, P.EO, 32, 128, 64) ||
+            !rows::make_rows_map4(&P.tmO, out, P.B, P.P, P.E, 64, 1, 8))
+            return cudaErrorInvalidValue;
         P.out = static_cast<__nv_bfloat16 *>(out);
     } else {
         // a = I, b = dO
