@@ -130,11 +130,12 @@ static capsconv_status_t make_problem(capsconv_dtype_t dt, int64_t B, int64_t H,
 // the problem, else the natural-layout path between two permutations.
 static bool rows_mma(capsconv_op_t op, const Problem &p) {
     if (p.layout != CAPSCONV_LAYOUT_ROWS || g_path_override.load() == CAPSCONV_PATH_SIMT) return false;
-    if (rows_fc_supported(op, p)) return true;
+    if (rows_fc_supported(op, p) || rows_walk_supported(op, p)) return true;
     return op == CAPSCONV_OP_BWD_KERNEL ? rows_wgrad_supported(p) : rows_conv_supported(op, p);
 }
 static size_t rows_mma_ws(capsconv_op_t op, const Problem &p) {
     if (rows_fc_supported(op, p)) return rows_fc_workspace_bytes(op, p);
+    if (rows_walk_supported(op, p)) return rows_walk_workspace_bytes(op, p);
     return op == CAPSCONV_OP_BWD_KERNEL ? rows_wgrad_workspace_bytes(p) : rows_conv_workspace_bytes(op, p);
 }
 static Problem natural_of(const Problem &p) {
@@ -207,6 +208,7 @@ static cudaError_t dispatch_rows(capsconv_op_t op, const Problem &p, const void 
     const size_t need = rows_mma(op, p) ? rows_mma_ws(op, p) : 0;
     if (rows_mma(op, p) && aligned16(a) && aligned16(b) && aligned16(out) && (need == 0 || aligned16(ws))) {
         if (rows_fc_supported(op, p)) return rows_fc_run(op, p, a, b, out, ws, ws_bytes, cs);
+        if (rows_walk_supported(op, p)) return rows_walk_run(op, p, a, b, out, ws, ws_bytes, cs);
         if (op == CAPSCONV_OP_BWD_KERNEL)
             return rows_wgrad_run(p, a, b, static_cast<float *>(out), ws, ws_bytes, cs);
         return rows_conv_run(op, p, a, b, out, ws, ws_bytes, cs);

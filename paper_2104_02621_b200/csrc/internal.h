@@ -129,6 +129,10 @@ bool rows_conv_supported(capsconv_op_t op, const Problem &p);
 size_t rows_conv_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t rows_conv_run(capsconv_op_t op, const Problem &p, const void *src, const void *K, void *out, void *ws,
                           size_t ws_bytes, cudaStream_t st);
+bool rows_walk_supported(capsconv_op_t op, const Problem &p);
+size_t rows_walk_workspace_bytes(capsconv_op_t op, const Problem &p);
+cudaError_t rows_walk_run(capsconv_op_t op, const Problem &p, const void *src, const void *K, void *out, void *ws,
+                          size_t ws_bytes, cudaStream_t st);
 bool rows_fc_supported(capsconv_op_t op, const Problem &p);
 size_t rows_fc_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const void *b, void *out, void *ws,

@@ -84,6 +84,13 @@ __device__ __forceinline__ void tma_store4d(const CUtensorMap *m, uint32_t src, 
                  "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                  : "memory");
 }
+__device__ __forceinline__ void tma_store5d(const CUtensorMap *m, uint32_t src, int c0, int c1, int c2, int c3,
+                                            int c4) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // wait until at most N committed store groups still READ shared memory
 template <int N>
@@ -135,12 +142,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // Host: tensor maps over a rows-layout bf16 tensor [B][Hs][Ws][4][E]
 // (E = C*D2 elements per capsule row).
-//   map5: dims (E, 4, Ws, Hs, B), box (ce, 4, bx, by, 1), element strides
+//   map5: dims (E, 4, Ws, Hs, B), box (ce, 4, bx, by, bb), element strides
 //         (1, 1, es_x, es_y, 1) -- a box lands [by'][bx'][4][ce] with
 //         bx' = bx / es_x pixels per row (every es_x-th pixel), zero filled
 //         outside the tensor; swizzle = 2*ce bytes.
 bool make_rows_map5(CUtensorMap *map, const void *base, int64_t B, int64_t Hs, int64_t Ws, int64_t E, int ce, int bx,
-                    int by, int es_x, int es_y);
+                    int by, int es_x, int es_y,
+                    int bb = 1);
 //   map2: a row-major [rows][E] bf16 matrix, box (ce, br), swizzle 2*ce bytes
 //         (ce = 16/32/64), or no swizzle when swz == 0 (then ce*2 must be 16).
 bool make_rows_map2(CUtensorMap *map, const void *base, int64_t rows, int64_t E, int ce, int br, int swz);

@@ -57,14 +57,14 @@ CUtensorMapSwizzle swz_enum(int bytes) {
 }  // namespace
 
 bool make_rows_map5(CUtensorMap *map, const void *base, int64_t B, int64_t Hs, int64_t Ws, int64_t E, int ce, int bx,
-                    int by, int es_x, int es_y) {
+                    int by, int es_x, int es_y, int bb) {
     EncodeTiledFn fn = encode_fn();
-    if (!fn || ce * 2 > 128 || bx > 256 || by > 256 || bx < 1 || by < 1) return false;
+    if (!fn || ce * 2 > 128 || bx > 256 || by > 256 || bx < 1 || by < 1 || bb < 1 || bb > 256) return false;
     const cuuint64_t el = 2;
     cuuint64_t dims[5] = {(cuuint64_t)E, 4, (cuuint64_t)Ws, (cuuint64_t)Hs, (cuuint64_t)B};
     cuuint64_t strides[4] = {(cuuint64_t)E * el, (cuuint64_t)(4 * E) * el, (cuuint64_t)(Ws * 4 * E) * el,
                              (cuuint64_t)(Hs * Ws * 4 * E) * el};
-    cuuint32_t box[5] = {(cuuint32_t)ce, 4, (cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t box[5] = {(cuuint32_t)ce, 4, (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bb};
     cuuint32_t estr[5] = {1, 1, (cuuint32_t)es_x, (cuuint32_t)es_y, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, swz_enum(ce * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

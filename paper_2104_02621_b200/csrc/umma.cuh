@@ -166,6 +166,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 #endif
 }
 
+// Waiting with a suspend-time hint: the thread sleeps until the phase
+// completes (or the hint elapses) instead of re-polling -- for consumer warps
+// that wait long, so they leave the issue slots to the producer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!ok);
+}
+
 // ---------------------------------------------------------------- bulk copies (TMA engine, 1-D)
 // global -> shared, completion counted in bytes on `bar` (caller arms expect_tx).
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {

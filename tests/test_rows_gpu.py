@@ -158,6 +158,41 @@ def test_rows_fc_exact(cc, oracle_mod, case):
     np.testing.assert_array_equal(to_np(dK), rdK)
 
 
+WALK_CASES = [
+    # B, H, W, C, Cout, KH, KW, D1, D2, D3, s: the row-walk kernel (rows_walk.cu) --
+    # G = 2 and 4 images per tile with a ragged last group, 32-pixel x tiles,
+    # more output rows than accumulator slots (ring wrap), KW = 2 / 4, two
+    # source chunks, 16-column rows, stride-2 phase planes
+    (3, 10, 12, 8, 8, 3, 3, 4, 4, 4, 1),
+    (2, 20, 40, 8, 8, 3, 3, 4, 4, 4, 1),
+    (5, 9, 6, 8, 4, 3, 2, 4, 4, 4, 1),
+    (2, 23, 23, 8, 16, 3, 3, 4, 4, 4, 2),
+    (2, 14, 70, 8, 8, 3, 3, 4, 4, 4, 2),
+    (2, 12, 12, 16, 16, 3, 4, 4, 4, 4, 1),
+    (1, 30, 9, 32, 16, 2, 3, 4, 4, 4, 1),
+    (2, 12, 12, 8, 4, 5, 3, 4, 4, 4, 1),
+]
+
+
+@pytest.mark.parametrize("case", WALK_CASES, ids=lambda c: "x".join(map(str, c)))
+def test_rows_walk_exact(cc, oracle_mod, case):
+    """Exact-integer bf16 inputs through the row-walk forward / dI kernel."""
+    L = capsinputs.Layer(*case)
+    dt = torch.bfloat16
+    I = capsinputs.make_input(L, "int", dt)
+    K = capsinputs.make_kernel(L, "int", dt)
+    Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "int", dt)
+    assert cc.select_path(cc.OP_FWD, dt, ext_of(L), "rows") == cc.PATH_MMA
+    O, dI, dK = run_rows(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), L.stride)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
+
+
 def test_rows_deterministic(cc):
     L = _stack_layers()[0]
     I = to_rows(capsinputs.make_input(L, dtype=torch.bfloat16).to(DEV))
