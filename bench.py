@@ -50,7 +50,22 @@ def parse():
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--layout", default="rows", choices=["rows", "natural"],
                     help="capsule-tensor layout of the stack's activations (include/capsconv.h)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the in-bench oracle parity check")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: re-launch this script as N
+    ranks of one node (torch.distributed.run, rendezvous on 127.0.0.1) and
+    return its exit code; the launcher's rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------- workload
@@ -274,9 +289,69 @@ def stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch):
     return X, dY
 
 
+# The paper's own result, quoted as context: not comparable
+# hardware, precision or workload, so vs_baseline stays null.
+PAPER_CONTEXT = {
+    "claim": "4x: capsule-conv CapsNet fwd+bwd 510 ms (ours, official APIs) vs 2220 ms ('GPU' baseline)",
+    "gpu": "NVIDIA TITAN X (Pascal), CUDA 10.0",
+    "source": "PAPER.md:29 (abstract), :278 (experiments), Table 1 :154-156",
+    "comparable": False,
+}
+
+
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+def parity_check(pkg, specs, H, W, D, PB, weights, X_nat, dY_nat, dtype, dev, layout):
+    """Max normalised error max|gpu - oracle| / max|oracle| of every tensor of
+    one stack step (forward outputs of every layer, dX, every dK) on PB images;
+    bf16 outputs and dI are compared with the oracle rounded at the same bf16
+    boundaries (reading R13).  Tolerance: north_star's 2e-2 (bf16) / 1e-5 (fp32)."""
+    import numpy as np
+    import oracle
+    from paper_2104_02621_b200.stack import CapsStack
+    st = CapsStack(specs, H, W, D, PB, weights, dev, overlap=False, layout=layout)
+    perm = (lambda t: t.permute(0, 1, 2, 4, 3, 5).contiguous()) if layout == "rows" else (lambda t: t)
+    st.step(perm(X_nat.to(dev)), perm(dY_nat.to(dev)))
+    torch.cuda.synchronize()
+    f64 = lambda t: t.detach().to("cpu", torch.float64).numpy()
+    strides = [sp.stride for sp in specs]
+    pads = [sp.pad for sp in specs]
+    acts, dX, dKs, _ = oracle.stack_fwd_bwd(f64(X_nat), [f64(k) for k in weights], strides, f64(dY_nat),
+                                            dtype == torch.bfloat16, pads=pads)
+    outs = [st.acts[i] for i in range(1, len(specs))] + [st.out]
+    errs = {}
+
+    def rel(a, b):
+        m = float(np.abs(b).max())
+        return float(np.abs(a - b).max()) / (m if m > 0 else 1.0)
+
+    for li, o in enumerate(outs):
+        errs["O%d" % (li + 1)] = rel(f64(perm(o)), acts[li + 1])
+    errs["dX"] = rel(f64(perm(st.grads[0])), dX)
+    for li, k in enumerate(st.dK):
+        errs["dK%d" % (li + 1)] = rel(f64(k), dKs[li])
+    tol = 2e-2 if dtype == torch.bfloat16 else 1e-5
+    worst = max(errs.values())
+    return {"images": PB, "max_norm_err": {k: float("%.3g" % v) for k, v in errs.items()}, "worst": float("%.3g" % worst),
+            "tol": tol, "pass": worst <= tol}
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -312,6 +387,8 @@ def main():
     X_host = capsinputs.make_input(L0, dtype=dtype, batch_offset=lo, batch=batch)
     dY_host = capsinputs.make_grad_output((gbatch, h, w, specs[-1].Cout, D, D), dtype=dtype, layer_idx=len(specs),
                                           batch_offset=lo, batch=batch)
+    PB = min(2, batch)            # images of the in-bench parity check (natural layout, for the oracle)
+    X_nat, dY_nat = X_host[:PB].clone(), dY_host[:PB].clone()
     if args.layout == "rows":   # the same synthetic tensors stored D1-outer: (B, H, W, D1, C, D2)
         X_host = X_host.permute(0, 1, 2, 4, 3, 5).contiguous()
         dY_host = dY_host.permute(0, 1, 2, 4, 3, 5).contiguous()
@@ -336,28 +413,37 @@ def main():
     torch.cuda.synchronize()
 
     # The timed step is one CUDA-graph replay of the whole step (every kernel
-    # of every pass; the graph removes host launch gaps between them).  The
+    # of every pass, and for N > 1 the per-layer NCCL dK all-reduces on the
+    # side stream; the graph removes host launch gaps between them).  The
     # per-call events are captured with it; launches are counted at capture.
-    # (N > 1: eager -- the per-layer NCCL all-reduces on the side stream are
-    # not captured into the graph; that path is only exercised on CPU/gloo here)
-    use_graph = not args.eager and world == 1
+    # If capture fails (e.g. an NCCL build without graph support) the step is
+    # timed eagerly and the line says so.
+    use_graph = not args.eager
+    graph_note = None
     gtimer = GraphCallTimer() if use_graph else None
     launches_per_step = None
     if use_graph:
-        graph = torch.cuda.CUDAGraph()
-        cap_stream = torch.cuda.Stream(dev)
-        cap_stream.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(cap_stream):
-            st.step(X, dY)                      # warm the capture stream's workspace
-        torch.cuda.synchronize()
-        c0 = pkg.launch_count()
-        with torch.cuda.graph(graph, stream=cap_stream):
-            st.step(X, dY, timer=gtimer)
-        launches_per_step = pkg.launch_count() - c0
-        torch.cuda.synchronize()
-        for _ in range(2):
-            graph.replay()
-        torch.cuda.synchronize()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cap_stream = torch.cuda.Stream(dev)
+            cap_stream.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(cap_stream):
+                st.step(X, dY)                      # warm the capture stream's workspace
+            torch.cuda.synchronize()
+            barrier()
+            c0 = pkg.launch_count()
+            with torch.cuda.graph(graph, stream=cap_stream):
+                st.step(X, dY, timer=gtimer)
+            launches_per_step = pkg.launch_count() - c0
+            torch.cuda.synchronize()
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:   # fall back to eager launches, reported in config.launch
+            graph_note = "graph capture failed (%s): eager launches" % str(exc).splitlines()[0][:120]
+            print("bench: " + graph_note, file=sys.stderr)
+            torch.cuda.synchronize()
+            use_graph, gtimer = False, None
 
     timer = CallTimer()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -478,26 +564,48 @@ def main():
            "d2h_bytes_per_step": dk_host.numel() * 4, "ms_per_step": e2e_ms,
            "note": "pinned host->device copy of step i+1 overlapped with step i on a copy stream"}
 
-    # ---- CPU baseline: the oracle as it stands, on host cores, bounded sample
+    # ---- CPU baseline: the oracle as it stands, on host cores, bounded
+    # samples: all cores (OpenMP, ~10 s) and one thread (~5 s)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             import oracle
             oracle.build()
             fl1, Ks, strides, layers = stack_oracle_setup(specs, H, W, D, dtype)
-            Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, 1, dtype, gbatch)
-            t0 = time.perf_counter()
-            oracle.stack_fwd_bwd(Xs, Ks, strides[0], dYs, dtype == torch.bfloat16, pads=strides[1])
-            t1 = time.perf_counter() - t0
+
+            def timed(b):
+                Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch)
+                t0 = time.perf_counter()
+                oracle.stack_fwd_bwd(Xs, Ks, strides[0], dYs, dtype == torch.bfloat16, pads=strides[1])
+                return time.perf_counter() - t0
+
+            ncores = oracle.num_threads()
+            t1 = timed(1)
             b = int(max(1, min(gbatch, 10.0 / max(t1, 1e-6))))
-            Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch)
-            t0 = time.perf_counter()
-            oracle.stack_fwd_bwd(Xs, Ks, strides[0], dYs, dtype == torch.bfloat16, pads=strides[1])
-            tb = time.perf_counter() - t0
-            cpu = {"value": fl1 * b / tb / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
-                   "sample": "oracle (C, fp64, OpenMP) %s fwd+bwd on %d of %d images, %.1f s" % (name, b, gbatch, tb)}
+            tb = timed(b)
+            oracle.set_num_threads(1)
+            try:
+                s1 = timed(1)
+                b1 = int(max(1, min(gbatch, 5.0 / max(s1, 1e-6))))
+                sb1 = timed(b1) if b1 > 1 else s1
+            finally:
+                oracle.set_num_threads(ncores)
+            cpu = {"value": fl1 * b / tb / 1e12, "unit": "TFLOP/s", "cores": ncores, "kind": "oracle",
+                   "sample": "oracle (C, fp64, OpenMP) %s fwd+bwd on %d of %d images, %.1f s" % (name, b, gbatch, tb),
+                   "single_thread": {"value": fl1 * b1 / sb1 / 1e12, "cores": 1,
+                                     "sample": "%d images, %.1f s" % (b1, sb1)},
+                   "host": host_cpu()}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "TFLOP/s", "cores": None, "kind": "oracle", "sample": "failed: %s" % e}
+
+    # ---- parity: the benchmarked stack (same layout, weights, launch path) on
+    # the first PB images of this rank's shard vs the oracle stack
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = parity_check(pkg, specs, H, W, D, PB, weights, X_nat, dY_nat, dtype, dev, args.layout)
+        except Exception as e:
+            parity = {"pass": False, "error": str(e)[:200]}
 
     if rank == 0:
         line = {
@@ -511,10 +619,13 @@ def main():
                        "layout": args.layout,
                        "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
                        "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None,
-                       "launch": ("one CUDA-graph replay of the captured step (%d libcapsconv kernels)" % launches_per_step)
-                       if use_graph else "eager launches"},
+                       "launch": ("one CUDA-graph replay of the captured step (%d libcapsconv kernels%s)" % (
+                           launches_per_step, " + %d NCCL all-reduces" % len(specs) if world > 1 else ""))
+                       if use_graph else (graph_note or "eager launches")},
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "parity": parity,
+            "paper_context": PAPER_CONTEXT,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),

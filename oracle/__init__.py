@@ -31,6 +31,7 @@ from .oracle import (  # noqa: F401
     bwd_kernel_slices,
     round_bf16,
     num_threads,
+    set_num_threads,
     stack_fwd_bwd,
     OracleError,
 )

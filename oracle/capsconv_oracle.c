@@ -222,6 +222,18 @@ int oracle_num_threads(void)
 #endif
 }
 
+/* Thread count of the OpenMP loops (timing only: bench.py's single-thread and
+   all-core baselines); the arithmetic and its order per output are unchanged. */
+void oracle_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+
 /* ------------------------------------------------------------------------
  * Zero padding (SPEC.md:48-53 symmetric zero padding -- the
  * paper itself has no padding term).  The definition with

@@ -69,6 +69,8 @@ def _load():
             lib.oracle_round_bf16_array.restype = None
             lib.oracle_num_threads.argtypes = []
             lib.oracle_num_threads.restype = ctypes.c_int
+            lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+            lib.oracle_set_num_threads.restype = None
             _lib = lib
     return _lib
 
@@ -84,6 +86,11 @@ def _f64(a) -> np.ndarray:
 
 def num_threads() -> int:
     return int(_load().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count of the oracle loops (timing only)."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def output_dims(H, W, KH, KW, stride, pad=0):

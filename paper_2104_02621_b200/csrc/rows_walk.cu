@@ -58,6 +58,7 @@ struct RowsWalk {
     int B, Hs, Ho, Wo;
     int G, Xs, nxt, ngi, n_items;  // images per tile, pixel slot per image, x tiles, image groups, items
     int x0mul, x0off;              // source pixel of plane 0, x tile xt: x0mul*xt + x0off
+    int box_px;                    // pixels per plane of one source-row box (per image)
     int npl, nch, Ea;              // planes (= s), source chunks per row, elements per chunk
     int ncls, ncl[2], pm[2];       // row classes (Ys mod s); taps per class; y0 = (Ys - pm)/s
     int NB, R;                     // accumulator columns per output row; ring slots
@@ -555,6 +556,7 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
         box_px = 32 + kwp - 1;
     }
     if (box_px * s > 256) return pl;
+    P.box_px = box_px;
     P.x0mul = dgrad ? 32 : 32 * s;
     P.x0off = dgrad ? -(KW - 1) : 0;
     P.ngi = (P.B + P.G - 1) / P.G;
@@ -696,8 +698,7 @@ cudaError_t rows_walk_run(capsconv_op_t op, const Problem &p, const void *src, c
     RowsWalk &P = pl.P;
     const int64_t Es = dgrad ? 4 * p.Cout : 4 * p.C, Eo = dgrad ? 4 * p.C : 4 * p.Cout;
     const int64_t Ws = dgrad ? p.Wo : p.W;
-    const int box_px = P.nxt == 1 ? P.Xs : 32 + (dgrad ? P.KW : (P.KW + P.s - 1) / P.s) - 1;
-    if (!rows::make_rows_map5(&P.tmS, src, p.B, P.Hs, Ws, Es, P.Ea, box_px * P.s, 1, P.s, 1, P.G) ||
+    if (!rows::make_rows_map5(&P.tmS, src, p.B, P.Hs, Ws, Es, P.Ea, P.box_px * P.s, 1, P.s, 1, P.G) ||
         !rows::make_rows_map5(&P.tmO, out, p.B, P.Ho, P.Wo, Eo, P.cw, 8, P.ey, 1, 1, 1))
         return cudaErrorInvalidValue;
     P.wpack = static_cast<const uint8_t *>(ws);

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace capsconv {
 namespace umma {
@@ -157,7 +158,17 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t *bar, uint32_t parity) {
 #define CAPSCONV_MBAR_POLL 0
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-#if CAPSCONV_MBAR_POLL
+#if defined(CAPSCONV_PROBES)
+    // probe builds: a watchdog names the barrier a hung pipeline waits on
+    unsigned long long n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++n == (1ull << 26)) {
+            printf("[mbar watchdog] block %d thread %d bar smem+%u parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
+                   smem_u32(bar) & 0xffffu, parity);
+            __trap();
+        }
+    }
+#elif CAPSCONV_MBAR_POLL
     while (!mbar_test_wait(bar, parity)) {
     }
 #else
@@ -171,6 +182,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // that wait long, so they leave the issue slots to the producer warps.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
+#if defined(CAPSCONV_PROBES)
+    unsigned long long n = 0;
+#endif
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -179,6 +193,13 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
             : "memory");
+#if defined(CAPSCONV_PROBES)
+        if (!ok && ++n == (1ull << 16)) {
+            printf("[mbar watchdog] block %d thread %d bar smem+%u parity %u (sleep wait)\n", (int)blockIdx.x,
+                   (int)threadIdx.x, smem_u32(bar) & 0xffffu, parity);
+            __trap();
+        }
+#endif
     } while (!ok);
 }
 

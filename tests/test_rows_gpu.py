@@ -130,6 +130,28 @@ def test_rows_stack_layers_full_batch_exact(cc, oracle_mod, li):
     np.testing.assert_array_equal(to_np(dK), rdK)
 
 
+@pytest.mark.parametrize("cfg", ["layer_s1", "layer_s2", "fc"])
+def test_rows_configs_full_exact(cc, oracle_mod, cfg):
+    """BASELINE.json configs 2-4 at their full batch in the rows layout (the
+    launch configuration of bench.py --config), exact-integer inputs."""
+    L = capsinputs.CONFIGS[cfg]
+    dt = torch.bfloat16
+    I = capsinputs.make_input(L, "int1", dt)
+    K = capsinputs.make_kernel(L, "int1", dt)
+    Ho, Wo = oracle_mod.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), "int1", dt)
+    for op in (cc.OP_FWD, cc.OP_BWD_DATA, cc.OP_BWD_KERNEL):
+        assert cc.select_path(op, dt, ext_of(L), "rows") == cc.PATH_MMA, op
+    O, dI, dK = run_rows(cc, L, I, K, dO)
+    rO, _ = oracle_mod.fwd(to_np(I), to_np(K), L.stride)
+    rdI, _ = oracle_mod.bwd_data(to_np(dO), to_np(K), L.stride, L.H, L.W)
+    rdK, _ = oracle_mod.bwd_kernel(to_np(I), to_np(dO), L.stride, L.KH, L.KW)
+    assert np.abs(rdK).max() < 2 ** 24
+    np.testing.assert_array_equal(to_np(O), oracle_mod.round_bf16(rO))
+    np.testing.assert_array_equal(to_np(dI), oracle_mod.round_bf16(rdI))
+    np.testing.assert_array_equal(to_np(dK), rdK)
+
+
 FC_CASES = [
     # B, S (= H = W = KH = KW), C, Cout: full-extent (fully-connected) layers on
     # the rows-layout GEMMs -- ragged batch tiles, several pixels, Cout < 16
@@ -171,6 +193,8 @@ WALK_CASES = [
     (2, 12, 12, 16, 16, 3, 4, 4, 4, 4, 1),
     (1, 30, 9, 32, 16, 2, 3, 4, 4, 4, 1),
     (2, 12, 12, 8, 4, 5, 3, 4, 4, 4, 1),
+    (2, 32, 32, 8, 8, 3, 3, 4, 4, 4, 1),    # dI rows read 34 source pixels, one 32-pixel tile
+    (3, 16, 16, 16, 32, 3, 3, 4, 4, 4, 2),  # config 3's layer at a small batch
 ]
 
 
