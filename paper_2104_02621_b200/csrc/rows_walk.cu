@@ -48,6 +48,7 @@ namespace {
 constexpr int kWkMaxR = 16;        // accumulator slots
 constexpr int kWkMaxStg = 12;   // stages over all streams
 constexpr int kWkMaxQ = 4;         // column taps (KW)
+constexpr int kWkMaxRows = 64;     // walked source rows (the schedule lives in the kernel parameters)
 constexpr uint32_t kWkSmemLimit = 227 * 1024;
 
 struct RowsWalk {
@@ -70,26 +71,35 @@ struct RowsWalk {
     uint32_t woff_s, wbytes, soff, sbytes;   // shared offsets (from the 1024-aligned base): weights, staging
     uint32_t roff;                 // shared offset of the per-source-row schedule (32 B per row)
     int ey;                        // output rows per epilogue store box
+    int rps;                       // source rows per pipeline step (1 or 2): stage = rps rows x planes of one chunk
     __nv_bfloat16 *out;
     uint32_t smem_bytes;
     uint32_t wof[2][kWkMaxQ];      // weight block (class, q) byte offsets in the image
     uint32_t aoff[kWkMaxQ];        // A offset of column tap q: plane * plane_bytes + shift * 4 rows
+    uint32_t sched[kWkMaxRows][8]; // per-source-row MMA schedule (wk_make_rec), built on the host
     unsigned long long *prof;      // probe builds only: per-CTA cycle counters [cta][8]
     int dbg;                       // probe builds only: 1 skip epilogue stores, 2 skip source loads, 4 skip MMAs
 };
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long wk_clk() { return kProbes ? clock64() : 0ull; }
 
-__device__ __forceinline__ int wk_y0(const RowsWalk &P, int Ys, int &cl) {
+__host__ __device__ __forceinline__ int wk_min(int a, int b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int wk_max(int a, int b) { return a > b ? a : b; }
+
+__host__ __device__ __forceinline__ int wk_y0(const RowsWalk &P, int Ys, int &cl) {
     cl = P.s == 2 ? (Ys & 1) : 0;
     return P.s == 2 ? (Ys - P.pm[cl]) >> 1 : Ys - P.pm[0];   // exact: Ys - pm[cl] is a multiple of s
 }
 
 // valid output rows [ya, yb] of source row Ys (empty if ya > yb)
-__device__ __forceinline__ void wk_rows(const RowsWalk &P, int Ys, int &cl, int &y0, int &ya, int &yb) {
+__host__ __device__ __forceinline__ void wk_rows(const RowsWalk &P, int Ys, int &cl, int &y0, int &ya, int &yb) {
     y0 = wk_y0(P, Ys, cl);
-    ya = max(y0, 0);
-    yb = min(y0 + P.ncl[cl] - 1, P.Ho - 1);
+    ya = wk_max(y0, 0);
+    yb = wk_min(y0 + P.ncl[cl] - 1, P.Ho - 1);
 }
 
 // Per-source-row MMA schedule, identical for every strip (the accumulator of
@@ -103,20 +113,20 @@ __device__ __forceinline__ void wk_rows(const RowsWalk &P, int Ys, int &cl, int 
 //               accumulate << 20 | N/8 << 21 (0: no segment)
 constexpr uint32_t kWkRecBytes = 32;
 
-__device__ __forceinline__ void wk_seg(const RowsWalk &P, int y0, int u, int v, uint32_t acc, uint32_t &a,
-                                       uint32_t &b) {
+__host__ __device__ __forceinline__ void wk_seg(const RowsWalk &P, int y0, int u, int v, uint32_t acc, uint32_t &a,
+                                                uint32_t &b) {
     a = 0u;
     b = 0u;
     if (u > v) return;
     const int slot = u % P.Rw;
-    const int w = min(v, u + (P.Rw - slot) - 1);
+    const int w = wk_min(v, u + (P.Rw - slot) - 1);
     a = (uint32_t)(slot * P.NB) | ((uint32_t)((u - y0) * P.NB) << 10) | (acc << 20) |
         ((uint32_t)((w - u + 1) * P.NB / 8) << 21);
     if (w < v)
         b = ((uint32_t)((w + 1 - y0) * P.NB) << 10) | (acc << 20) | ((uint32_t)((v - w) * P.NB / 8) << 21);
 }
 
-__device__ void wk_make_rec(const RowsWalk &P, int Ys, uint32_t (&w)[8]) {
+__host__ __device__ void wk_make_rec(const RowsWalk &P, int Ys, uint32_t (&w)[8]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = 0u;
     int cl, y0, ya, yb;
@@ -133,7 +143,7 @@ __device__ void wk_make_rec(const RowsWalk &P, int Ys, uint32_t (&w)[8]) {
         wk_rows(P, Yn, c2, y02, ya2, yb2);
         if (ya2 <= yb2) { ynext = ya2; break; }
     }
-    const int yf = max(ya, yfresh);
+    const int yf = wk_max(ya, yfresh);
     uint32_t wm = 0u, cm = 0u;
     for (int y = yf; y <= yb; ++y) wm |= 1u << (y % P.Rw);
     for (int y = ya; y < ynext; ++y) cm |= 1u << (y % P.Rw);
@@ -183,44 +193,67 @@ __device__ __forceinline__ void wk_mma(const RowsWalk &P, int w, uint32_t stg0, 
     uint32_t ph = 0, mph = 0;   // stage phase; per-slot acce phases
     unsigned long long pw_full = 0, pw_acce = 0;
     const unsigned long long pstart = wk_clk();
+    const int rps = P.rps;                                       // source rows per pipeline step
+    const uint32_t rowb16 = (uint32_t)P.npl * (P.plane_bytes >> 4);  // next row of a step
     for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += P.nmw * (int)gridDim.x) {
-        for (int r = 0; r < nrow; ++r) {
-            const uint4 h0 = ld_shared_v4(sched + (uint32_t)r * kWkRecBytes);
-            if (!(h0.y & 1u)) continue;
-            const uint4 h1 = ld_shared_v4(sched + (uint32_t)r * kWkRecBytes + 16u);
+        for (int r0 = 0; r0 < nrow; r0 += rps) {
+            // the step's rows: records, then the slots their first touches need
+            uint4 h0[2], h1[2];
+            bool v[2];
+            uint32_t wm = 0u, cm = 0u;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                v[j] = false;
+                h0[j] = make_uint4(0u, 0u, 0u, 0u);
+                h1[j] = h0[j];
+                if (j < rps && r0 + j < nrow) {
+                    const uint32_t *rec = P.sched[r0 + j];
+                    h0[j] = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+                    v[j] = (h0[j].y & 1u) != 0u;
+                    if (v[j]) {
+                        h1[j] = make_uint4(rec[4], rec[5], rec[6], rec[7]);
+                        wm |= h0[j].x & 0xffffu;
+                        cm |= h0[j].x >> 16;
+                    }
+                }
+            }
+            if (!v[0] && !v[1]) continue;
             unsigned long long t0 = wk_clk();
-            for (uint32_t m = h0.x & 0xffffu; m; m &= m - 1u) {   // slots first touched here
+            for (uint32_t m = wm; m; m &= m - 1u) {   // slots first touched in this step
                 const int j = __ffs(m) - 1;
                 mbar_wait(acce + j, ((mph >> j) & 1u) ^ 1u);
                 mph ^= 1u << j;
             }
             if (kProbes) pw_acce += wk_clk() - t0;
             fence_after_sync();
-            const int cl = (h0.y >> 1) & 1u;
-            const uint32_t bstc = cl ? bst[1] : bst[0];
-            uint32_t wqc[KWT];
-#pragma unroll
-            for (int q = 0; q < KWT; ++q) wqc[q] = cl ? wq[1][q] : wq[0][q];
             for (int c = 0; c < nch; ++c) {
                 t0 = wk_clk();
                 mbar_wait(full + sb, ph);
                 if (kProbes) pw_full += wk_clk() - t0;
                 fence_after_sync();
-                const uint32_t alo = a0lo + (uint32_t)sb * sbytes16;
 #pragma unroll
-                for (int q = 0; q < (kProbes && (P.dbg & 4) ? 0 : KWT); ++q) {
+                for (int j = 0; j < 2; ++j) {
+                    if (!v[j]) continue;
+                    const uint32_t alo = a0lo + (uint32_t)sb * sbytes16 + (uint32_t)j * rowb16;
+                    const int cl = (h0[j].y >> 1) & 1u;
+                    const uint32_t bstc = cl ? bst[1] : bst[0];
 #pragma unroll
-                    for (int kk = 0; kk < KPC; ++kk) {
-                        const uint64_t ad = ((uint64_t)ahi << 32) | (uint64_t)(alo + aoff[q] + 2u * (uint32_t)kk);
-                        const uint32_t bk = wqc[q] + (uint32_t)(c * KPC + kk) * bstc;
-                        if (q == 0 && kk == 0 && c == 0) {
-                            if (h0.z >> 21) wk_mma_seg(h0.z, dbase, ad, bhi, bk, ibase, (h0.z >> 20) & 1u);
-                            if (h0.w >> 21) wk_mma_seg(h0.w, dbase, ad, bhi, bk, ibase, (h0.w >> 20) & 1u);
-                            if (h1.x >> 21) wk_mma_seg(h1.x, dbase, ad, bhi, bk, ibase, (h1.x >> 20) & 1u);
-                            if (h1.y >> 21) wk_mma_seg(h1.y, dbase, ad, bhi, bk, ibase, (h1.y >> 20) & 1u);
-                        } else {
-                            wk_mma_seg(h1.z, dbase, ad, bhi, bk, ibase, 1u);
-                            if (h1.w >> 21) wk_mma_seg(h1.w, dbase, ad, bhi, bk, ibase, 1u);
+                    for (int q = 0; q < (kProbes && (P.dbg & 4) ? 0 : KWT); ++q) {
+                        const uint32_t wqc = cl ? wq[1][q] : wq[0][q];
+#pragma unroll
+                        for (int kk = 0; kk < KPC; ++kk) {
+                            const uint64_t ad = ((uint64_t)ahi << 32) | (uint64_t)(alo + aoff[q] + 2u * (uint32_t)kk);
+                            const uint32_t bk = wqc + (uint32_t)(c * KPC + kk) * bstc;
+                            if (q == 0 && kk == 0 && c == 0) {
+                                const uint4 a = h0[j], b = h1[j];
+                                if (a.z >> 21) wk_mma_seg(a.z, dbase, ad, bhi, bk, ibase, (a.z >> 20) & 1u);
+                                if (a.w >> 21) wk_mma_seg(a.w, dbase, ad, bhi, bk, ibase, (a.w >> 20) & 1u);
+                                if (b.x >> 21) wk_mma_seg(b.x, dbase, ad, bhi, bk, ibase, (b.x >> 20) & 1u);
+                                if (b.y >> 21) wk_mma_seg(b.y, dbase, ad, bhi, bk, ibase, (b.y >> 20) & 1u);
+                            } else {
+                                wk_mma_seg(h1[j].z, dbase, ad, bhi, bk, ibase, 1u);
+                                if (h1[j].w >> 21) wk_mma_seg(h1[j].w, dbase, ad, bhi, bk, ibase, 1u);
+                            }
                         }
                     }
                 }
@@ -229,7 +262,7 @@ __device__ __forceinline__ void wk_mma(const RowsWalk &P, int w, uint32_t stg0, 
                 if (++sb == nstg) { sb = 0; ph ^= 1; }
             }
             if (elect_one())   // rows no later source row touches
-                for (uint32_t m = h0.x >> 16; m; m &= m - 1u) mma_commit(accf + (__ffs(m) - 1));
+                for (uint32_t m = cm; m; m &= m - 1u) mma_commit(accf + (__ffs(m) - 1));
             __syncwarp();
         }
     }
@@ -287,14 +320,6 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
         mbar_fence_init();
     }
     if (warp == 1) tmem_alloc_dyn(tmem_slot, 512);
-    // the per-source-row schedule (independent of the data: built before the PDL wait)
-    for (int r = threadIdx.x; r <= P.ys_hi - P.ys_lo; r += blockDim.x) {
-        uint32_t w[8];
-        wk_make_rec(P, P.ys_lo + r, w);
-        uint8_t *dst = smem_raw + (sched - smem_u32(smem_raw)) + (size_t)r * kWkRecBytes;
-        reinterpret_cast<uint4 *>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        reinterpret_cast<uint4 *>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
-    }
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
@@ -321,8 +346,15 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
             for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += nmw * (int)gridDim.x) {
                 const int gi = it / P.nxt, xt = it - gi * P.nxt;
                 const int X0 = P.x0mul * xt + P.x0off;
-                for (int r = 0; r < nrow; ++r) {
-                    if (!(ld_shared_v4(sched + (uint32_t)r * kWkRecBytes).y & 1u)) continue;
+                for (int r0 = 0; r0 < nrow; r0 += P.rps) {
+                    bool v[2];
+                    int nv = 0;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        v[j] = j < P.rps && r0 + j < nrow && (P.sched[r0 + j][1] & 1u);
+                        nv += v[j] ? 1 : 0;
+                    }
+                    if (!nv) continue;
                     for (int c = 0; c < P.nch; ++c) {
                         const unsigned long long t0 = wk_clk();
                         mbar_wait(emptyw + sb, ph ^ 1);
@@ -334,10 +366,13 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
                             if (++sb == P.nstg) { sb = 0; ph ^= 1; }
                             continue;
                         }
-                        mbar_arrive_expect_tx(fullw + sb, P.stage_tx);
-                        for (int pl = 0; pl < P.npl; ++pl)
-                            rows::tma_load5d(stg + (uint32_t)pl * P.plane_bytes, &P.tmS, c * P.Ea, 0, X0 + pl,
-                                             P.ys_lo + r, gi * P.G, mb);
+                        mbar_arrive_expect_tx(fullw + sb, P.stage_tx * (uint32_t)nv);
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            if (v[j])
+                                for (int pl = 0; pl < P.npl; ++pl)
+                                    rows::tma_load5d(stg + (uint32_t)(j * P.npl + pl) * P.plane_bytes, &P.tmS, c * P.Ea,
+                                                     0, X0 + pl, P.ys_lo + r0 + j, gi * P.G, mb);
                         if (++sb == P.nstg) { sb = 0; ph ^= 1; }
                     }
                 }
@@ -361,12 +396,22 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
         // group g serves stream w = g / gps; its rows y = g % gps (mod gps)
         const int e = warp - 2 * nmw, grp = e >> 2, qq = warp & 3;   // TMEM lane quarter of this warp
         const int gps = P.nepi / nmw, w = grp / gps, gl = grp - w * gps;
+        // One TMA box store per group and row block: the group's four warps
+        // stage their 32 rows each into the group buffer (box (cw, 4, Xs, ey, G)
+        // image: row ((b*ey + yy)*Xs + x)*4 + d1), meet at a named barrier, and
+        // the group's first warp issues the store (4x fewer TMA operations than
+        // one box per warp: the TMA unit's operation rate bounds thin layers).
         const uint32_t rowb = (uint32_t)P.cw * 2u;              // staged row bytes (= swizzle span)
         const int EY = P.ey, nbuf = P.nbuf;
-        const uint32_t bufb = (uint32_t)EY * 32u * rowb;         // one staging box
-        const uint32_t sbuf0 = base + P.soff + (uint32_t)(e * nbuf) * bufb;
-        const int px0 = 8 * qq;                                  // first tile pixel of this warp's lanes
+        const uint32_t bufb = (uint32_t)EY * 128u * rowb;        // one group staging box
+        const uint32_t sbuf0 = base + P.soff + (uint32_t)(grp * nbuf) * bufb;
+        const bool leader = (e & 3) == 0 && lane == 0;
+        const int bar_id = 1 + grp;
+        const int pxl = 8 * qq + (lane >> 2), d1 = lane & 3;     // this lane's tile pixel and d1 row
         const int Rw = P.Rw, NB = P.NB, cw = P.cw;
+        // staging row of (yy, this lane): b = pxl / Xs, x = pxl % Xs
+        const int lb = P.G > 1 ? pxl / P.Xs : 0, lx = P.G > 1 ? pxl - lb * P.Xs : pxl;
+        const int sxs = P.G > 1 ? P.Xs : 32;
         accf += w * Rw;
         acce += w * Rw;
         const uint32_t tl = ((uint32_t)(qq * 32) << 16) + (uint32_t)(w * Rw * NB);
@@ -376,9 +421,7 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
         const unsigned long long pe_start = wk_clk();
         for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += nmw * (int)gridDim.x) {
             const int gi = it / P.nxt, xt = it - gi * P.nxt;
-            const int img = gi * P.G + (P.G > 1 ? px0 / P.Xs : 0);
-            const int x0 = P.G > 1 ? px0 % P.Xs : 32 * xt + px0;
-            const bool st_ok = img < P.B && x0 < P.Wo;
+            const int img0 = gi * P.G, xg0 = P.G > 1 ? 0 : 32 * xt;
             // row blocks [y0, y0 + EY), y0 = EY * gl (mod EY * gps): EY * gps divides Rw
             int slot = EY * gl;
             for (int y0 = EY * gl; y0 < P.Ho; y0 += EY * gps) {
@@ -392,11 +435,11 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
                 fence_after_sync();
                 for (int c0 = 0; c0 < NB; c0 += cw) {
                     const uint32_t buf = sbuf0 + (uint32_t)(nbuf > 1 ? (bi & 1) : 0) * bufb;
-                    if (lane == 0) {   // this buffer's previous store has read it
+                    if (leader) {   // this buffer's previous store has read it
                         if (nbuf > 1) rows::bulk_wait_read<1>();
                         else rows::bulk_wait_read<0>();
                     }
-                    __syncwarp();
+                    named_bar_sync(bar_id, 128);
                     for (int yy = 0; yy < ny; ++yy) {
                         const uint32_t tb = tl + (uint32_t)((slot + yy) * NB + c0);
                         float v[64];
@@ -413,14 +456,15 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
                             if (lane == 0) mbar_arrive(acce + slot + yy);
                         }
                         if (kProbes && (P.dbg & 1)) continue;
-                        if (cw == 16) wk_stage<16>(v, buf, yy * 32 + lane);
-                        else if (cw == 32) wk_stage<32>(v, buf, yy * 32 + lane);
-                        else wk_stage<64>(v, buf, yy * 32 + lane);
+                        const int r = ((lb * EY + yy) * sxs + lx) * 4 + d1;
+                        if (cw == 16) wk_stage<16>(v, buf, r);
+                        else if (cw == 32) wk_stage<32>(v, buf, r);
+                        else wk_stage<64>(v, buf, r);
                     }
                     fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0 && st_ok && !(kProbes && (P.dbg & 1))) {
-                        rows::tma_store5d(&P.tmO, buf, c0, 0, x0, y0, img);
+                    named_bar_sync(bar_id, 128);
+                    if (leader && img0 < P.B && !(kProbes && (P.dbg & 1))) {
+                        rows::tma_store5d(&P.tmO, buf, c0, 0, xg0, y0, img0);
                         rows::bulk_commit();
                     }
                     ++bi;
@@ -429,7 +473,7 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
                 if (slot >= Rw) slot -= Rw;
             }
         }
-        if (lane == 0) rows::bulk_wait_all();
+        if (leader) rows::bulk_wait_all();
         if (kProbes && P.prof && e == 0 && lane == 0) {
             unsigned long long *o = P.prof + (size_t)blockIdx.x * 8;
             o[3] = pe_wait;
@@ -534,8 +578,8 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // two TMA + MMA warp pairs (alternate strips, half the slots each) when the
     // halves still hold a window plus slack: one warp's issue rate is the limit
     // for thin rows
-    P.nmw = P.R / 2 >= nmax + 2 ? 2 : 1;
-    if (kProbes && probe_env("CAPSCONV_WK_NMW")) P.nmw = std::max(1, std::min(2, atoi(probe_env("CAPSCONV_WK_NMW"))));
+    P.nmw = P.R / 3 >= nmax + 2 ? 3 : P.R / 2 >= nmax + 2 ? 2 : 1;
+    if (kProbes && probe_env("CAPSCONV_WK_NMW")) P.nmw = std::max(1, std::min(3, atoi(probe_env("CAPSCONV_WK_NMW"))));
     if (P.R / P.nmw < nmax + 2) P.nmw = 1;
     P.Rw = P.R / P.nmw;
     // columns: plane q mod s, shift q / s (fwd); one plane, shift KW-1-q (dI)
@@ -604,40 +648,54 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // prefer >= 4 stages, then more epilogue groups, then double-buffered stores
     if (kProbes && probe_env("CAPSCONV_WK_DBG")) P.dbg = atoi(probe_env("CAPSCONV_WK_DBG"));
     const size_t limit = std::min<size_t>(kWkSmemLimit, device_info().smem_optin ? device_info().smem_optin : kWkSmemLimit);
-    const uint32_t rbytes = (uint32_t)(P.ys_hi - P.ys_lo + 1) * 32u;
+    const uint32_t rbytes = 0u;   // the schedule lives in the kernel parameters
     int max_epi = 4, max_ey = 2;
     if (kProbes && probe_env("CAPSCONV_WK_NEPI")) max_epi = atoi(probe_env("CAPSCONV_WK_NEPI"));
     if (kProbes && probe_env("CAPSCONV_WK_EY")) max_ey = atoi(probe_env("CAPSCONV_WK_EY"));
     bool found = false;
     // candidates (epilogue groups, rows per store box, staging buffers)
-    const int cand[10][3] = {{4, 2, 2}, {4, 2, 1}, {4, 1, 2}, {2, 2, 2}, {4, 1, 1},
-                             {2, 2, 1}, {2, 1, 2}, {2, 1, 1}, {1, 1, 2}, {1, 1, 1}};
-    for (int want = 4; want >= 2 && !found; --want)
-        for (int ci = 0; ci < 10 && !found; ++ci) {
-            const int nepi = cand[ci][0], ey = cand[ci][1], nbuf = cand[ci][2];
-            if (nepi > max_epi || ey > max_ey || nepi % P.nmw || P.Rw % (ey * (nepi / P.nmw))) continue;
-            const uint32_t sb = (uint32_t)(nepi * 4 * nbuf * ey) * 32u * (uint32_t)P.cw * 2u;
-            for (int nstg = kWkMaxStg / P.nmw; nstg >= want; --nstg) {
-                const uint32_t wo = (uint32_t)(nstg * P.nmw) * P.stage_bytes;
-                const uint32_t ro = (wo + P.wbytes + 127u) & ~127u;
-                const uint32_t so = (ro + rbytes + 1023u) & ~1023u;
-                const size_t tot = 2048u + (size_t)so + sb;
-                if (tot <= limit) {
-                    P.nstg = nstg;
-                    P.nepi = nepi;
-                    P.ey = ey;
-                    P.nbuf = nbuf;
-                    P.woff_s = wo;
-                    P.roff = ro;
-                    P.soff = so;
-                    P.sbytes = sb;
-                    P.smem_bytes = (uint32_t)tot;
-                    found = true;
-                    break;
+    const int cand[12][3] = {{4, 2, 2}, {4, 2, 1}, {4, 1, 2}, {2, 2, 2}, {4, 1, 1}, {3, 1, 2},
+                             {2, 2, 1}, {2, 1, 2}, {3, 1, 1}, {2, 1, 1}, {1, 1, 2}, {1, 1, 1}};
+    // two source rows per pipeline step when >= 3 such stages fit (halves the
+    // per-row waits and releases of the MMA and TMA warps), else one
+    int rps_max = 2;
+    if (kProbes && probe_env("CAPSCONV_WK_RPS")) rps_max = std::max(1, std::min(2, atoi(probe_env("CAPSCONV_WK_RPS"))));
+    const uint32_t row_bytes = P.plane_bytes * (uint32_t)P.npl;
+    for (int rps = rps_max; rps >= 1 && !found; --rps)
+        for (int want = rps == 2 ? 4 : 4; want >= (rps == 2 ? 3 : 2) && !found; --want)
+            for (int ci = 0; ci < 12 && !found; ++ci) {
+                const int nepi = cand[ci][0], ey = cand[ci][1], nbuf = cand[ci][2];
+                if (nepi > max_epi || ey > max_ey || nepi % P.nmw || P.Rw % (ey * (nepi / P.nmw)) ||
+                    64 * P.nmw + 128 * nepi > 640)
+                    continue;
+                const uint32_t sb = (uint32_t)(nepi * nbuf * ey) * 128u * (uint32_t)P.cw * 2u;
+                const uint32_t stage = row_bytes * (uint32_t)rps;
+                for (int nstg = kWkMaxStg / P.nmw; nstg >= want; --nstg) {
+                    const uint32_t wo = (uint32_t)(nstg * P.nmw) * stage;
+                    const uint32_t ro = (wo + P.wbytes + 127u) & ~127u;
+                    const uint32_t so = (ro + rbytes + 1023u) & ~1023u;
+                    const size_t tot = 2048u + (size_t)so + sb;
+                    if (tot <= limit) {
+                        P.rps = rps;
+                        P.stage_bytes = stage;
+                        P.nstg = nstg;
+                        P.nepi = nepi;
+                        P.ey = ey;
+                        P.nbuf = nbuf;
+                        P.woff_s = wo;
+                        P.roff = ro;
+                        P.soff = so;
+                        P.sbytes = sb;
+                        P.smem_bytes = (uint32_t)tot;
+                        found = true;
+                        break;
+                    }
                 }
             }
-        }
     if (!found) return pl;
+    // the per-source-row schedule (identical for every strip)
+    if (P.ys_hi - P.ys_lo + 1 > kWkMaxRows) return pl;
+    for (int r = 0; r <= P.ys_hi - P.ys_lo; ++r) wk_make_rec(P, P.ys_lo + r, P.sched[r]);
     // the walk must touch every output row, with windows moving forward
     {
         int yfresh = 0, last_ya = 0;
@@ -656,9 +714,9 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     if (kProbes && probe_env("CAPSCONV_WK_DEBUG"))
         fprintf(stderr,
                 "[wk plan] %s s=%d G=%d Xs=%d nxt=%d items=%d Ea=%d nch=%d NB=%d R=%d nmw=%d ncl=%d/%d stage=%u nstg=%d "
-                "nepi=%d nbuf=%d cw=%d ey=%d wbytes=%u smem=%u ys=[%d,%d]\n",
+                "nepi=%d nbuf=%d cw=%d ey=%d rps=%d wbytes=%u smem=%u ys=[%d,%d]\n",
                 dgrad ? "dI" : "fwd", s, P.G, P.Xs, P.nxt, P.n_items, P.Ea, P.nch, P.NB, P.R, P.nmw, P.ncl[0], P.ncl[1],
-                P.stage_bytes, P.nstg, P.nepi, P.nbuf, P.cw, P.ey, P.wbytes, P.smem_bytes, P.ys_lo, P.ys_hi);
+                P.stage_bytes, P.nstg, P.nepi, P.nbuf, P.cw, P.ey, P.rps, P.wbytes, P.smem_bytes, P.ys_lo, P.ys_hi);
     pl.ok = true;
     return pl;
 }
@@ -699,7 +757,7 @@ cudaError_t rows_walk_run(capsconv_op_t op, const Problem &p, const void *src, c
     const int64_t Es = dgrad ? 4 * p.Cout : 4 * p.C, Eo = dgrad ? 4 * p.C : 4 * p.Cout;
     const int64_t Ws = dgrad ? p.Wo : p.W;
     if (!rows::make_rows_map5(&P.tmS, src, p.B, P.Hs, Ws, Es, P.Ea, P.box_px * P.s, 1, P.s, 1, P.G) ||
-        !rows::make_rows_map5(&P.tmO, out, p.B, P.Ho, P.Wo, Eo, P.cw, 8, P.ey, 1, 1, 1))
+        !rows::make_rows_map5(&P.tmO, out, p.B, P.Ho, P.Wo, Eo, P.cw, P.G > 1 ? P.Xs : 32, P.ey, 1, 1, P.G))
         return cudaErrorInvalidValue;
     P.wpack = static_cast<const uint8_t *>(ws);
     P.out = static_cast<__nv_bfloat16 *>(out);
