@@ -13,7 +13,8 @@
 //   dK    dK[(p,c,d2), (c',d3)]    = sum_{(b,d1)} I[b,p,d1,(c,d2)] dO[b,d1,(c',d3)]
 //         A = I^T MN-major (two 64-element atoms per tile), B = dO MN-major;
 //         split-K over images, fp32 partials, fixed-order finalize into dK.
-// Roles (192 threads): warp 0 TMA, warp 1 MMA (TMEM owner), warps 2-5 epilogue.
+// Roles (320 threads): warp 0 TMA, warp 1 MMA (TMEM owner), warps 2-9 epilogue (two per TMEM
+// lane quarter, each taking half of the columns).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -32,7 +33,8 @@ using namespace umma;
 
 namespace {
 
-constexpr int kFcThreads = 192;
+constexpr int kFcEpw = 2;                      // epilogue warps per TMEM lane quarter
+constexpr int kFcThreads = 64 + 128 * kFcEpw;  // warp 0 TMA, warp 1 MMA, then the epilogue warps
 constexpr uint32_t kFcSmemLimit = 227 * 1024;
 
 struct RowsFc {
@@ -52,6 +54,7 @@ struct RowsFc {
     float *part;                   // fwd / dK: [ksplit][M][N] fp32 partials
     __nv_bfloat16 *out;            // dI output
     uint32_t epi_off;              // dI: per-warp store staging (2 x 4 KB per epilogue warp) from stg0
+    int dst_direct;                // dI: 1 coalesced 16-byte stores from the staging, 0 TMA box stores
     uint32_t smem_bytes;
 };
 
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(accf + i, 1);
-            mbar_init(acce + i, 4);
+            mbar_init(acce + i, 4 * kFcEpw);
         }
         mbar_fence_init();
     }
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int q = warp & 3;
+        const int q = warp & 3, half = (warp - 2) >> 2;   // lane quarter; column part (of kFcEpw)
         const int row = q * 32 + lane;
         int slot = 0, ebi = 0;
         uint32_t aph = 0;
@@ -194,15 +197,15 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
                 // written to a per-warp SWIZZLE_128B staging box (row = lane, 16-byte
                 // chunk j at j ^ (lane & 7): conflict-free) and stored by one TMA
                 // (64, 4, 1, 8) box; two staging buffers alternate.
-                const uint32_t ebuf = stg0 + P.epi_off + (uint32_t)q * 8192u;
+                const uint32_t ebuf = stg0 + P.epi_off + (uint32_t)(warp - 2) * 8192u;
                 const int b0 = 32 * mt + 8 * q;
-                for (int c0 = 0; c0 < P.N; c0 += 64) {
+                for (int c0 = half * (P.N / kFcEpw); c0 < (half + 1) * (P.N / kFcEpw); c0 += 64) {
                     float v[64];
                     rows::tmem_ld32(tb + (uint32_t)c0, *reinterpret_cast<float(*)[32]>(v));
                     rows::tmem_ld32(tb + (uint32_t)c0 + 32u, *reinterpret_cast<float(*)[32]>(v + 32));
                     tmem_wait_ld();
                     const uint32_t buf = ebuf + (uint32_t)(ebi & 1) * 4096u;
-                    if (lane == 0) rows::bulk_wait_read<1>();
+                    if (lane == 0 && !P.dst_direct) rows::bulk_wait_read<1>();
                     __syncwarp();
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -217,19 +220,35 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
                                      "r"(w[2]), "r"(w[3])
                                      : "memory");
                     }
-                    fence_proxy_async_smem();
-                    __syncwarp();
                     const int n = nt * P.N + c0, p = n / P.E, e = n - p * P.E;
-                    if (lane == 0 && b0 < P.B) {
-                        rows::tma_store4d(&P.tmO, buf, e, 0, p, b0);
-                        rows::bulk_commit();
+                    if (P.dst_direct) {
+                        // coalesced 16-byte stores: 8 lanes write one 128-byte capsule-row piece
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int k = i * 32 + lane, r = k >> 3, j = k & 7;
+                            const int b = b0 + (r >> 2);
+                            if (b < P.B) {
+                                const uint4 x = ld_shared_v4(buf + (uint32_t)r * 128u + (uint32_t)((j ^ (r & 7)) * 16));
+                                *reinterpret_cast<uint4 *>(P.out + ((((size_t)b * P.P + p) * 4 + (r & 3)) * (size_t)P.E + e +
+                                                                    (size_t)j * 8)) = x;
+                            }
+                        }
+                        __syncwarp();
+                    } else {
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0 && b0 < P.B) {
+                            rows::tma_store4d(&P.tmO, buf, e, 0, p, b0);
+                            rows::bulk_commit();
+                        }
                     }
                     ++ebi;
                 }
             } else {
                 // fp32 partial rows [ks][M][N]
                 float *dst = P.part + ((size_t)ks * P.nmt * 128 + (size_t)mt * 128 + row) * P.N;
-                for (int c0 = 0; c0 < P.N; c0 += 16) {
+                for (int c0 = 16 * half; c0 < P.N; c0 += 16 * kFcEpw) {
                     float v[16];
                     tmem_ld16(tb + (uint32_t)c0, v);
                     tmem_wait_ld();
@@ -243,7 +262,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
             if (lane == 0) mbar_arrive(acce + slot);
             if (++slot == P.nacc) { slot = 0; aph ^= 1; }
         }
-        if (P.mode == 1 && lane == 0) rows::bulk_wait_all();
+        if (P.mode == 1 && lane == 0 && !P.dst_direct) rows::bulk_wait_all();
     }
     fence_before_sync();
     __syncthreads();
@@ -379,12 +398,14 @@ FcPlan make_fc_plan(const Problem &p, int mode) {
             if (P.kst % k == 0 && P.nmt * k <= 2 * nsm) P.ksplit = k;
     }
     P.stage_bytes = (P.a_bytes + P.b_bytes + 1023u) & ~1023u;
-    const uint32_t epi = mode == 1 ? 4u * 8192u : 0u;
+    const uint32_t epi = mode == 1 ? 4u * kFcEpw * 8192u : 0u;
     P.nstg = std::min(8, (int)((kFcSmemLimit - 2048u - epi) / P.stage_bytes));
     if (P.nstg < 2) return pl;
     P.nacc = 2;
     P.n_items = P.nmt * P.nnt * P.ksplit;
     P.epi_off = (uint32_t)P.nstg * P.stage_bytes;
+    P.dst_direct = 1;
+    if (kProbes && probe_env("CAPSCONV_FC_TMASTORE")) P.dst_direct = 0;
     P.smem_bytes = 2048u + P.epi_off + epi;
     if (mode != 1) pl.part_bytes = (size_t)P.ksplit * P.nmt * 128 * P.N * 4;
     pl.ok = true;

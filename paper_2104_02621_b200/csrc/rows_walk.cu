@@ -71,6 +71,7 @@ struct RowsWalk {
     uint32_t woff_s, wbytes, soff, sbytes;   // shared offsets (from the 1024-aligned base): weights, staging
     uint32_t roff;                 // shared offset of the per-source-row schedule (32 B per row)
     int ey;                        // output rows per epilogue store box
+    int est;                       // epilogue stores: 0 one TMA box per group, 2 per-warp coalesced 16-byte stores
     int rps;                       // source rows per pipeline step (1 or 2): stage = rps rows x planes of one chunk
     __nv_bfloat16 *out;
     uint32_t smem_bytes;
@@ -297,6 +298,123 @@ __device__ __forceinline__ void wk_stage(const float *v, uint32_t buf, int r) {
     }
 }
 
+// Epilogue warps.  Group g serves stream w = g / gps and its row blocks
+// y0 = EY*gl (mod EY*gps).  Each warp owns TMEM lane quarter qq = 32 rows of
+// the accumulator (8 pixels x 4 d1).  EST 2: per-warp swizzled staging, then
+// coalesced 16-byte stores (the SM's TMA unit serves only the source loads);
+// EST 0: the group's four warps stage one box (cw, 4, Xs, ey, G) and its first
+// warp issues one TMA store.
+template <int CW, int EST>
+__device__ __forceinline__ void wk_epilogue(const RowsWalk &P, int warp, int lane, uint32_t base, uint64_t *accf,
+                                            uint64_t *acce) {
+    const int nmw = P.nmw;
+    const int e = warp - 2 * nmw, grp = e >> 2, qq = warp & 3;
+    const int gps = P.nepi / nmw, w = grp / gps, gl = grp - w * gps;
+    constexpr uint32_t rowb = (uint32_t)CW * 2u;             // staged row bytes (= swizzle span)
+    constexpr int cpr = CW / 8;                               // 16-byte chunks per staged row
+    constexpr uint32_t zsh = rowb == 128u ? 0u : rowb == 64u ? 1u : 2u;
+    const int EY = P.ey, nbuf = P.nbuf;
+    const uint32_t bufb = (uint32_t)EY * 128u * rowb;         // one group staging box
+    const uint32_t sbuf0 = base + P.soff + (uint32_t)(grp * nbuf) * bufb;
+    const uint32_t wbuf = sbuf0 + (uint32_t)(e & 3) * (uint32_t)EY * 32u * rowb;   // EST 2: this warp's rows
+    const bool leader = (e & 3) == 0 && lane == 0;
+    const int bar_id = 1 + grp;
+    const int pxl = 8 * qq + (lane >> 2), d1 = lane & 3;      // this lane's tile pixel and d1 row
+    const int Rw = P.Rw, NB = P.NB;
+    const int lb = P.G > 1 ? pxl / P.Xs : 0, lx = P.G > 1 ? pxl - lb * P.Xs : pxl;
+    const int sxs = P.G > 1 ? P.Xs : 32;
+    const int wimg_off = P.G > 1 ? (8 * qq) / P.Xs : 0, wx_off = P.G > 1 ? (8 * qq) % P.Xs : 8 * qq;
+    accf += w * Rw;
+    acce += w * Rw;
+    const uint32_t tl = ((uint32_t)(qq * 32) << 16) + (uint32_t)(w * Rw * NB);
+    uint32_t eph = 0;                                         // per-slot accf phases
+    int bi = 0;
+    unsigned long long pe_wait = 0, pe_rows = 0;
+    const unsigned long long pe_start = wk_clk();
+    for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += nmw * (int)gridDim.x) {
+        const int gi = it / P.nxt, xt = it - gi * P.nxt;
+        const int img0 = gi * P.G, xg0 = P.G > 1 ? 0 : 32 * xt;
+        const int wimg = img0 + wimg_off, wx0 = xg0 + wx_off;
+        int slot = EY * gl;
+        for (int y0 = EY * gl; y0 < P.Ho; y0 += EY * gps) {
+            const int ny = min(EY, P.Ho - y0);
+            const unsigned long long e0 = wk_clk();
+            for (int yy = 0; yy < ny; ++yy) {
+                mbar_wait_sleep(accf + slot + yy, (eph >> (slot + yy)) & 1u);
+                eph ^= 1u << (slot + yy);
+            }
+            if (kProbes) { pe_wait += wk_clk() - e0; pe_rows += ny; }
+            fence_after_sync();
+            for (int c0 = 0; c0 < NB; c0 += CW) {
+                const uint32_t buf = sbuf0 + (uint32_t)(nbuf > 1 ? (bi & 1) : 0) * bufb;
+                if (EST == 0) {
+                    if (leader) {   // this buffer's previous store has read it
+                        if (nbuf > 1) rows::bulk_wait_read<1>();
+                        else rows::bulk_wait_read<0>();
+                    }
+                    named_bar_sync(bar_id, 128);
+                }
+                for (int yy = 0; yy < ny; ++yy) {
+                    const uint32_t tb = tl + (uint32_t)((slot + yy) * NB + c0);
+                    float v[CW];
+                    if (CW == 16) {
+                        tmem_ld16(tb, *reinterpret_cast<float(*)[16]>(v));
+                    } else {
+                        rows::tmem_ld32(tb, *reinterpret_cast<float(*)[32]>(v));
+                        if (CW == 64) rows::tmem_ld32(tb + 32u, *reinterpret_cast<float(*)[32]>(v + 32 % CW));
+                    }
+                    tmem_wait_ld();
+                    if (c0 + CW >= NB) {   // slot drained: hand it back to the MMA warp
+                        fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(acce + slot + yy);
+                    }
+                    if (kProbes && (P.dbg & 1)) continue;
+                    if (EST == 0) {
+                        wk_stage<CW>(v, buf, ((lb * EY + yy) * sxs + lx) * 4 + d1);
+                    } else {
+                        const uint32_t ybuf = wbuf + (uint32_t)yy * 32u * rowb;
+                        wk_stage<CW>(v, ybuf, lane);
+                        __syncwarp();
+                        if (wimg < P.B) {
+                            uint8_t *gb = reinterpret_cast<uint8_t *>(P.out) +
+                                          ((((size_t)wimg * P.Ho + (y0 + yy)) * P.Wo + wx0) * 4 * (size_t)NB + c0) * 2;
+#pragma unroll
+                            for (int i = 0; i < cpr; ++i) {
+                                const int k = i * 32 + lane, r = k / cpr, j = k % cpr;
+                                if (wx0 + (r >> 2) < P.Wo) {
+                                    const uint32_t rsw = ((uint32_t)r >> zsh) & (uint32_t)(cpr - 1);
+                                    const uint4 x = ld_shared_v4(ybuf + (uint32_t)r * rowb + ((uint32_t)j ^ rsw) * 16u);
+                                    *reinterpret_cast<uint4 *>(gb + (size_t)r * NB * 2 + (size_t)j * 16) = x;
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (EST == 0) {
+                    fence_proxy_async_smem();
+                    named_bar_sync(bar_id, 128);
+                    if (leader && img0 < P.B && !(kProbes && (P.dbg & 1))) {
+                        rows::tma_store5d(&P.tmO, buf, c0, 0, xg0, y0, img0);
+                        rows::bulk_commit();
+                    }
+                }
+                ++bi;
+            }
+            slot += EY * gps;
+            if (slot >= Rw) slot -= Rw;
+        }
+    }
+    if (EST == 0 && leader) rows::bulk_wait_all();
+    if (kProbes && P.prof && e == 0 && lane == 0) {
+        unsigned long long *o = P.prof + (size_t)blockIdx.x * 8;
+        o[3] = pe_wait;
+        o[4] = pe_rows;
+        o[5] = wk_clk() - pe_start;
+    }
+}
+
 __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant__ RowsWalk P) {
     pdl_launch_dependents();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -393,92 +511,14 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
         else __trap();
     } else {
         // ------------------------------------------------------------ epilogue
-        // group g serves stream w = g / gps; its rows y = g % gps (mod gps)
-        const int e = warp - 2 * nmw, grp = e >> 2, qq = warp & 3;   // TMEM lane quarter of this warp
-        const int gps = P.nepi / nmw, w = grp / gps, gl = grp - w * gps;
-        // One TMA box store per group and row block: the group's four warps
-        // stage their 32 rows each into the group buffer (box (cw, 4, Xs, ey, G)
-        // image: row ((b*ey + yy)*Xs + x)*4 + d1), meet at a named barrier, and
-        // the group's first warp issues the store (4x fewer TMA operations than
-        // one box per warp: the TMA unit's operation rate bounds thin layers).
-        const uint32_t rowb = (uint32_t)P.cw * 2u;              // staged row bytes (= swizzle span)
-        const int EY = P.ey, nbuf = P.nbuf;
-        const uint32_t bufb = (uint32_t)EY * 128u * rowb;        // one group staging box
-        const uint32_t sbuf0 = base + P.soff + (uint32_t)(grp * nbuf) * bufb;
-        const bool leader = (e & 3) == 0 && lane == 0;
-        const int bar_id = 1 + grp;
-        const int pxl = 8 * qq + (lane >> 2), d1 = lane & 3;     // this lane's tile pixel and d1 row
-        const int Rw = P.Rw, NB = P.NB, cw = P.cw;
-        // staging row of (yy, this lane): b = pxl / Xs, x = pxl % Xs
-        const int lb = P.G > 1 ? pxl / P.Xs : 0, lx = P.G > 1 ? pxl - lb * P.Xs : pxl;
-        const int sxs = P.G > 1 ? P.Xs : 32;
-        accf += w * Rw;
-        acce += w * Rw;
-        const uint32_t tl = ((uint32_t)(qq * 32) << 16) + (uint32_t)(w * Rw * NB);
-        uint32_t eph = 0;                                        // per-slot accf phases
-        int bi = 0;
-        unsigned long long pe_wait = 0, pe_rows = 0;
-        const unsigned long long pe_start = wk_clk();
-        for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += nmw * (int)gridDim.x) {
-            const int gi = it / P.nxt, xt = it - gi * P.nxt;
-            const int img0 = gi * P.G, xg0 = P.G > 1 ? 0 : 32 * xt;
-            // row blocks [y0, y0 + EY), y0 = EY * gl (mod EY * gps): EY * gps divides Rw
-            int slot = EY * gl;
-            for (int y0 = EY * gl; y0 < P.Ho; y0 += EY * gps) {
-                const int ny = min(EY, P.Ho - y0);
-                const unsigned long long e0 = wk_clk();
-                for (int yy = 0; yy < ny; ++yy) {
-                    mbar_wait_sleep(accf + slot + yy, (eph >> (slot + yy)) & 1u);
-                    eph ^= 1u << (slot + yy);
-                }
-                if (kProbes) { pe_wait += wk_clk() - e0; pe_rows += ny; }
-                fence_after_sync();
-                for (int c0 = 0; c0 < NB; c0 += cw) {
-                    const uint32_t buf = sbuf0 + (uint32_t)(nbuf > 1 ? (bi & 1) : 0) * bufb;
-                    if (leader) {   // this buffer's previous store has read it
-                        if (nbuf > 1) rows::bulk_wait_read<1>();
-                        else rows::bulk_wait_read<0>();
-                    }
-                    named_bar_sync(bar_id, 128);
-                    for (int yy = 0; yy < ny; ++yy) {
-                        const uint32_t tb = tl + (uint32_t)((slot + yy) * NB + c0);
-                        float v[64];
-                        if (cw == 16) {
-                            tmem_ld16(tb, *reinterpret_cast<float(*)[16]>(v));
-                        } else {
-                            rows::tmem_ld32(tb, *reinterpret_cast<float(*)[32]>(v));
-                            if (cw == 64) rows::tmem_ld32(tb + 32u, *reinterpret_cast<float(*)[32]>(v + 32));
-                        }
-                        tmem_wait_ld();
-                        if (c0 + cw >= NB) {   // slot drained: hand it back to the MMA warp
-                            fence_before_sync();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(acce + slot + yy);
-                        }
-                        if (kProbes && (P.dbg & 1)) continue;
-                        const int r = ((lb * EY + yy) * sxs + lx) * 4 + d1;
-                        if (cw == 16) wk_stage<16>(v, buf, r);
-                        else if (cw == 32) wk_stage<32>(v, buf, r);
-                        else wk_stage<64>(v, buf, r);
-                    }
-                    fence_proxy_async_smem();
-                    named_bar_sync(bar_id, 128);
-                    if (leader && img0 < P.B && !(kProbes && (P.dbg & 1))) {
-                        rows::tma_store5d(&P.tmO, buf, c0, 0, xg0, y0, img0);
-                        rows::bulk_commit();
-                    }
-                    ++bi;
-                }
-                slot += EY * gps;
-                if (slot >= Rw) slot -= Rw;
-            }
-        }
-        if (leader) rows::bulk_wait_all();
-        if (kProbes && P.prof && e == 0 && lane == 0) {
-            unsigned long long *o = P.prof + (size_t)blockIdx.x * 8;
-            o[3] = pe_wait;
-            o[4] = pe_rows;
-            o[5] = wk_clk() - pe_start;
+        if (P.est == 2) {
+            if (P.cw == 16) wk_epilogue<16, 2>(P, warp, lane, base, accf, acce);
+            else if (P.cw == 32) wk_epilogue<32, 2>(P, warp, lane, base, accf, acce);
+            else wk_epilogue<64, 2>(P, warp, lane, base, accf, acce);
+        } else {
+            if (P.cw == 16) wk_epilogue<16, 0>(P, warp, lane, base, accf, acce);
+            else if (P.cw == 32) wk_epilogue<32, 0>(P, warp, lane, base, accf, acce);
+            else wk_epilogue<64, 0>(P, warp, lane, base, accf, acce);
         }
     }
     fence_before_sync();
@@ -647,6 +687,8 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // shared memory: [1024 barriers][stages][weights][row schedule][staging];
     // prefer >= 4 stages, then more epilogue groups, then double-buffered stores
     if (kProbes && probe_env("CAPSCONV_WK_DBG")) P.dbg = atoi(probe_env("CAPSCONV_WK_DBG"));
+    P.est = 0;
+    if (kProbes && probe_env("CAPSCONV_WK_EST")) P.est = atoi(probe_env("CAPSCONV_WK_EST"));
     const size_t limit = std::min<size_t>(kWkSmemLimit, device_info().smem_optin ? device_info().smem_optin : kWkSmemLimit);
     const uint32_t rbytes = 0u;   // the schedule lives in the kernel parameters
     int max_epi = 4, max_ey = 2;
