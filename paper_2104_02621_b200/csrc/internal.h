@@ -55,6 +55,9 @@ inline const char *probe_env(const char *) { return nullptr; }
 // (the attribute is per function and per device).  Thread-safe; the driver
 // call is made once per (function, device, larger size).
 cudaError_t smem_optin(const void *func, int bytes);
+// probe builds only: skip the weight-pack and split-K finalize launches (timing
+// experiments; results are then wrong)
+inline bool probe_skip_small() { return kProbes && probe_env("CAPSCONV_SKIP_SMALL") != nullptr; }
 
 // Programmatic dependent launch (PDL) for the kernels of the hot path: the
 // launch may begin while the previous kernel in the stream is still running;

@@ -464,7 +464,7 @@ cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const
             !rows::make_rows_map2(&P.tmB, b, (int64_t)P.B * 4, P.EO, 64, 128, 128))
             return cudaErrorInvalidValue;
     }
-    if (mode != 2) {
+    if (mode != 2 && !probe_skip_small()) {
         const long long total16 = (long long)pl.wpack_bytes / 16;
         e = launch_k(fc_pack, dim3((unsigned)((total16 + 255) / 256)), dim3(256), 0, st,
                      static_cast<const __nv_bfloat16 *>(b), w8, mode, P.P, P.C, P.Cout, P.N, total16);
@@ -478,7 +478,8 @@ cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const
     if (e != cudaSuccess) return e;
     note_launches(1);
     const long long mstride = (long long)P.nmt * 128 * P.N;
-    if (mode == 0) {
+    if (probe_skip_small()) {
+    } else if (mode == 0) {
         const long long n = (long long)P.B * 4 * P.EO;
         e = launch_k(fc_fin_fwd, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, static_cast<const float *>(P.part),
                      static_cast<__nv_bfloat16 *>(out), P.B * 4, P.N, P.EO, P.ksplit, mstride);

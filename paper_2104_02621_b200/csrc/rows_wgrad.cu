@@ -511,7 +511,7 @@ cudaError_t rows_wgrad_run(const Problem &p, const void *I, const void *dO, floa
     e = launch_k(rows_wgrad_kernel, dim3(grid), dim3(kRwThreads), P.smem_bytes, st, P);
     if (e != cudaSuccess) return e;
     note_launches(1);
-    if (P.ksplit > 1) {
+    if (P.ksplit > 1 && !probe_skip_small()) {
         const long long n4 = P.nK / 4;
         e = launch_k(rw_finalize, dim3((unsigned)((n4 + 31) / 32)), dim3(kFinWarps * 32), 0, st,
                      static_cast<const float *>(P.part), dK, n4, P.nK, P.ksplit);
