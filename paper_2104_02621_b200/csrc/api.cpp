@@ -247,7 +247,7 @@ static cudaError_t dispatch(capsconv_op_t op, const Problem &p, const void *a, c
     const bool mma = choose_path(op, p) == CAPSCONV_PATH_MMA && aligned16(a) && aligned16(b) && aligned16(out) &&
                      (need == 0 || aligned16(ws));
     switch (op) {
-        case CAPSCONV_OP_FWD: return mma ? mma_fwd(p, a, b, out, ws, ws_bytes, cs) : simt_fwd(p, a, b, out, cs);
+        case CAPSCONV_OP_FWD: return mma ? mma_fwd(p, a, b, out, ws, ws_bytes, cs) : simt_fwd(p, a, b, out, ws, ws_bytes, cs);
         case CAPSCONV_OP_BWD_DATA:
             return mma ? mma_bwd_data(p, a, b, out, ws, ws_bytes, cs) : simt_bwd_data(p, a, b, out, cs);
         default:

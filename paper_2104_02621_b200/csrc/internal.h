@@ -89,7 +89,8 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 
 // ---------------------------------------------------------------- SIMT path
 size_t simt_workspace_bytes(capsconv_op_t op, const Problem &p);
-cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, cudaStream_t st);
+cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
+                     cudaStream_t st);
 cudaError_t simt_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, cudaStream_t st);
 cudaError_t simt_bwd_kernel(const Problem &p, const void *I, const void *dO, float *dK,
                             void *ws, size_t ws_bytes, cudaStream_t st);

@@ -620,7 +620,8 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // for thin rows
     P.nmw = P.R / 3 >= nmax + 2 ? 3 : P.R / 2 >= nmax + 2 ? 2 : 1;
     if (kProbes && probe_env("CAPSCONV_WK_NMW")) P.nmw = std::max(1, std::min(3, atoi(probe_env("CAPSCONV_WK_NMW"))));
-    if (P.R / P.nmw < nmax + 2) P.nmw = 1;
+    const int slack = kProbes && probe_env("CAPSCONV_WK_SLACK") ? atoi(probe_env("CAPSCONV_WK_SLACK")) : 2;
+    if (P.R / P.nmw < nmax + slack) P.nmw = 1;
     P.Rw = P.R / P.nmw;
     // columns: plane q mod s, shift q / s (fwd); one plane, shift KW-1-q (dI)
     P.npl = dgrad ? 1 : s;

@@ -84,7 +84,7 @@ struct Dims {
 // Thread = (b, x', y', group of CG output channels); acc[CG][d1][d3].
 template <typename T, int CG>
 __global__ void __launch_bounds__(128) fwd_d4(Dims d, const T *__restrict__ I, const T *__restrict__ K,
-                                              T *__restrict__ O) {
+                                              T *__restrict__ O, float *__restrict__ part, int nsplit) {
     const int64_t ngroups = (d.Cout + CG - 1) / CG;
     const int64_t total = d.B * d.Ho * d.Wo * ngroups;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -100,10 +100,14 @@ __global__ void __launch_bounds__(128) fwd_d4(Dims d, const T *__restrict__ I, c
     for (int j = 0; j < CG; ++j)
 #pragma unroll
         for (int e = 0; e < 16; ++e) acc[j][e] = 0.f;
-    for (int64_t p = 0; p < d.KH; ++p) {
+    // split blockIdx.y of nsplit takes the taps [t0, t1) (fixed ranges: the
+    // partials are summed in split order, deterministic)
+    const int64_t ntap = d.KH * d.KW, t0 = ntap * blockIdx.y / nsplit, t1 = ntap * (blockIdx.y + 1) / nsplit;
+    for (int64_t t = t0; t < t1; ++t) {
+        const int64_t p = t / d.KW, q = t - p * d.KW;
         const int64_t h = x * d.s + p - d.pad;
         if (h < 0 || h >= d.H) continue;
-        for (int64_t q = 0; q < d.KW; ++q) {
+        {
             const int64_t w = y * d.s + q - d.pad;
             if (w < 0 || w >= d.W) continue;
             const T *ip = I + (((b * d.H + h) * d.W + w) * d.C) * 16;
@@ -128,10 +132,17 @@ __global__ void __launch_bounds__(128) fwd_d4(Dims d, const T *__restrict__ I, c
             }
         }
     }
-    T *op = O + (((b * d.Ho + x) * d.Wo + y) * d.Cout + co0) * 16;
+    const int64_t oo = (((b * d.Ho + x) * d.Wo + y) * d.Cout + co0) * 16;
+    if (nsplit > 1) {
+        float *pp = part + (int64_t)blockIdx.y * (d.B * d.Ho * d.Wo * d.Cout * 16) + oo;
+#pragma unroll
+        for (int j = 0; j < CG; ++j)
+            if (co0 + j < d.Cout) store_caps16<float>(pp + j * 16, acc[j]);
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < CG; ++j)
-        if (co0 + j < d.Cout) store_caps16<T>(op + j * 16, acc[j]);
+        if (co0 + j < d.Cout) store_caps16<T>(O + oo + j * 16, acc[j]);
 }
 
 template <typename T>
@@ -163,20 +174,26 @@ __global__ void __launch_bounds__(256) fwd_gen(Dims d, const T *__restrict__ I, 
 
 // ============================================================ backward data
 // Thread = (b, h, w, c) input capsule; acc[d1][d2] (gather form).
-template <typename T>
+// Thread = (b, h, w, group of CG input channels); acc[CG][d1][d2]: each dO
+// capsule is loaded once per (tap, c') and reused for the CG channels.
+template <typename T, int CG>
 __global__ void __launch_bounds__(128) bwd_data_d4(Dims d, const T *__restrict__ dO, const T *__restrict__ K,
                                                    T *__restrict__ dI) {
-    const int64_t total = d.B * d.H * d.W * d.C;
+    const int64_t ngroups = (d.C + CG - 1) / CG;
+    const int64_t total = d.B * d.H * d.W * ngroups;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= total) return;
     int64_t r = idx;
-    const int64_t c = r % d.C; r /= d.C;
+    const int64_t g = r % ngroups; r /= ngroups;
     const int64_t w = r % d.W; r /= d.W;
     const int64_t h = r % d.H;
     const int64_t b = r / d.H;
-    float acc[16];
+    const int64_t c0 = g * CG;
+    float acc[CG][16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+    for (int j = 0; j < CG; ++j)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[j][e] = 0.f;
     for (int64_t p = 0; p < d.KH; ++p) {
         const int64_t hx = h + d.pad - p;
         if (hx < 0 || hx % d.s) continue;
@@ -188,22 +205,31 @@ __global__ void __launch_bounds__(128) bwd_data_d4(Dims d, const T *__restrict__
             const int64_t y = wy / d.s;
             if (y >= d.Wo) continue;
             const T *gp = dO + ((b * d.Ho + x) * d.Wo + y) * d.Cout * 16;
-            const T *kp = K + (((p * d.KW + q) * d.C + c) * d.Cout) * 16;
+            const T *kp = K + (((p * d.KW + q) * d.C + c0) * d.Cout) * 16;
             for (int64_t co = 0; co < d.Cout; ++co) {
-                float g[16], k[16];
-                load_caps16<T>(gp + co * 16, g);
-                load_caps16<T>(kp + co * 16, k);
+                float gv[16];
+                load_caps16<T>(gp + co * 16, gv);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int j = 0; j < CG; ++j) {
+                    if (c0 + j < d.C) {
+                        float k[16];
+                        load_caps16<T>(kp + ((int64_t)j * d.Cout + co) * 16, k);
 #pragma unroll
-                    for (int t = 0; t < 4; ++t)
+                        for (int i = 0; i < 4; ++i)
 #pragma unroll
-                        for (int n = 0; n < 4; ++n)
-                            acc[i * 4 + t] = fmaf(g[i * 4 + n], k[t * 4 + n], acc[i * 4 + t]);
+                            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                                for (int n = 0; n < 4; ++n)
+                                    acc[j][i * 4 + t] = fmaf(gv[i * 4 + n], k[t * 4 + n], acc[j][i * 4 + t]);
+                    }
+                }
             }
         }
     }
-    store_caps16<T>(dI + idx * 16, acc);
+    T *ip = dI + (((b * d.H + h) * d.W + w) * d.C + c0) * 16;
+#pragma unroll
+    for (int j = 0; j < CG; ++j)
+        if (c0 + j < d.C) store_caps16<T>(ip + j * 16, acc[j]);
 }
 
 template <typename T>
@@ -325,6 +351,17 @@ __global__ void __launch_bounds__(256) reduce_splits(const float *__restrict__ p
     out[idx] = acc;
 }
 
+// Fixed-order sum of forward tap-split partials into T outputs.
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_splits_to(const float *__restrict__ part, T *__restrict__ out,
+                                                        int64_t n, int64_t nsplit) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n) return;
+    float acc = 0.f;
+    for (int64_t s = 0; s < nsplit; ++s) acc += part[s * n + idx];
+    out[idx] = static_cast<T>(acc);
+}
+
 Dims dims_of(const Problem &p) {
     return Dims{p.B, p.H, p.W, p.C, p.Cout, p.KH, p.KW, p.D1, p.D2, p.D3, p.s, p.Ho, p.Wo, p.pad};
 }
@@ -346,17 +383,39 @@ int64_t dk_splits(const Problem &p) {
     return s;
 }
 
+// Tap splits of the vectorised forward: when few output capsule groups exist
+// (the FC layer: B*Cout/4 threads, each a 64-tap reduction) the taps are split
+// over blockIdx.y into fp32 partials, summed in split order afterwards.
+int64_t fwd_splits(const Problem &p) {
+    if (!is_d4(p)) return 1;
+    const int64_t units = p.B * p.Ho * p.Wo * (p.Cout >= 4 ? (p.Cout + 3) / 4 : p.Cout);
+    const int64_t target = (int64_t)device_info().num_sms * 1024;
+    int64_t s = units >= target ? 1 : (target + units - 1) / units;
+    if (s > p.KH * p.KW) s = p.KH * p.KW;
+    while (s > 1 && (size_t)s * (size_t)p.n_out() * 4 > ((size_t)64 << 20)) --s;
+    return s < 1 ? 1 : s;
+}
+
 template <typename T>
-cudaError_t fwd_impl(const Problem &p, const void *I, const void *K, void *O, cudaStream_t st) {
+cudaError_t fwd_impl(const Problem &p, const void *I, const void *K, void *O, void *ws, cudaStream_t st) {
     const Dims d = dims_of(p);
-    const bool vec = is_d4(p) && ((uintptr_t)I % 16 == 0) && ((uintptr_t)K % 16 == 0) && ((uintptr_t)O % 16 == 0);
+    const bool vec = is_d4(p) && ((uintptr_t)I % 16 == 0) && ((uintptr_t)K % 16 == 0) && ((uintptr_t)O % 16 == 0) &&
+                     ((uintptr_t)ws % 16 == 0);
     if (vec) {
+        const int64_t nsplit = ws ? fwd_splits(p) : 1;
+        float *part = static_cast<float *>(ws);
         if (p.Cout >= 4) {
             const int64_t n = p.B * p.Ho * p.Wo * ((p.Cout + 3) / 4);
-            fwd_d4<T, 4><<<blocks_for(n, 128), 128, 0, st>>>(d, (const T *)I, (const T *)K, (T *)O);
+            fwd_d4<T, 4><<<dim3(blocks_for(n, 128), (unsigned)nsplit), 128, 0, st>>>(d, (const T *)I, (const T *)K,
+                                                                                  (T *)O, part, (int)nsplit);
         } else {
             const int64_t n = p.B * p.Ho * p.Wo * p.Cout;
-            fwd_d4<T, 1><<<blocks_for(n, 128), 128, 0, st>>>(d, (const T *)I, (const T *)K, (T *)O);
+            fwd_d4<T, 1><<<dim3(blocks_for(n, 128), (unsigned)nsplit), 128, 0, st>>>(d, (const T *)I, (const T *)K,
+                                                                                  (T *)O, part, (int)nsplit);
+        }
+        if (nsplit > 1) {
+            note_launches(1);
+            reduce_splits_to<T><<<blocks_for(p.n_out(), 256), 256, 0, st>>>(part, (T *)O, p.n_out(), nsplit);
         }
     } else {
         fwd_gen<T><<<blocks_for(p.n_out(), 256), 256, 0, st>>>(d, (const T *)I, (const T *)K, (T *)O);
@@ -370,8 +429,13 @@ cudaError_t bwd_data_impl(const Problem &p, const void *dO, const void *K, void 
     const Dims d = dims_of(p);
     const bool vec = is_d4(p) && ((uintptr_t)dO % 16 == 0) && ((uintptr_t)K % 16 == 0) && ((uintptr_t)dI % 16 == 0);
     if (vec) {
-        const int64_t n = p.B * p.H * p.W * p.C;
-        bwd_data_d4<T><<<blocks_for(n, 128), 128, 0, st>>>(d, (const T *)dO, (const T *)K, (T *)dI);
+        if (p.C >= 4) {
+            const int64_t n = p.B * p.H * p.W * ((p.C + 3) / 4);
+            bwd_data_d4<T, 4><<<blocks_for(n, 128), 128, 0, st>>>(d, (const T *)dO, (const T *)K, (T *)dI);
+        } else {
+            const int64_t n = p.B * p.H * p.W * p.C;
+            bwd_data_d4<T, 1><<<blocks_for(n, 128), 128, 0, st>>>(d, (const T *)dO, (const T *)K, (T *)dI);
+        }
     } else {
         bwd_data_gen<T><<<blocks_for(p.n_in(), 256), 256, 0, st>>>(d, (const T *)dO, (const T *)K, (T *)dI);
     }
@@ -406,14 +470,20 @@ cudaError_t bwd_kernel_impl(const Problem &p, const void *I, const void *dO, flo
 }  // namespace
 
 size_t simt_workspace_bytes(capsconv_op_t op, const Problem &p) {
+    if (op == CAPSCONV_OP_FWD) {
+        const int64_t s = fwd_splits(p);
+        return s <= 1 ? 0 : (size_t)s * (size_t)p.n_out() * sizeof(float);
+    }
     if (op != CAPSCONV_OP_BWD_KERNEL) return 0;
     const int64_t s = dk_splits(p);
     if (s <= 1) return 0;
     return (size_t)s * (size_t)p.n_k() * sizeof(float);
 }
 
-cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, cudaStream_t st) {
-    return p.dt == CAPSCONV_BF16 ? fwd_impl<__nv_bfloat16>(p, I, K, O, st) : fwd_impl<float>(p, I, K, O, st);
+cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
+                     cudaStream_t st) {
+    if (ws_bytes < simt_workspace_bytes(CAPSCONV_OP_FWD, p)) ws = nullptr;   // no room: no tap split
+    return p.dt == CAPSCONV_BF16 ? fwd_impl<__nv_bfloat16>(p, I, K, O, ws, st) : fwd_impl<float>(p, I, K, O, ws, st);
 }
 
 cudaError_t simt_bwd_data(const Problem &p, const void *dO, const void *K, void *dI, cudaStream_t st) {
