@@ -36,9 +36,27 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def full_summaries(caps, rnd, traffic):
+# Round 2, final build (tests/probe/prof_r2b.sh): every rows kernel of the stack
+CAPS_R2B = [("L%d_%s" % (l, o), "r2b_L%d_%s.ncu-rep" % (l, o), 0, desc) for (l, o, desc) in [
+    (1, "fwd", "rows_walk_kernel fwd s1: 3 row taps stacked in N=96, 3 TMA+MMA streams"),
+    (1, "dI", "rows_walk_kernel dI s1"),
+    (1, "dK", "rows_wgrad_kernel"),
+    (2, "fwd", "rows_walk_kernel fwd s2 (phase planes), 2 streams"),
+    (2, "dI", "rows_conv_kernel dI s2 (output phases)"),
+    (2, "dK", "rows_wgrad_kernel s2"),
+    (3, "fwd", "rows_conv_kernel fwd, N=128 per tap"),
+    (3, "dI", "rows_walk_kernel dI, N=192, one stream"),
+    (3, "dK", "rows_wgrad_kernel"),
+    (4, "fwd", "rows_fc_kernel mode 0 (split-K GEMM)"),
+    (4, "dI", "rows_fc_kernel mode 1 (N=256 tiles, coalesced stores)"),
+    (4, "dK", "rows_fc_kernel mode 2")]]
+
+
+def full_summaries(caps, rnd, traffic, tag=None, src=None):
+    tag = tag or "r%d" % rnd
+    src = src or (PROF if rnd == 1 else PROF)
     out = ["# Round %d ncu --set full captures (one launch each, --clock-control none, bf16, 1 B200)" % rnd,
-           "# commands: " + ("tests/probe/run_layer.py / capture_ops.py" if rnd == 1 else "tests/probe/prof_r2.sh") +
+           "# commands: " + ("tests/probe/run_layer.py / capture_ops.py" if rnd == 1 else "tests/probe/prof_%s.sh" % tag) +
            " under ncu --set full -k regex:<kernel>",
            "# (cache control on: cold L2; shares/stalls matter, not the absolute time; dram writes still dirty",
            "#  in the 126 MB L2 when the kernel ends are not counted, so writes can read below the algorithmic bytes)",
@@ -46,11 +64,14 @@ def full_summaries(caps, rnd, traffic):
     for name, f, row, desc in caps:
         path = os.path.join(PROF, f)
         if not os.path.exists(path):
+            path = os.path.join(ROOT, "gpurun_out", f)
+        if not os.path.exists(path):
             continue
         raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         r = list(csv.reader(raw.splitlines()))
         h, u, v = r[0], r[1], r[2 + row]
-        out.append("[%s]  (profiles/%s)  %s" % (name, f, desc))
+        where = "profiles/" + f if path.startswith(PROF) else f + ", summary only (report not committed)"
+        out.append("[%s]  (%s)  %s" % (name, where, desc))
         d = {}
         for k in KEYS:
             if k in h:
@@ -59,14 +80,15 @@ def full_summaries(caps, rnd, traffic):
                 d[k] = (float(v[i].replace(",", "")), u[i])
         tb = int(d["dram__bytes_read.sum"][0] * SCALE[d["dram__bytes_read.sum"][1]] +
                  d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]])
-        traffic[name if rnd == 2 else "r1_" + name] = tb
+        traffic[name if tag == "r2b" else tag + "_" + name] = tb
         out.append("  %-80s %d" % ("dram read+write bytes per launch", tb))
         out.append("")
-    open(os.path.join(PROF, "r%d_ncu_full_summary.txt" % rnd), "w").write("\n".join(out) + "\n")
+    open(os.path.join(PROF, "%s_ncu_full_summary.txt" % tag), "w").write("\n".join(out) + "\n")
 
 
-def launches(rnd, cmd):
-    rows = [r for r in csv.reader(open(os.path.join(PROF, "r%d_stack_launches.csv" % rnd))) if len(r) > 5]
+def launches(rnd, cmd, tag=None):
+    tag = tag or "r%d" % rnd
+    rows = [r for r in csv.reader(open(os.path.join(PROF, "%s_stack_launches.csv" % tag))) if len(r) > 5]
     h, data = rows[0], rows[1:]
     iK, iV, iU = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     agg, tot = collections.OrderedDict(), 0.0
@@ -77,23 +99,26 @@ def launches(rnd, cmd):
         a[0] += 1
         a[1] += val
         tot += val
-    out = ["# r%d launch list: ncu --metrics gpu__time_duration.sum --clock-control none" % rnd,
+    out = ["# %s launch list: ncu --metrics gpu__time_duration.sum --clock-control none" % tag,
            "# command: python bench.py %s --no-cpu-baseline (eager warm-up steps, graph capture," % cmd,
            "#          graph replays, L2 flush fills); ncu times are cold-cache and serialised: compare SHARES",
            "launches %d, total %.1f us" % (len(data), tot / 1e3)]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         out.append("%-22s n=%4d total=%9.1f us share=%5.1f%% avg=%7.1f us" % (k, n, t / 1e3, 100 * t / tot, t / n / 1e3))
-    open(os.path.join(PROF, "r%d_stack_launches_summary.txt" % rnd), "w").write("\n".join(out) + "\n")
+    open(os.path.join(PROF, "%s_stack_launches_summary.txt" % tag), "w").write("\n".join(out) + "\n")
     print("\n".join(out))
 
 
 if __name__ == "__main__":
     traffic = {}
     full_summaries(CAPS, 1, traffic)
-    full_summaries(CAPS_R2, 2, traffic)
+    full_summaries(CAPS_R2, 2, traffic, tag="r2a")
+    full_summaries(CAPS_R2B, 2, traffic, tag="r2b")
     traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the ncu --set full "
-                        "captures in profiles/ (tests/probe/profile_summary.py); unprefixed keys: round 2 "
-                        "(rows layout, the kernels bench.py times); r1_*: round-1 natural-layout kernels")
+                        "captures in profiles/ (tests/probe/profile_summary.py); unprefixed keys: round-2 final build "
+                        "(r2b captures of the kernels bench.py times); r2a_*: earlier round-2 rows kernels; r1_*: "
+                        "round-1 natural-layout kernels")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     launches(1, "--steps 3 --warmup 3")
-    launches(2, "--steps 2 --warmup 1")
+    launches(2, "--steps 2 --warmup 1", tag="r2")
+    launches(2, "--steps 2 --warmup 1 --no-parity", tag="r2b")
