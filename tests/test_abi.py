@@ -127,7 +127,10 @@ def test_select_path_is_total(cc):
 def test_no_device_error(cc):
     lib = _raw(cc)
     fake = ctypes.c_void_p(0x1000)
-    st = lib.capsconv_fwd(0, *EXT_OK, fake, fake, fake, None, 0, None)
+    # a workspace of the required size, so that the device check is what fails
+    need = ctypes.c_size_t()
+    assert lib.capsconv_workspace_bytes(0, 0, *EXT_OK, ctypes.byref(need)) == 0
+    st = lib.capsconv_fwd(0, *EXT_OK, fake, fake, fake, fake if need.value else None, need.value, None)
     assert st == 7
 
 
