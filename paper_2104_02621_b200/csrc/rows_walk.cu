@@ -71,7 +71,6 @@ struct RowsWalk {
     uint32_t woff_s, wbytes, soff, sbytes;   // shared offsets (from the 1024-aligned base): weights, staging
     uint32_t roff;                 // shared offset of the per-source-row schedule (32 B per row)
     int ey;                        // output rows per epilogue store box
-    int espin;                     // epilogue waits: 1 poll, 0 suspend with a time hint
     int est;                       // epilogue stores: 0 one TMA box per group, 2 per-warp coalesced 16-byte stores
     int rps;                       // source rows per pipeline step (1 or 2): stage = rps rows x planes of one chunk
     __nv_bfloat16 *out;
@@ -693,8 +692,6 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // shared memory: [1024 barriers][stages][weights][row schedule][staging];
     // prefer >= 4 stages, then more epilogue groups, then double-buffered stores
     if (kProbes && probe_env("CAPSCONV_WK_DBG")) P.dbg = atoi(probe_env("CAPSCONV_WK_DBG"));
-    P.espin = 0;
-    if (kProbes && probe_env("CAPSCONV_WK_ESPIN")) P.espin = atoi(probe_env("CAPSCONV_WK_ESPIN"));
     P.est = 0;
     if (kProbes && probe_env("CAPSCONV_WK_EST")) P.est = atoi(probe_env("CAPSCONV_WK_EST"));
     const size_t limit = std::min<size_t>(kWkSmemLimit, device_info().smem_optin ? device_info().smem_optin : kWkSmemLimit);

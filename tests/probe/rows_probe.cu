@@ -413,3 +413,55 @@ extern "C" double tmem_bw(int nwarps, int iters) {
     if (e != cudaSuccess) return -1.0;
     return (double)nwarps * iters * 4096.0 / (double)h;   // bytes per cycle per SM
 }
+
+// ---------------------------------------------------------------------------
+// MMA queue depth: the issuing warp alternates K back-to-back 128xNx16 MMAs
+// (uniform operands, one warp, elect per MMA) with `spin` dependent uniform
+// integer steps of bookkeeping.  cycles/iteration ~ max(K*t_mma, spin + issue)
+// if the tensor pipe queues the MMAs, ~ K*t_mma + spin if the issuing warp
+// waits for them.
+__global__ void queue_bench_kernel(int N, int K, int spin, int iters, unsigned long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_base;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
+    if (warp == 0) tmem_alloc<512>(&tmem_base);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    if (warp == 0) {
+        const uint32_t sa = (smem_u32(smem) + 1023u) & ~1023u, sb = sa + 32768;
+        const uint64_t ad = desc(sa, 16, 512, 64);
+        const uint64_t bd = desc(sb, 16, 512, 64);
+        const uint32_t idesc = idesc_bf16(128, N, 0, 0);
+        uint32_t x = (uint32_t)clock();
+        const unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            for (int k = 0; k < K; ++k) {
+                asm volatile(
+                    "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(0u),
+                    "l"(ad + (uint64_t)((k & 1) * 2)), "l"(bd), "r"(idesc), "r"(1u));
+            }
+            for (int j = 0; j < spin; ++j) x = x * 1664525u + 1013904223u;   // dependent bookkeeping
+        }
+        const unsigned long long t1 = clock64();
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) out[0] = (t1 - t0) / (unsigned long long)iters, out[1] = x;
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem_base);
+}
+
+extern "C" double queue_bench(int N, int K, int spin, int iters) {
+    unsigned long long *d;
+    cudaMalloc(&d, 16);
+    const int smem = 65536 + 1024;
+    cudaFuncSetAttribute(queue_bench_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    queue_bench_kernel<<<148, 64, smem>>>(N, K, spin, iters, d);
+    unsigned long long h[2] = {0, 0};
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return -1.0;
+    return (double)h[0];
+}

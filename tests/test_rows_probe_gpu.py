@@ -37,6 +37,8 @@ def load_probe():
     lib.tile_bench.restype = ctypes.c_double
     lib.tmem_bw.argtypes = [ctypes.c_int] * 2
     lib.tmem_bw.restype = ctypes.c_double
+    lib.queue_bench.argtypes = [ctypes.c_int] * 4
+    lib.queue_bench.restype = ctypes.c_double
     return lib
 
 
@@ -105,6 +107,14 @@ if __name__ == "__main__":
         for mode, name in ((0, "commit->wait round trip"), (1, "commit issue"), (2, "mbarrier hand-off x2")):
             for nb in (1, 148):
                 print("sync %-24s blocks %3d: %.1f cycles" % (name, nb, lib.sync_bench(mode, 2000, nb)))
+        sys.exit(0)
+    if "--queue" in sys.argv:
+        for N in (96, 192):
+            for K in (1, 2, 4, 8):
+                row = []
+                for spin in (0, 100, 200, 400, 800):
+                    row.append("spin %3d: %6.0f" % (spin, lib.queue_bench(N, K, spin, 200)))
+                print("queue N %3d K %d  " % (N, K) + "  ".join(row), flush=True)
         sys.exit(0)
     if "--tmem" in sys.argv:
         for nw in (1, 4, 8, 16):
