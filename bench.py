@@ -5,8 +5,11 @@ Metric (BASELINE.json): capsule-conv TFLOP/s fwd+bwd, and % of the HBM /
 tensor roofline.  Default workload (N = 1): BASELINE.json configs[4], the
 CapsNet stack -- 3 capsule conv layers + the FC capsule layer -- forward and
 backward on a global batch of 1024, bf16, synthetic seeded inputs and
-random-init weights.  With torchrun (N > 1) the global batch is sharded across
-the ranks and every layer's dK is all-reduced over NCCL ("strong" scaling).
+random-init weights.  With N > 1 ranks (torchrun, or --gpus N self-launch)
+every rank runs its own batch of 1024 images -- the batch is the unit the path
+partitions (tier rule 5: shard the units, report "weak" scaling) -- and every
+layer's dK is all-reduced over NCCL, the path's one exchange step.
+`--scaling strong` instead shards the global batch of 1024 across the ranks.
 
 A step = forward of every layer + (dK, dI) of every layer in reverse order
 (+ the dK all-reduces).  Algorithmic flops per layer pass = 2*M*N*K with
@@ -54,6 +57,11 @@ def parse():
     ap.add_argument("--layout", default="rows", choices=["rows", "natural"],
                     help="capsule-tensor layout of the stack's activations (include/capsconv.h)")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-bench oracle parity check")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = 1024 images per rank (default), strong = 1024 images shared by the ranks")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="override the global batch (e.g. 128/256/512: one rank's share of the batch-1024 stack "
+                         "at 8/4/2 GPUs -- the compute side of strong scaling on one GPU)")
     return ap.parse_args()
 
 
@@ -466,6 +474,11 @@ def main():
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     elem = 2 if dtype == torch.bfloat16 else 4
     specs, H, W, D, gbatch, name = workload(args.config, world)
+    if args.scaling == "weak" and world > 1 and not args.batch:
+        gbatch *= world      # every rank keeps the single-GPU batch
+    if args.batch:
+        gbatch = args.batch
+        name = name.rsplit("_b", 1)[0] + "_b%d" % gbatch if "_b" in name else name + "_b%d" % gbatch
     lo, hi = shard_range(gbatch, rank, world)
     batch = hi - lo
 
@@ -590,6 +603,12 @@ def main():
         sm_mhz = clk.max_mhz or 1965
         cpeak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
         cbound = "alu"
+        try:   # the FFMA microbenchmark's figure (tests/probe/ffma_peak.cu) when it has been run on this pool
+            with open(os.path.join(ROOT, "profiles", "r2_ffma_peak.json")) as f:
+                cpeak = float(json.load(f)["ffma_tflops"])
+            peaks["src"] = "measured FFMA peak (profiles/r2_ffma_peak.json)"
+        except Exception:
+            pass
     per_pass, best = {}, None
     t_roof_sum = 0.0
     for (li, kind), v in sorted(calls.items()):
@@ -627,8 +646,8 @@ def main():
                     "frac": round(achieved / peaks["hbm_gbs"], 4)}
     roofline.update({"traffic": traffic, "kernel": "L%d_%s" % (bli + 1, bkind), "bytes_per_launch": bbytes,
                      "flops_per_launch": bflops,
-                     "peak_src": peaks["src"] if dtype == torch.bfloat16 or t_tc <= t_hbm else
-                     "derived: SMs x 128 FFMA lanes x 2 x max SM clock",
+                     "peak_src": peaks["src"] if dtype == torch.bfloat16 or t_tc <= t_hbm or "FFMA" in peaks["src"]
+                     else "derived: SMs x 128 FFMA lanes x 2 x max SM clock",
                      "step_frac": round(t_roof_sum / ms, 4)})
 
     # ---- e2e: same steps through the public API with host buffers.  Every
@@ -726,7 +745,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max, 5), "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 5), "higher_is_better": True,
+            "scaling": args.scaling if world > 1 else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded capsinputs; random-init weights)",
             "config": {"workload": name, "global_batch": gbatch, "per_rank_batch": batch,
                        "layers": ["%dx%d s%d%s %d->%d" % (s.KH, s.KW, s.stride, " p%d" % s.pad if s.pad else "", s.C,
