@@ -261,7 +261,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": name, "global_batch": gbatch, "sample_batch": b, "io_dtype": args.dtype},
         "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                          "sample": "oracle (C, fp64, OpenMP) %s fwd+bwd on %d of %d images per step" % (name, b, gbatch)},
@@ -435,7 +435,7 @@ def run_paper_alg34(args, rank, world):
     ms = sum(ts) / len(ts)
     line = {"impl": "paper-alg34", "metric": METRIC, "value": round(flops / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded capsinputs)",
             "config": {"workload": name, "global_batch": gbatch,
                        "scheme": "PAPER.md Alg 3/4: materialised capsule_im2col, input/kernel/output extends, "
