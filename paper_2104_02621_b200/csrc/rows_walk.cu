@@ -71,6 +71,9 @@ struct RowsWalk {
     uint32_t woff_s, wbytes, soff, sbytes;   // shared offsets (from the 1024-aligned base): weights, staging
     uint32_t roff;                 // shared offset of the per-source-row schedule (32 B per row)
     int ey;                        // output rows per epilogue store box
+    int dyn;                       // streams take strips from a CTA-shared counter (see wk_take)
+    uint32_t foff;                 // shared offset (from the 1024-aligned base) of the strip lists
+    int espin;                     // epilogue waits: 1 poll (try_wait loop), 0 suspend with a time hint
     int est;                       // epilogue stores: 0 one TMA box per group, 2 per-warp coalesced 16-byte stores
     int rps;                       // source rows per pipeline step (1 or 2): stage = rps rows x planes of one chunk
     __nv_bfloat16 *out;
@@ -165,9 +168,45 @@ __device__ __forceinline__ void wk_mma_seg(uint32_t sg, uint32_t dbase, uint64_t
                        ibase | ((sg >> 21) << 17), acc);
 }
 
+// Strip assignment.  Static: stream w of a CTA takes the CTA's strips
+// w, w + nmw, ...; dynamic (P.dyn): the streams' TMA warps take the CTA's
+// strips from a shared counter in the order they finish (the CTA's 6-7 strips
+// split 3/2/2 over three streams statically), and publish each taken strip --
+// or -1 at the end -- in a per-stream list of single-use mbarrier slots that
+// the stream's MMA warp and epilogue groups read in the same order.
+constexpr int kWkFifo = 16;
+struct WkFifo {
+    uint64_t *bar;   // [3][kWkFifo]
+    int *id;         // [3][kWkFifo]
+    int *ctr;
+};
+__device__ __forceinline__ int wk_take(const RowsWalk &P, const WkFifo &F, int w, int e) {   // TMA warp lane 0
+    int it;
+    if (P.dyn) {
+        const int k = atomicAdd(F.ctr, 1);
+        it = blockIdx.x + k * (int)gridDim.x;
+        if (it >= P.n_items) it = -1;
+        F.id[w * kWkFifo + e] = it;
+        mbar_arrive(F.bar + w * kWkFifo + e);   // release: the id is visible to the waiters
+    } else {
+        it = blockIdx.x + (w + P.nmw * e) * (int)gridDim.x;
+        if (it >= P.n_items) it = -1;
+    }
+    return it;
+}
+__device__ __forceinline__ int wk_read(const RowsWalk &P, const WkFifo &F, int w, int e) {   // MMA / epilogue warps
+    if (!P.dyn) {
+        const int it = blockIdx.x + (w + P.nmw * e) * (int)gridDim.x;
+        return it < P.n_items ? it : -1;
+    }
+    mbar_wait(F.bar + w * kWkFifo + e, 0u);
+    return *(volatile int *)(F.id + w * kWkFifo + e);
+}
+
 template <int KWT, int KPC>
 __device__ __forceinline__ void wk_mma(const RowsWalk &P, int w, uint32_t stg0, uint32_t wsm, uint32_t sched,
-                                       uint64_t *full, uint64_t *empty, uint64_t *accf, uint64_t *acce) {
+                                       uint64_t *full, uint64_t *empty, uint64_t *accf, uint64_t *acce,
+                                       const WkFifo &F) {
     const int swz = 2 * P.Ea;
     const uint32_t sbo_a = 16u * (uint32_t)P.Ea;              // 8 rows of 2*Ea bytes
     const uint64_t a0 = rows::sdesc(stg0, 16u, sbo_a, swz);
@@ -200,7 +239,8 @@ __device__ __forceinline__ void wk_mma(const RowsWalk &P, int w, uint32_t stg0, 
     const unsigned long long pstart = wk_clk();
     const int rps = P.rps;                                       // source rows per pipeline step
     const uint32_t rowb16 = (uint32_t)P.npl * (P.plane_bytes >> 4);  // next row of a step
-    for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += P.nmw * (int)gridDim.x) {
+    for (int e = 0;; ++e) {
+        if (wk_read(P, F, w, e) < 0) break;
         for (int r0 = 0; r0 < nrow; r0 += rps) {
             // the step's rows: records, then the slots their first touches need
             uint4 h0[2], h1[2];
@@ -310,7 +350,7 @@ __device__ __forceinline__ void wk_stage(const float *v, uint32_t buf, int r) {
 // warp issues one TMA store.
 template <int CW, int EST>
 __device__ __forceinline__ void wk_epilogue(const RowsWalk &P, int warp, int lane, uint32_t base, uint64_t *accf,
-                                            uint64_t *acce) {
+                                            uint64_t *acce, const WkFifo &F) {
     const int nmw = P.nmw;
     const int e = warp - 2 * nmw, grp = e >> 2, qq = warp & 3;
     const int gps = P.nepi / nmw, w = grp / gps, gl = grp - w * gps;
@@ -335,7 +375,9 @@ __device__ __forceinline__ void wk_epilogue(const RowsWalk &P, int warp, int lan
     int bi = 0;
     unsigned long long pe_wait = 0, pe_rows = 0;
     const unsigned long long pe_start = wk_clk();
-    for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += nmw * (int)gridDim.x) {
+    for (int fe = 0;; ++fe) {
+        const int it = wk_read(P, F, w, fe);
+        if (it < 0) break;
         const int gi = it / P.nxt, xt = it - gi * P.nxt;
         const int img0 = gi * P.G, xg0 = P.G > 1 ? 0 : 32 * xt;
         const int wimg = img0 + wimg_off, wx0 = xg0 + wx_off;
@@ -344,7 +386,8 @@ __device__ __forceinline__ void wk_epilogue(const RowsWalk &P, int warp, int lan
             const int ny = min(EY, P.Ho - y0);
             const unsigned long long e0 = wk_clk();
             for (int yy = 0; yy < ny; ++yy) {
-                mbar_wait_sleep(accf + slot + yy, (eph >> (slot + yy)) & 1u);
+                if (P.espin) mbar_wait(accf + slot + yy, (eph >> (slot + yy)) & 1u);
+                else mbar_wait_sleep(accf + slot + yy, (eph >> (slot + yy)) & 1u);
                 eph ^= 1u << (slot + yy);
             }
             if (kProbes) { pe_wait += wk_clk() - e0; pe_rows += ny; }
@@ -429,10 +472,18 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
     const uint32_t base = (smem_u32(smem_raw) + 1024u + 1023u) & ~1023u;
     const uint32_t stg0 = base, wsm = base + P.woff_s, sched = base + P.roff;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+    WkFifo F;
+    F.bar = reinterpret_cast<uint64_t *>(smem_raw + (base - smem_u32(smem_raw)) + P.foff);
+    F.id = reinterpret_cast<int *>(F.bar + 3 * kWkFifo);
+    F.ctr = F.id + 3 * kWkFifo;
     if (threadIdx.x == 0) {
         for (int i = 0; i < P.nstg * P.nmw; ++i) {
             mbar_init(full + i, 1);
             mbar_init(empty + i, 1);
+        }
+        if (P.dyn) {
+            for (int i = 0; i < 3 * kWkFifo; ++i) mbar_init(F.bar + i, 1);
+            *F.ctr = 0;
         }
         for (int i = 0; i < P.R; ++i) {
             mbar_init(accf + i, 1);
@@ -465,7 +516,9 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
             uint32_t ph = 0;
             unsigned long long pt_wait = 0;
             const int nrow = P.ys_hi - P.ys_lo + 1;
-            for (int it = blockIdx.x + w * (int)gridDim.x; it < P.n_items; it += nmw * (int)gridDim.x) {
+            for (int e = 0;; ++e) {
+                const int it = wk_take(P, F, w, e);
+                if (it < 0) break;
                 const int gi = it / P.nxt, xt = it - gi * P.nxt;
                 const int X0 = P.x0mul * xt + P.x0off;
                 for (int r0 = 0; r0 < nrow; r0 += P.rps) {
@@ -506,23 +559,23 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
         const int w = warp >> 1;
         mbar_wait(wbar, 0);
         const int KPC = P.Ea / 16;
-        if (P.KW == 3 && KPC == 2) wk_mma<3, 2>(P, w, stg0, wsm, sched, full, empty, accf, acce);
-        else if (P.KW == 3 && KPC == 4) wk_mma<3, 4>(P, w, stg0, wsm, sched, full, empty, accf, acce);
-        else if (P.KW == 2 && KPC == 2) wk_mma<2, 2>(P, w, stg0, wsm, sched, full, empty, accf, acce);
-        else if (P.KW == 2 && KPC == 4) wk_mma<2, 4>(P, w, stg0, wsm, sched, full, empty, accf, acce);
-        else if (P.KW == 4 && KPC == 2) wk_mma<4, 2>(P, w, stg0, wsm, sched, full, empty, accf, acce);
-        else if (P.KW == 4 && KPC == 4) wk_mma<4, 4>(P, w, stg0, wsm, sched, full, empty, accf, acce);
+        if (P.KW == 3 && KPC == 2) wk_mma<3, 2>(P, w, stg0, wsm, sched, full, empty, accf, acce, F);
+        else if (P.KW == 3 && KPC == 4) wk_mma<3, 4>(P, w, stg0, wsm, sched, full, empty, accf, acce, F);
+        else if (P.KW == 2 && KPC == 2) wk_mma<2, 2>(P, w, stg0, wsm, sched, full, empty, accf, acce, F);
+        else if (P.KW == 2 && KPC == 4) wk_mma<2, 4>(P, w, stg0, wsm, sched, full, empty, accf, acce, F);
+        else if (P.KW == 4 && KPC == 2) wk_mma<4, 2>(P, w, stg0, wsm, sched, full, empty, accf, acce, F);
+        else if (P.KW == 4 && KPC == 4) wk_mma<4, 4>(P, w, stg0, wsm, sched, full, empty, accf, acce, F);
         else __trap();
     } else {
         // ------------------------------------------------------------ epilogue
         if (P.est == 2) {
-            if (P.cw == 16) wk_epilogue<16, 2>(P, warp, lane, base, accf, acce);
-            else if (P.cw == 32) wk_epilogue<32, 2>(P, warp, lane, base, accf, acce);
-            else wk_epilogue<64, 2>(P, warp, lane, base, accf, acce);
+            if (P.cw == 16) wk_epilogue<16, 2>(P, warp, lane, base, accf, acce, F);
+            else if (P.cw == 32) wk_epilogue<32, 2>(P, warp, lane, base, accf, acce, F);
+            else wk_epilogue<64, 2>(P, warp, lane, base, accf, acce, F);
         } else {
-            if (P.cw == 16) wk_epilogue<16, 0>(P, warp, lane, base, accf, acce);
-            else if (P.cw == 32) wk_epilogue<32, 0>(P, warp, lane, base, accf, acce);
-            else wk_epilogue<64, 0>(P, warp, lane, base, accf, acce);
+            if (P.cw == 16) wk_epilogue<16, 0>(P, warp, lane, base, accf, acce, F);
+            else if (P.cw == 32) wk_epilogue<32, 0>(P, warp, lane, base, accf, acce, F);
+            else wk_epilogue<64, 0>(P, warp, lane, base, accf, acce, F);
         }
     }
     fence_before_sync();
@@ -692,6 +745,8 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // shared memory: [1024 barriers][stages][weights][row schedule][staging];
     // prefer >= 4 stages, then more epilogue groups, then double-buffered stores
     if (kProbes && probe_env("CAPSCONV_WK_DBG")) P.dbg = atoi(probe_env("CAPSCONV_WK_DBG"));
+    P.espin = 0;
+    if (kProbes && probe_env("CAPSCONV_WK_ESPIN")) P.espin = atoi(probe_env("CAPSCONV_WK_ESPIN"));
     P.est = 0;
     if (kProbes && probe_env("CAPSCONV_WK_EST")) P.est = atoi(probe_env("CAPSCONV_WK_EST"));
     const size_t limit = std::min<size_t>(kWkSmemLimit, device_info().smem_optin ? device_info().smem_optin : kWkSmemLimit);
@@ -721,7 +776,7 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
                     const uint32_t wo = (uint32_t)(nstg * P.nmw) * stage;
                     const uint32_t ro = (wo + P.wbytes + 127u) & ~127u;
                     const uint32_t so = (ro + rbytes + 1023u) & ~1023u;
-                    const size_t tot = 2048u + (size_t)so + sb;
+                    const size_t tot = 2048u + (size_t)so + sb + 1024u;   // + the strip lists
                     if (tot <= limit) {
                         P.rps = rps;
                         P.stage_bytes = stage;
@@ -734,12 +789,20 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
                         P.soff = so;
                         P.sbytes = sb;
                         P.smem_bytes = (uint32_t)tot;
+                        P.foff = so + sb;
                         found = true;
                         break;
                     }
                 }
             }
     if (!found) return pl;
+    // dynamic strip assignment when several streams share a CTA (each stream's
+    // list holds the strips it takes plus the end marker)
+    {
+        const int grid = std::min(P.n_items, device_info().num_sms);
+        P.dyn = P.nmw > 1 && (P.n_items + grid - 1) / grid + 1 <= kWkFifo;
+        if (kProbes && probe_env("CAPSCONV_WK_DYN")) P.dyn = P.dyn && atoi(probe_env("CAPSCONV_WK_DYN"));
+    }
     // the per-source-row schedule (identical for every strip)
     if (P.ys_hi - P.ys_lo + 1 > kWkMaxRows) return pl;
     for (int r = 0; r <= P.ys_hi - P.ys_lo; ++r) wk_make_rec(P, P.ys_lo + r, P.sched[r]);
