@@ -44,7 +44,13 @@
  *              ignored and on return are unspecified.
  * Streams      calls enqueue on `stream` (NULL = legacy default stream) and
  *              return without synchronising.  Concurrent calls on different
- *              streams (with disjoint workspaces) are safe.
+ *              streams (with disjoint workspaces) are safe.  Calls on one
+ *              stream run in order, with one relaxation: a call's weight
+ *              packing (K into the workspace) may overlap the end of the
+ *              previous libcapsconv call on that stream (programmatic
+ *              dependent launch), so K must not be an output of that
+ *              immediately preceding libcapsconv call.  Kernels of other
+ *              libraries or of the caller are fully ordered as usual.
  * Errors       every call returns a status.  All validation happens before
  *              any launch, so a non-OK status other than CAPSCONV_ERR_CUDA
  *              guarantees nothing was written.  Asynchronous device faults

@@ -97,7 +97,8 @@ FcPlan fc_plan(const Problem &p) {
 // K[c][c'][d2][d3]; columns past 4*Cout are zero.
 __global__ void __launch_bounds__(256) fc_pack(const __nv_bfloat16 *__restrict__ K, uint32_t *__restrict__ wp,
                                                int ksteps, int NT, int Cout) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)ksteps * NT * 32;
@@ -156,7 +157,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat
                                                                 const uint32_t *__restrict__ wp,
                                                                 float *__restrict__ part, int B, int C, int kslice,
                                                                 int ksteps) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(128) uint8_t fw_smem[];
     uint8_t *ring = fw_smem;
@@ -256,7 +258,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_fwd_kernel(const __nv_bfloat
 // O[b][c'][d1][d3] = sum over splits (fixed order) of part[ks][(b, d1)][(c', d3)], rounded to bf16
 __global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ part, __nv_bfloat16 *__restrict__ O,
                                                    int B, int Cout, int ncol, int ksplit) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (row, c')
     const int64_t rows = (int64_t)B * 4;
@@ -291,7 +294,8 @@ __global__ void __launch_bounds__(256) fc_finalize(const float *__restrict__ par
 // K[c][c'][d2][d3]; c' >= Cout is zero.
 __global__ void __launch_bounds__(256) fc_pack_dgrad(const __nv_bfloat16 *__restrict__ K, uint32_t *__restrict__ wp,
                                                      int ksteps, int NT, int Cout) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t total = (int64_t)ksteps * NT * 32;
@@ -326,7 +330,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dgrad_kernel(const __nv_bflo
                                                                   const uint32_t *__restrict__ wp,
                                                                   __nv_bfloat16 *__restrict__ dI, int B, int C,
                                                                   int Cout, int ksteps, int NTall, int ntper) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(16) uint32_t wsm[];
     const int nb = blockIdx.x, mb = blockIdx.y;
@@ -441,7 +446,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
                                                                const __nv_bfloat16 *__restrict__ dO,
                                                                float *__restrict__ part, int B, int C, int Cout,
                                                                int bslice, int dbg) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(128) uint8_t dk_smem[];
     uint8_t *ring = dk_smem;   // kDkStages x (4 I rows, then 4 dO rows)
@@ -562,7 +568,8 @@ __global__ void __launch_bounds__(kFcWarps * 32) fc_dk_kernel(const __nv_bfloat1
 
 __global__ void __launch_bounds__(256) fc_dk_finalize(const float *__restrict__ part, float *__restrict__ dK,
                                                       int64_t n, int ksplit) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // float4 index, n % 4 == 0
     if (i >= n / 4) return;

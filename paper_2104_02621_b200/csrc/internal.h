@@ -58,6 +58,8 @@ cudaError_t smem_optin(const void *func, int bytes);
 // probe builds only: skip the weight-pack and split-K finalize launches (timing
 // experiments; results are then wrong)
 inline bool probe_skip_small() { return kProbes && probe_env("CAPSCONV_SKIP_SMALL") != nullptr; }
+inline bool probe_skip_pack() { return probe_skip_small() || (kProbes && probe_env("CAPSCONV_SKIP_PACK") != nullptr); }
+inline bool probe_skip_fin() { return probe_skip_small() || (kProbes && probe_env("CAPSCONV_SKIP_FIN") != nullptr); }
 
 // Programmatic dependent launch (PDL) for the kernels of the hot path: the
 // launch may begin while the previous kernel in the stream is still running;

@@ -414,7 +414,8 @@ __device__ __forceinline__ void mma_taps(const ConvMma &P, const Item &it, const
 }
 
 __global__ void __launch_bounds__(kConvThreads, 1) conv_mma_kernel(const __grid_constant__ ConvMma P) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
@@ -686,7 +687,8 @@ struct PackArgs {
 };
 
 __global__ void __launch_bounds__(256) pack_weights_kernel(const __grid_constant__ PackArgs A) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     const int kcpc = A.CC / 2;
     const long long total = (long long)A.n_ntiles * A.nchunks * A.ntaps * kcpc * A.N_tile;
@@ -723,7 +725,8 @@ __global__ void __launch_bounds__(256) pack_weights_kernel(const __grid_constant
 
 // ------------------------------------------------------------------ split-K finalize
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ ConvMma P) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     // one thread per (virtual row R = u*4 + d1, output channel)
     const long long rows = (long long)P.Bn * P.Hg * P.Wg * 4;

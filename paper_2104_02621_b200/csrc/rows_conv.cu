@@ -541,7 +541,6 @@ __device__ __forceinline__ void rc_epilogue(const RowsConv &P, float *xbuf, cons
 }
 
 __global__ void __launch_bounds__(kRcThreads, 1) rows_conv_kernel(const __grid_constant__ RowsConv P) {
-    pdl_launch_dependents();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *full = bars, *empty = bars + 4, *accf = bars + 8, *acce = bars + 24, *wbar = bars + 40;   // up to 16 slots
@@ -578,17 +577,24 @@ __global__ void __launch_bounds__(kRcThreads, 1) rows_conv_kernel(const __grid_c
     fence_after_sync();
     if (*tmem_slot != 0u) __trap();
     pdl_wait();   // the previous grid's writes (source, weights) are visible from here on
+    // The packed weights are the only workspace bytes this kernel reads: once
+    // they are in shared memory the next kernel may launch (PDL) -- e.g. the
+    // next call's weight pack, which rewrites the workspace.
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(wbar, P.wbytes);
+        for (uint32_t o = 0; o < P.wbytes; o += 32768u) {
+            const uint32_t n = min(32768u, P.wbytes - o);
+            bulk_g2s_u32(wsm + o, P.wpack + o, n, wbar);
+        }
+    }
+    mbar_wait(wbar, 0);
+    pdl_launch_dependents();
 
     if (warp == kTmaWarp) {
         // ------------------------------------------------------------ TMA
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&P.tmS)) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&P.tmH)) : "memory");
-            mbar_arrive_expect_tx(wbar, P.wbytes);
-            for (uint32_t o = 0; o < P.wbytes; o += 32768u) {
-                const uint32_t n = min(32768u, P.wbytes - o);
-                bulk_g2s_u32(wsm + o, P.wpack + o, n, wbar);
-            }
             int sb = 0;
             uint32_t ph = 0;
             for (int it = blockIdx.x; it < P.n_items; it += gridDim.x) {
@@ -716,11 +722,7 @@ struct RcPackArgs {
 
 // One thread per 16-byte unit (8 consecutive k of one row n) of the K-major
 // no-swizzle image: unit (k/8, n) of slice m at woff + (k/8)*N*16 + n*16.
-__global__ void rc_pack_kernel(const __grid_constant__ RcPackArgs A) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= A.total16) return;
+__device__ __forceinline__ void rc_pack_unit(const RcPackArgs &A, uint32_t g) {
     int m = 0;
     while (m + 1 < A.nmma && A.m[m + 1].woff / 16 <= g) ++m;
     const RcPackMma &M = A.m[m];
@@ -742,6 +744,19 @@ __global__ void rc_pack_kernel(const __grid_constant__ RcPackArgs A) {
         memcpy(w, v, 16);
     }
     reinterpret_cast<uint4 *>(A.dst)[g] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// The pack reads only K and writes only the workspace, which the previous
+// libcapsconv kernel no longer reads once it has triggered its dependents
+// (rows_walk / rows_conv: after their weights landed in shared memory; every
+// other kernel: at completion): so it runs alongside that kernel's tail (64-
+// thread blocks fit next to a resident conv CTA), and waits for the previous
+// grid only before it exits, so that its own completion keeps stream order.
+__global__ void __launch_bounds__(64) rc_pack_kernel(const __grid_constant__ RcPackArgs A) {
+    pdl_launch_dependents();
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < A.total16) rc_pack_unit(A, g);
+    pdl_wait();
 }
 
 struct RcPlan {
@@ -1137,8 +1152,8 @@ cudaError_t rows_conv_run(capsconv_op_t op, const Problem &p, const void *src, c
     RcPackArgs &A = pl.pack;
     A.K = static_cast<const __nv_bfloat16 *>(K);
     A.dst = static_cast<uint8_t *>(ws);
-    cudaError_t e = probe_skip_small() ? cudaSuccess
-                                       : launch_k(rc_pack_kernel, dim3((A.total16 + 255) / 256), dim3(256), 0, st, A);
+    cudaError_t e = probe_skip_pack() ? cudaSuccess
+                                       : launch_k(rc_pack_kernel, dim3((A.total16 + 63) / 64), dim3(64), 0, st, A);
     if (e != cudaSuccess) return e;
     note_launches(1);
     e = smem_optin(reinterpret_cast<const void *>(rows_conv_kernel), (int)P.smem_bytes);

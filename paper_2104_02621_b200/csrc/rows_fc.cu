@@ -66,7 +66,8 @@ __device__ __forceinline__ void fc_decode(const RowsFc &P, int item, int &mt, in
 }
 
 __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_constant__ RowsFc P) {
-    pdl_launch_dependents();
+    // no early PDL trigger: the packed weights (and split partials) in the
+    // workspace are read until the end
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *full = bars, *empty = bars + 8, *accf = bars + 16, *acce = bars + 18;
@@ -272,8 +273,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) rows_fc_kernel(const __grid_con
 // fwd: O[r][n] = bf16(sum_k part[k][r][n]), n < EO (rows r = (b, d1) < 4B)
 __global__ void fc_fin_fwd(const float *__restrict__ part, __nv_bfloat16 *__restrict__ O, int rows, int N, int EO,
                            int ksplit, long long mstride) {
-    pdl_launch_dependents();
-    pdl_wait();
+    pdl_wait();   // no early trigger: the partials in the workspace are read to the end
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long long)rows * EO) return;
     const int r = (int)(i / EO), n = (int)(i - (long long)r * EO);
@@ -285,8 +285,7 @@ __global__ void fc_fin_fwd(const float *__restrict__ part, __nv_bfloat16 *__rest
 // dK: rows m = (p, c, d2) over E per pixel, columns n = (c', d3) < EO
 __global__ void fc_fin_dk(const float *__restrict__ part, float *__restrict__ dK, int M, int N, int C, int Cout,
                           int ksplit, long long mstride) {
-    pdl_launch_dependents();
-    pdl_wait();
+    pdl_wait();   // no early trigger: the partials in the workspace are read to the end
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int EO = 4 * Cout;
     if (i >= (long long)M * EO) return;
@@ -301,12 +300,8 @@ __global__ void fc_fin_dk(const float *__restrict__ part, float *__restrict__ dK
 // Packed weight images, SWIZZLE_128B K-major rows of 64 bf16 (128 B):
 //   fwd: chunk c (p = c / (E/64), (c,d2) block (c % (E/64))*64), rows n < N = (c', d3)
 //   dI : rows n = (p, c, d2) < P*E, k = (c', d3) < 64 (zero past EO)
-__global__ void fc_pack(const __nv_bfloat16 *__restrict__ K, uint8_t *__restrict__ dst, int mode, int P, int C,
-                        int Cout, int N, long long total16) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= total16) return;
+__device__ __forceinline__ void fc_pack_unit(const __nv_bfloat16 *__restrict__ K, uint8_t *__restrict__ dst, int mode,
+                                             int C, int Cout, int N, long long g) {
     const int E = 4 * C, EO = 4 * Cout;
     const long long rowi = g / 8;            // 8 sixteen-byte units per 128-byte row
     const int unit = (int)(g - rowi * 8);    // physical unit in the row
@@ -340,6 +335,17 @@ __global__ void fc_pack(const __nv_bfloat16 *__restrict__ K, uint8_t *__restrict
     uint4 w;
     memcpy(&w, v, 16);
     reinterpret_cast<uint4 *>(dst)[g] = w;
+}
+
+// Runs alongside the previous kernel's tail (see rc_pack_kernel): reads only K,
+// writes only the workspace, and waits for the previous grid before it exits.
+__global__ void __launch_bounds__(64) fc_pack(const __nv_bfloat16 *__restrict__ K, uint8_t *__restrict__ dst, int mode,
+                                              int P, int C, int Cout, int N, long long total16) {
+    (void)P;
+    pdl_launch_dependents();
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < total16) fc_pack_unit(K, dst, mode, C, Cout, N, g);
+    pdl_wait();
 }
 
 struct FcPlan {
@@ -464,9 +470,9 @@ cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const
             !rows::make_rows_map2(&P.tmB, b, (int64_t)P.B * 4, P.EO, 64, 128, 128))
             return cudaErrorInvalidValue;
     }
-    if (mode != 2 && !probe_skip_small()) {
+    if (mode != 2 && !probe_skip_pack()) {
         const long long total16 = (long long)pl.wpack_bytes / 16;
-        e = launch_k(fc_pack, dim3((unsigned)((total16 + 255) / 256)), dim3(256), 0, st,
+        e = launch_k(fc_pack, dim3((unsigned)((total16 + 63) / 64)), dim3(64), 0, st,
                      static_cast<const __nv_bfloat16 *>(b), w8, mode, P.P, P.C, P.Cout, P.N, total16);
         if (e != cudaSuccess) return e;
         note_launches(1);
@@ -478,7 +484,7 @@ cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const
     if (e != cudaSuccess) return e;
     note_launches(1);
     const long long mstride = (long long)P.nmt * 128 * P.N;
-    if (probe_skip_small()) {
+    if (probe_skip_fin()) {
     } else if (mode == 0) {
         const long long n = (long long)P.B * 4 * P.EO;
         e = launch_k(fc_fin_fwd, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, static_cast<const float *>(P.part),

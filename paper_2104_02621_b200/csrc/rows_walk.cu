@@ -463,7 +463,6 @@ __device__ __forceinline__ void wk_epilogue(const RowsWalk &P, int warp, int lan
 }
 
 __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant__ RowsWalk P) {
-    pdl_launch_dependents();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *full = bars, *empty = bars + kWkMaxStg, *accf = bars + 2 * kWkMaxStg,
@@ -498,6 +497,16 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
     fence_after_sync();
     if (*tmem_slot != 0u) __trap();
     pdl_wait();
+    // The packed weights are the only workspace bytes this kernel reads: once
+    // they are in shared memory the next kernel may launch (PDL) -- e.g. the
+    // next call's weight pack, which rewrites the workspace.
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(wbar, P.wbytes);
+        for (uint32_t o = 0; o < P.wbytes; o += 32768u)
+            bulk_g2s_u32(wsm + o, P.wpack + o, min(32768u, P.wbytes - o), wbar);
+    }
+    mbar_wait(wbar, 0);
+    pdl_launch_dependents();
 
     const int nmw = P.nmw;
     if (warp < 2 * nmw && !(warp & 1)) {
@@ -505,11 +514,6 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
         const int w = warp >> 1;
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&P.tmS)) : "memory");
-            if (w == 0) {
-                mbar_arrive_expect_tx(wbar, P.wbytes);
-                for (uint32_t o = 0; o < P.wbytes; o += 32768u)
-                    bulk_g2s_u32(wsm + o, P.wpack + o, min(32768u, P.wbytes - o), wbar);
-            }
             uint64_t *fullw = full + w * P.nstg, *emptyw = empty + w * P.nstg;
             const uint32_t stgw = stg0 + (uint32_t)(w * P.nstg) * P.stage_bytes;
             int sb = 0;
@@ -596,11 +600,7 @@ struct WkPackArgs {
 
 // One thread per 16-byte unit (8 consecutive k of one row n) of the K-major
 // no-swizzle image: unit (k/8, n) of block (cl, q) at bo + (k/8)*Ncl + n.
-__global__ void wk_pack_kernel(const __grid_constant__ WkPackArgs A) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= A.total16) return;
+__device__ __forceinline__ void wk_pack_unit(const WkPackArgs &A, uint32_t g) {
     int b = 0;
     while (b + 1 < A.nblk && A.bo[b + 1] <= g) ++b;
     const uint32_t loc = g - A.bo[b];
@@ -620,6 +620,16 @@ __global__ void wk_pack_kernel(const __grid_constant__ WkPackArgs A) {
     uint4 w;
     memcpy(&w, v, 16);
     reinterpret_cast<uint4 *>(A.dst)[g] = w;
+}
+
+// Runs alongside the previous kernel's tail (see rc_pack_kernel): it reads only
+// K and writes only the workspace, and waits for the previous grid before it
+// exits so that its completion keeps stream order.
+__global__ void __launch_bounds__(64) wk_pack_kernel(const __grid_constant__ WkPackArgs A) {
+    pdl_launch_dependents();
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < A.total16) wk_pack_unit(A, g);
+    pdl_wait();
 }
 
 struct WkPlan {
@@ -874,8 +884,8 @@ cudaError_t rows_walk_run(capsconv_op_t op, const Problem &p, const void *src, c
     WkPackArgs &A = pl.pack;
     A.K = static_cast<const __nv_bfloat16 *>(K);
     A.dst = static_cast<uint8_t *>(ws);
-    cudaError_t e = probe_skip_small() ? cudaSuccess
-                                       : launch_k(wk_pack_kernel, dim3((A.total16 + 255) / 256), dim3(256), 0, st, A);
+    cudaError_t e = probe_skip_pack() ? cudaSuccess
+                                       : launch_k(wk_pack_kernel, dim3((A.total16 + 63) / 64), dim3(64), 0, st, A);
     if (e != cudaSuccess) return e;
     note_launches(1);
     static unsigned long long *prof_buf = nullptr;

@@ -143,8 +143,7 @@ __device__ __forceinline__ void rw_mma_item(const RowsWgrad &P, const RwSet &S, 
 }
 
 __global__ void __launch_bounds__(kRwThreads, 1) rows_wgrad_kernel(const __grid_constant__ RowsWgrad P) {
-    pdl_launch_dependents();
-    pdl_wait();
+    pdl_wait();   // no early PDL trigger: the split partials go to the workspace at the end
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
     uint64_t *full = bars, *empty = bars + 8, *acc_full = bars + 16, *acc_empty = bars + 17;
@@ -276,7 +275,7 @@ __global__ void __launch_bounds__(kRwThreads, 1) rows_wgrad_kernel(const __grid_
 constexpr int kFinWarps = 16;
 __global__ void __launch_bounds__(kFinWarps * 32) rw_finalize(const float *__restrict__ part, float *__restrict__ dK,
                                                               long long n4, long long nK, int ksplit) {
-    pdl_launch_dependents();
+    
     pdl_wait();
     __shared__ float4 red[kFinWarps][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -511,7 +510,7 @@ cudaError_t rows_wgrad_run(const Problem &p, const void *I, const void *dO, floa
     e = launch_k(rows_wgrad_kernel, dim3(grid), dim3(kRwThreads), P.smem_bytes, st, P);
     if (e != cudaSuccess) return e;
     note_launches(1);
-    if (P.ksplit > 1 && !probe_skip_small()) {
+    if (P.ksplit > 1 && !probe_skip_fin()) {
         const long long n4 = P.nK / 4;
         e = launch_k(rw_finalize, dim3((unsigned)((n4 + 31) / 32)), dim3(kFinWarps * 32), 0, st,
                      static_cast<const float *>(P.part), dK, n4, P.nK, P.ksplit);

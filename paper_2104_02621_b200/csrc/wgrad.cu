@@ -595,7 +595,8 @@ __device__ __forceinline__ void w_load_A(const WgradMma &P, const WLane &L, int 
 }
 
 __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_constant__ WgradMma P) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw);
@@ -934,7 +935,8 @@ __global__ void __launch_bounds__(kWThreads, 1) wgrad_kernel(const __grid_consta
 // then added in slice order (a fixed summation tree for every launch).
 __global__ void __launch_bounds__(256) w_finalize(const float *__restrict__ part, float *__restrict__ dK, int64_t n,
                                                   int ksplit, int nsl) {
-    pdl_launch_dependents();   // PDL: the next kernel may launch; it waits for this grid
+    // (no early PDL trigger: the workspace may be read until the end, and the
+    // rows-layout weight packs that may follow do not wait before writing it)
     pdl_wait();                // the previous grid has completed and its writes are visible
     __shared__ float red[256];
     const int E = 256 / nsl;
