@@ -231,6 +231,19 @@ def pass_bytes(st, li, kind, elem):
     return (nI + nO) * elem + 4 * nK
 
 
+def pass_write_bytes(st, li, kind, elem):
+    """The part of pass_bytes the pass writes: |O| (fwd), |dI| (dI), 4|dK| (dK)."""
+    sp = st.specs[li]
+    h, w = st.hw[li]
+    ho, wo = st.hw[li + 1]
+    D = st.D
+    if kind == "fwd":
+        return st.batch * ho * wo * sp.Cout * D * D * elem
+    if kind == "dI":
+        return st.batch * h * w * sp.C * D * D * elem
+    return 4 * sp.KH * sp.KW * sp.C * sp.Cout * D * D
+
+
 # ---------------------------------------------------------------- reference (oracle) arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -559,6 +572,18 @@ def main():
             torch.cuda.synchronize()
             use_graph, gtimer = False, None
 
+    # HBM write bandwidth, live: the L2 flush is a plain write of 2x L2 (a
+    # write-only stream reaches about half the copy figure on this part, so
+    # the write-heavy passes get a second, write-aware floor in per_pass)
+    wa, wb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    wa.record()
+    for _ in range(5):
+        flush.zero_()
+    wb.record()
+    torch.cuda.synchronize()
+    write_gbs = 5 * flush.numel() / (wa.elapsed_time(wb) * 1e-3) / 1e9
+
     timer = CallTimer()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -617,10 +642,12 @@ def main():
         fl = st.layer_flops(li)
         gbs = byts / (avg * 1e-3) / 1e9
         tr = max(byts / (peaks["hbm_gbs"] * 1e9), fl / (cpeak * 1e12)) * 1e3
+        tw = max(tr, pass_write_bytes(st, li, kind, elem) / (write_gbs * 1e9) * 1e3)
         t_roof_sum += tr
         per_pass["L%d_%s" % (li + 1, kind)] = {"ms": round(avg, 5), "GB_s": round(gbs, 1),
                                                 "TFLOP_s": round(fl / (avg * 1e-3) / 1e12, 1),
-                                                "roof_frac": round(tr / avg, 3)}
+                                                "roof_frac": round(tr / avg, 3),
+                                                "wfloor_frac": round(tw / avg, 3)}
         if best is None or avg > best[1]:
             best = ((li, kind), avg, byts)
     (bli, bkind), bavg, bbytes = best
@@ -648,7 +675,8 @@ def main():
                      "flops_per_launch": bflops,
                      "peak_src": peaks["src"] if dtype == torch.bfloat16 or t_tc <= t_hbm or "FFMA" in peaks["src"]
                      else "derived: SMs x 128 FFMA lanes x 2 x max SM clock",
-                     "step_frac": round(t_roof_sum / ms, 4)})
+                     "step_frac": round(t_roof_sum / ms, 4),
+                     "hbm_write_gbs_live": round(write_gbs, 1)})
 
     # ---- e2e: same steps through the public API with host buffers.  Every
     # step copies its input X and dY from pinned host memory and reads all dK

@@ -50,6 +50,20 @@ CAPS_R2B = [("L%d_%s" % (l, o), "r2b_L%d_%s.ncu-rep" % (l, o), 0, desc) for (l, 
     (4, "fwd", "rows_fc_kernel mode 0 (split-K GEMM)"),
     (4, "dI", "rows_fc_kernel mode 1 (N=256 tiles, coalesced stores)"),
     (4, "dK", "rows_fc_kernel mode 2")]]
+# Round 2, final build after dynamic strips + PDL weight packs (tests/probe/prof_r2c.sh)
+CAPS_R2C = [("L%d_%s" % (l, o), "r2c_L%d_%s.ncu-rep" % (l, o), 0, desc) for (l, o, desc) in [
+    (1, "fwd", "rows_walk_kernel fwd s1: 3 row taps stacked in N=96, 3 streams, dynamic strips"),
+    (1, "dI", "rows_walk_kernel dI s1"),
+    (1, "dK", "rows_wgrad_kernel"),
+    (2, "fwd", "rows_walk_kernel fwd s2 (phase planes)"),
+    (2, "dI", "rows_conv_kernel dI s2 (output phases)"),
+    (2, "dK", "rows_wgrad_kernel s2"),
+    (3, "fwd", "rows_conv_kernel fwd, N=128 per tap"),
+    (3, "dI", "rows_walk_kernel dI, N=192"),
+    (3, "dK", "rows_wgrad_kernel"),
+    (4, "fwd", "rows_fc_kernel mode 0 (split-K GEMM)"),
+    (4, "dI", "rows_fc_kernel mode 1 (N=256 tiles, coalesced stores)"),
+    (4, "dK", "rows_fc_kernel mode 2")]]
 
 
 def full_summaries(caps, rnd, traffic, tag=None, src=None):
@@ -80,7 +94,7 @@ def full_summaries(caps, rnd, traffic, tag=None, src=None):
                 d[k] = (float(v[i].replace(",", "")), u[i])
         tb = int(d["dram__bytes_read.sum"][0] * SCALE[d["dram__bytes_read.sum"][1]] +
                  d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]])
-        traffic[name if tag == "r2b" else tag + "_" + name] = tb
+        traffic[name if tag == "r2c" else tag + "_" + name] = tb
         out.append("  %-80s %d" % ("dram read+write bytes per launch", tb))
         out.append("")
     open(os.path.join(PROF, "%s_ncu_full_summary.txt" % tag), "w").write("\n".join(out) + "\n")
@@ -114,11 +128,13 @@ if __name__ == "__main__":
     full_summaries(CAPS, 1, traffic)
     full_summaries(CAPS_R2, 2, traffic, tag="r2a")
     full_summaries(CAPS_R2B, 2, traffic, tag="r2b")
+    full_summaries(CAPS_R2C, 2, traffic, tag="r2c")
     traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the ncu --set full "
                         "captures in profiles/ (tests/probe/profile_summary.py); unprefixed keys: round-2 final build "
-                        "(r2b captures of the kernels bench.py times); r2a_*: earlier round-2 rows kernels; r1_*: "
+                        "(r2c captures of the kernels bench.py times); r2b_*: before dynamic strips / PDL packs; r2a_*: earlier round-2 rows kernels; r1_*: "
                         "round-1 natural-layout kernels")
     json.dump(traffic, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     launches(1, "--steps 3 --warmup 3")
     launches(2, "--steps 2 --warmup 1", tag="r2")
     launches(2, "--steps 2 --warmup 1 --no-parity", tag="r2b")
+    launches(2, "--steps 2 --warmup 1 --no-parity", tag="r2c")
