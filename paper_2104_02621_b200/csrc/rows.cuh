@@ -125,6 +125,15 @@ __device__ __forceinline__ void tmem_ld16x(uint32_t taddr, uint32_t (&r)[16]) {
         : "r"(taddr));
 }
 
+// 16 columns of zeros into this warp's 32 TMEM lanes (one zero register, 16 operands)
+__device__ __forceinline__ void tmem_st_zero16(uint32_t taddr) {
+    const uint32_t z = 0u;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n"
+        ::"r"(taddr), "r"(z) : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
     asm volatile(

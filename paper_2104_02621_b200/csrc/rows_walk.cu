@@ -82,6 +82,7 @@ struct RowsWalk {
     uint32_t aoff[kWkMaxQ];        // A offset of column tap q: plane * plane_bytes + shift * 4 rows
     uint32_t sched[kWkMaxRows][8]; // per-source-row MMA schedule (wk_make_rec), built on the host
     unsigned long long *prof;      // probe builds only: per-CTA cycle counters [cta][8]
+    int zfill;                     // drained slots are zeroed by the epilogue: every MMA accumulates
     int dbg;                       // probe builds only: 1 skip epilogue stores, 2 skip source loads, 4 skip MMAs
 };
 
@@ -115,8 +116,9 @@ __host__ __device__ __forceinline__ void wk_rows(const RowsWalk &P, int Ys, int 
 // once per CTA in shared memory.  Record of 8 words:
 //   w0: slots to wait free (rows touched first here) | slots to commit << 16
 //   w1: bit 0 valid, bit 1 row class
-//   w2..w5: segments of the first MMA (split where the fresh rows start)
-//   w6..w7: segments of the other MMAs
+//   w2..w5: segments of the first MMA (split where the fresh rows start; with
+//           zfill the fresh slots already hold zeros and w2..w3 = w6..w7)
+//   w6..w7: segments of the other MMAs (split only where the rows wrap the ring)
 // segment word: dcol (10 bits) | B row offset in 16-byte units (10) << 10 |
 //               accumulate << 20 | N/8 << 21 (0: no segment)
 constexpr uint32_t kWkRecBytes = 32;
@@ -157,9 +159,14 @@ __host__ __device__ void wk_make_rec(const RowsWalk &P, int Ys, uint32_t (&w)[8]
     for (int y = ya; y < ynext; ++y) cm |= 1u << (y % P.Rw);
     w[0] = wm | (cm << 16);
     w[1] = 1u | ((uint32_t)cl << 1);
-    wk_seg(P, y0, ya, yf - 1, 1u, w[2], w[3]);
-    wk_seg(P, y0, yf, yb, 0u, w[4], w[5]);
     wk_seg(P, y0, ya, yb, 1u, w[6], w[7]);
+    if (P.zfill) {
+        w[2] = w[6];
+        w[3] = w[7];
+    } else {
+        wk_seg(P, y0, ya, yf - 1, 1u, w[2], w[3]);
+        wk_seg(P, y0, yf, yb, 0u, w[4], w[5]);
+    }
 }
 
 __device__ __forceinline__ void wk_mma_seg(uint32_t sg, uint32_t dbase, uint64_t ad, uint32_t bhi, uint32_t bk,
@@ -411,7 +418,12 @@ __device__ __forceinline__ void wk_epilogue(const RowsWalk &P, int warp, int lan
                         if (CW == 64) rows::tmem_ld32(tb + 32u, *reinterpret_cast<float(*)[32]>(v + 32 % CW));
                     }
                     tmem_wait_ld();
+                    if (P.zfill) {   // leave zeros behind: the slot's next row starts by accumulating
+#pragma unroll
+                        for (int z = 0; z < CW; z += 16) rows::tmem_st_zero16(tb + (uint32_t)z);
+                    }
                     if (c0 + CW >= NB) {   // slot drained: hand it back to the MMA warp
+                        if (P.zfill) rows::tmem_wait_st();
                         fence_before_sync();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(acce + slot + yy);
@@ -496,6 +508,17 @@ __global__ void __launch_bounds__(640, 1) rows_walk_kernel(const __grid_constant
     __syncthreads();
     fence_after_sync();
     if (*tmem_slot != 0u) __trap();
+    if (P.zfill) {   // every accumulator column starts at zero (epilogue warps, own lane quarter)
+        const int e = warp - 2 * P.nmw;
+        if (e >= 0) {
+            const uint32_t tl = (uint32_t)((warp & 3) * 32) << 16;
+            for (int c = (e >> 2) * 16; c < 512; c += 16 * P.nepi) rows::tmem_st_zero16(tl + (uint32_t)c);
+            rows::tmem_wait_st();
+        }
+        fence_before_sync();
+        __syncthreads();
+        fence_after_sync();
+    }
     pdl_wait();
     // The packed weights are the only workspace bytes this kernel reads: once
     // they are in shared memory the next kernel may launch (PDL) -- e.g. the
@@ -755,6 +778,8 @@ WkPlan make_wk_plan(const Problem &p, bool dgrad) {
     // shared memory: [1024 barriers][stages][weights][row schedule][staging];
     // prefer >= 4 stages, then more epilogue groups, then double-buffered stores
     if (kProbes && probe_env("CAPSCONV_WK_DBG")) P.dbg = atoi(probe_env("CAPSCONV_WK_DBG"));
+    P.zfill = 1;
+    if (kProbes && probe_env("CAPSCONV_WK_ZFILL")) P.zfill = atoi(probe_env("CAPSCONV_WK_ZFILL"));
     P.espin = 0;
     if (kProbes && probe_env("CAPSCONV_WK_ESPIN")) P.espin = atoi(probe_env("CAPSCONV_WK_ESPIN"));
     P.est = 0;
