@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--config", default="stack", choices=["stack", "stack_same", "layer_s1", "layer_s2", "fc"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce on the compute stream")
+    ap.add_argument("--no-dk-stream", action="store_true", help="dK passes on the compute stream (no second chain)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--layout", default="rows", choices=["rows", "natural"],
@@ -516,7 +517,8 @@ def main():
     X = X_host.to(dev)
     dY = dY_host.to(dev)
 
-    st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap, layout=args.layout)
+    st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap, layout=args.layout,
+                   dk_stream=not args.no_dk_stream)
     gflops = st.step_flops(batch=gbatch)          # whole-job algorithmic flops per step
     peaks = load_peaks()
 
@@ -783,8 +785,10 @@ def main():
                        "layout": args.layout,
                        "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
                        "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None,
-                       "launch": ("one CUDA-graph replay of the captured step (%d libcapsconv kernels%s)" % (
-                           launches_per_step, " + %d NCCL all-reduces" % len(specs) if world > 1 else ""))
+                       "launch": ("one CUDA-graph replay of the captured step (%d libcapsconv kernels%s%s; "
+                                  "per-pass times from a second graph running the passes one by one)" % (
+                           launches_per_step, " + %d NCCL all-reduces" % len(specs) if world > 1 else "",
+                           ", the dK chain on a second stream beside the dI chain" if st.dk_stream is not None else ""))
                        if use_graph else (graph_note or "eager launches")},
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -18,6 +18,7 @@ all-reduce logic with the gloo backend on CPU.
 """
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -44,7 +45,8 @@ def shard_range(global_batch: int, rank: int, world: int):
 
 class CapsStack:
     def __init__(self, specs: Sequence[LayerSpec], H: int, W: int, D: int, batch: int, weights: List[torch.Tensor],
-                 device, ops=None, group=None, overlap: bool = True, layout: str = "natural"):
+                 device, ops=None, group=None, overlap: bool = True, layout: str = "natural",
+                 dk_stream: bool = True):
         if ops is None:
             from . import capsconv as ops
         self.ops = ops
@@ -82,6 +84,11 @@ class CapsStack:
         self.dK = [torch.empty(k.shape, dtype=kdt, device=self.device) for k in self.K]
         self.comm_stream = torch.cuda.Stream(self.device) if self.overlap else None
         self.events = [torch.cuda.Event() for _ in self.K] if self.overlap else None
+        # dK on a stream of its own: the dK chain and the dI chain of the
+        # backward are independent once a layer's incoming gradient exists, so
+        # their kernels fill each other's tails and share dO reads through L2
+        self.dk_stream = torch.cuda.Stream(self.device) if (self.overlap and dk_stream) else None
+        self.g_events = [torch.cuda.Event() for _ in self.K] if self.dk_stream is not None else None
 
     def caps_shape(self, b, h, w, c):
         """Shape of a capsule tensor of this stack's layout."""
@@ -118,15 +125,26 @@ class CapsStack:
     def backward(self, dy: torch.Tensor, timer=None) -> List[torch.Tensor]:
         g = dy
         cur = torch.cuda.current_stream(self.device) if self.overlap else None
+        # per-pass timing (timer) runs the passes one after another so that each
+        # event pair brackets one pass alone
+        ks = self.dk_stream if timer is None else None
+        if ks is not None:
+            ks.wait_stream(cur)   # the previous step's readers of dK are behind us
         for li in range(len(self.specs) - 1, -1, -1):
             sp = self.specs[li]
             h, w = self.hw[li]
-            if timer: timer.begin(li, "dK")
-            self.ops.bwd_kernel(self.acts[li], g, sp.stride, sp.KH, sp.KW, out=self.dK[li], pad=sp.pad, **self._lk)
-            if timer: timer.end(li, "dK")
+            if ks is not None:
+                # dK(li) reads acts[li] and g on the dK stream once g exists
+                self.g_events[li].record(cur)
+                ks.wait_event(self.g_events[li])
+            with torch.cuda.stream(ks) if ks is not None else contextlib.nullcontext():
+                if timer: timer.begin(li, "dK")
+                self.ops.bwd_kernel(self.acts[li], g, sp.stride, sp.KH, sp.KW, out=self.dK[li], pad=sp.pad,
+                                    **self._lk)
+                if timer: timer.end(li, "dK")
             if self.world > 1:
                 if self.overlap:
-                    self.events[li].record(cur)
+                    self.events[li].record(ks if ks is not None else cur)
                     self.comm_stream.wait_event(self.events[li])
                     with torch.cuda.stream(self.comm_stream):
                         dist.all_reduce(self.dK[li], op=dist.ReduceOp.SUM, group=self.group)
@@ -136,6 +154,8 @@ class CapsStack:
             self.ops.bwd_data(g, self.K[li], sp.stride, h, w, out=self.grads[li], pad=sp.pad, **self._lk)
             if timer: timer.end(li, "dI")
             g = self.grads[li]
+        if ks is not None:
+            cur.wait_stream(ks)
         if self.world > 1 and self.overlap:
             cur.wait_stream(self.comm_stream)
         return self.dK
