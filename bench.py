@@ -654,9 +654,10 @@ def main():
             best = ((li, kind), avg, byts)
     (bli, bkind), bavg, bbytes = best
     traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get("L%d_%s" % (bli + 1, bkind))
+    try:   # the committed captures are of the bf16 rows kernels of the stack
+        if dtype == torch.bfloat16 and args.layout == "rows" and args.config == "stack":
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get("L%d_%s" % (bli + 1, bkind))
     except Exception:
         pass
     # the binding roof of the dominant pass: HBM time of its algorithmic bytes
