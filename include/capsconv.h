@@ -45,11 +45,12 @@
  * Streams      calls enqueue on `stream` (NULL = legacy default stream) and
  *              return without synchronising.  Concurrent calls on different
  *              streams (with disjoint workspaces) are safe.  Calls on one
- *              stream run in order, with one relaxation: a call's weight
- *              packing (K into the workspace) may overlap the end of the
- *              previous libcapsconv call on that stream (programmatic
- *              dependent launch), so K must not be an output of that
- *              immediately preceding libcapsconv call.  Kernels of other
+ *              stream run in order.  A call's weight packing (K into the
+ *              workspace) may overlap the end of the previous libcapsconv
+ *              call on that stream (programmatic dependent launch); the
+ *              library remembers each stream's last output range and packs
+ *              fully ordered when K overlaps it, so K may be any buffer,
+ *              including the previous call's output.  Kernels of other
  *              libraries or of the caller are fully ordered as usual.
  * Errors       every call returns a status.  All validation happens before
  *              any launch, so a non-OK status other than CAPSCONV_ERR_CUDA

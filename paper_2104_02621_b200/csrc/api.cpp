@@ -12,6 +12,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include <cuda_runtime.h>
 
@@ -38,6 +39,39 @@ cudaError_t smem_optin(const void *func, int bytes) {
     if (e == cudaSuccess) have = bytes;
     return e;
 }
+
+// Per stream, the byte range of the last libcapsconv call's output: a call
+// whose K overlaps it packs K fully ordered (no programmatic overlap).
+static thread_local bool t_pack_overlap = true;
+bool pack_may_overlap() { return t_pack_overlap; }
+
+namespace {
+struct OutRange {
+    uintptr_t lo = 0, hi = 0;
+};
+std::mutex g_out_mu;
+std::unordered_map<cudaStream_t, OutRange> g_last_out;
+
+// Before a call: may its weight pack overlap the previous call on `cs`?
+void pack_guard_begin(cudaStream_t cs, const void *K, size_t k_bytes) {
+    bool ok = true;
+    if (K) {
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(K), hi = lo + k_bytes;
+        std::lock_guard<std::mutex> lock(g_out_mu);
+        auto it = g_last_out.find(cs);
+        if (it != g_last_out.end() && lo < it->second.hi && it->second.lo < hi) ok = false;
+    }
+    t_pack_overlap = ok;
+}
+// After a call: remember its output range on `cs`.
+void pack_guard_end(cudaStream_t cs, const void *out, size_t out_bytes) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(out);
+    std::lock_guard<std::mutex> lock(g_out_mu);
+    if (g_last_out.size() > 4096) g_last_out.clear();   // bound the table (streams come and go)
+    g_last_out[cs] = OutRange{lo, lo + out_bytes};
+    t_pack_overlap = true;
+}
+}  // namespace
 
 bool pdl_enabled() {
     static const bool on = probe_env("CAPSCONV_NO_PDL") == nullptr;
@@ -384,7 +418,11 @@ static capsconv_status_t run_op(capsconv_op_t op, capsconv_dtype_t dt, capsconv_
     if (need && !workspace) return fail(CAPSCONV_ERR_NULL, "workspace is NULL but %zu bytes are required", need);
     st = check_device();
     if (st) return st;
-    return finish(dispatch(op, p, a, b, out, workspace, workspace_bytes, (cudaStream_t)stream), what);
+    const cudaStream_t cs = (cudaStream_t)stream;
+    pack_guard_begin(cs, op == CAPSCONV_OP_BWD_KERNEL ? nullptr : b, p.kernel_bytes());
+    const cudaError_t e = dispatch(op, p, a, b, out, workspace, workspace_bytes, cs);
+    pack_guard_end(cs, out, p.out_bytes(op));
+    return finish(e, what);
 }
 
 capsconv_status_t capsconv_fwd_ex(capsconv_dtype_t dt, capsconv_layout_t layout, int64_t B, int64_t H, int64_t W,
@@ -497,6 +535,7 @@ capsconv_status_t capsconv_fwd_slices(capsconv_dtype_t dt, int64_t B, int64_t H,
     CAPSCONV_SLICES_PROLOGUE(CAPSCONV_OP_FWD, I, K, O)
     cudaError_t e = slices_expand_kernel(dt, K, ws8, KH * KW, C, Cout, S, D2 * D3, cs);
     if (e == cudaSuccess) e = dispatch(CAPSCONV_OP_FWD, pe, I, ws8, O, inner_ws, inner_bytes, cs);
+    pack_guard_end(cs, O, (size_t)pe.n_out() * pe.elem());
     return finish(e, "capsconv_fwd_slices");
 }
 
@@ -507,6 +546,7 @@ capsconv_status_t capsconv_bwd_data_slices(capsconv_dtype_t dt, int64_t B, int64
     CAPSCONV_SLICES_PROLOGUE(CAPSCONV_OP_BWD_DATA, dO, K, dI)
     cudaError_t e = slices_expand_kernel(dt, K, ws8, KH * KW, C, Cout, S, D2 * D3, cs);
     if (e == cudaSuccess) e = dispatch(CAPSCONV_OP_BWD_DATA, pe, dO, ws8, dI, inner_ws, inner_bytes, cs);
+    pack_guard_end(cs, dI, (size_t)pe.n_in() * pe.elem());
     return finish(e, "capsconv_bwd_data_slices");
 }
 
@@ -518,6 +558,7 @@ capsconv_status_t capsconv_bwd_kernel_slices(capsconv_dtype_t dt, int64_t B, int
     float *dKx = reinterpret_cast<float *>(ws8);
     cudaError_t e = dispatch(CAPSCONV_OP_BWD_KERNEL, pe, I, dO, dKx, inner_ws, inner_bytes, cs);
     if (e == cudaSuccess) e = slices_extract_dk(dKx, dK, KH * KW, C, Cout, S, D2 * D3, cs);
+    pack_guard_end(cs, dK, (size_t)pe.n_k() * 4);   // bound: the expanded dK
     return finish(e, "capsconv_bwd_kernel_slices");
 }
 

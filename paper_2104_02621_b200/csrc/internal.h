@@ -24,6 +24,12 @@ struct Problem {
     int64_t n_out() const { return B * Ho * Wo * Cout * D1 * D3; }
     int64_t n_k() const { return KH * KW * C * Cout * D2 * D3; }
     int64_t n_pix_out() const { return B * Ho * Wo; }
+    size_t kernel_bytes() const { return (size_t)n_k() * elem(); }
+    // bytes a call writes: O (fwd), dI (bwd_data), fp32 dK (bwd_kernel)
+    size_t out_bytes(capsconv_op_t op) const {
+        return op == CAPSCONV_OP_FWD ? (size_t)n_out() * elem()
+               : op == CAPSCONV_OP_BWD_DATA ? (size_t)n_in() * elem() : (size_t)n_k() * 4;
+    }
 };
 
 // Device facts, cached once per device.
@@ -82,6 +88,27 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+// Weight packs (K -> workspace) read K while the previous kernel on the stream
+// may still run (they trigger their dependents on entry and wait for the
+// previous grid only before exiting).  The API entry clears this per call
+// when K overlaps the output of the previous libcapsconv call on the same
+// stream; the pack then launches fully ordered (see capsconv.h, "Streams").
+bool pack_may_overlap();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pack(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() && pack_may_overlap() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 #ifdef __CUDACC__

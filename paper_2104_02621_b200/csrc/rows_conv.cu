@@ -1153,7 +1153,7 @@ cudaError_t rows_conv_run(capsconv_op_t op, const Problem &p, const void *src, c
     A.K = static_cast<const __nv_bfloat16 *>(K);
     A.dst = static_cast<uint8_t *>(ws);
     cudaError_t e = probe_skip_pack() ? cudaSuccess
-                                       : launch_k(rc_pack_kernel, dim3((A.total16 + 63) / 64), dim3(64), 0, st, A);
+                                       : launch_pack(rc_pack_kernel, dim3((A.total16 + 63) / 64), dim3(64), 0, st, A);
     if (e != cudaSuccess) return e;
     note_launches(1);
     e = smem_optin(reinterpret_cast<const void *>(rows_conv_kernel), (int)P.smem_bytes);

@@ -472,7 +472,7 @@ cudaError_t rows_fc_run(capsconv_op_t op, const Problem &p, const void *a, const
     }
     if (mode != 2 && !probe_skip_pack()) {
         const long long total16 = (long long)pl.wpack_bytes / 16;
-        e = launch_k(fc_pack, dim3((unsigned)((total16 + 63) / 64)), dim3(64), 0, st,
+        e = launch_pack(fc_pack, dim3((unsigned)((total16 + 63) / 64)), dim3(64), 0, st,
                      static_cast<const __nv_bfloat16 *>(b), w8, mode, P.P, P.C, P.Cout, P.N, total16);
         if (e != cudaSuccess) return e;
         note_launches(1);

@@ -224,3 +224,37 @@ def test_rows_deterministic(cc):
     a = cc.bwd_kernel(I, dO, 1, 3, 3, layout="rows")
     b = cc.bwd_kernel(I, dO, 1, 3, 3, layout="rows")
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("second", ["fwd", "dI"])
+def test_rows_k_is_previous_output(cc, oracle_mod, second):
+    """A call whose K is the output of the immediately preceding call on the
+    same stream (no synchronisation between them): the library sees the
+    overlap and packs K fully ordered instead of beside the previous kernel's
+    tail (include/capsconv.h, "Streams").  Exact-integer data, bitwise."""
+    dt = torch.bfloat16
+    L1 = capsinputs.Layer(16, 12, 12, 8, 8, 3, 3, 4, 4, 4, 1)        # walk fwd, O: 16x10x10 x 8 caps
+    L2 = capsinputs.Layer(4, 10, 10, 8, 8, 3, 3, 4, 4, 4, 1)         # K: 3x3 x 8 x 8 caps
+    I1 = to_rows(capsinputs.make_input(L1, "int1", dt).to(DEV))
+    K1 = capsinputs.make_kernel(L1, "int1", dt).to(DEV)
+    n1 = 16 * 10 * 10 * 4 * 8 * 4
+    nk2 = 3 * 3 * 8 * 8 * 16
+    buf = torch.zeros(n1, dtype=dt, device=DEV)
+    O1 = buf.view(16, 10, 10, 4, 8, 4)
+    K2 = buf[:nk2].view(3, 3, 8, 8, 4, 4)
+    I2 = capsinputs.make_input(L2, "int1", dt)
+    dO2 = capsinputs.make_grad_output(L2.o_shape(8, 8), "int1", dt)
+    torch.cuda.synchronize()
+    cc.fwd(I1, K1, 1, out=O1, layout="rows")
+    if second == "fwd":
+        R = cc.fwd(to_rows(I2.to(DEV)), K2, 1, layout="rows")
+    else:
+        R = cc.bwd_data(to_rows(dO2.to(DEV)), K2, 1, L2.H, L2.W, layout="rows")
+    torch.cuda.synchronize()
+    k2 = to_np(K2)
+    assert np.abs(k2).max() > 0
+    if second == "fwd":
+        ref, _ = oracle_mod.fwd(to_np(I2), k2, 1)
+    else:
+        ref, _ = oracle_mod.bwd_data(to_np(dO2), k2, 1, L2.H, L2.W)
+    np.testing.assert_array_equal(to_np(from_rows(R)), oracle_mod.round_bf16(ref))
