@@ -55,15 +55,19 @@ def parse():
     ap.add_argument("--no-dk-stream", action="store_true", help="dK passes on the compute stream (no second chain)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
-    ap.add_argument("--layout", default="rows", choices=["rows", "natural"],
-                    help="capsule-tensor layout of the stack's activations (include/capsconv.h)")
+    ap.add_argument("--layout", default=None, choices=["rows", "natural"],
+                    help="capsule-tensor layout of the stack's activations (include/capsconv.h); default rows for "
+                         "bf16 (its tensor-core kernels), natural for fp32 (the SIMT kernels' own layout)")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-bench oracle parity check")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = 1024 images per rank (default), strong = 1024 images shared by the ranks")
     ap.add_argument("--batch", type=int, default=0,
                     help="override the global batch (e.g. 128/256/512: one rank's share of the batch-1024 stack "
                          "at 8/4/2 GPUs -- the compute side of strong scaling on one GPU)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.layout is None:
+        args.layout = "natural" if args.dtype == "fp32" else "rows"
+    return args
 
 
 def self_launch(args):

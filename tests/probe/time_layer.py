@@ -1,7 +1,7 @@
 """Probe: event-time one pass of one config-5 stack layer (rows layout) with
 either library flavour, L2 flushed between reps; knobs come from the
 environment (read once per process when the plan is built).
-Usage: [CAPSCONV_PROBE_LIB=1] python tests/probe/time_layer.py <layer 1-4> <fwd|dI|dK> [reps]"""
+Usage: [CAPSCONV_PROBE_LIB=1] [DTYPE=fp32] python tests/probe/time_layer.py <layer 1-4> <fwd|dI|dK> [reps]"""
 import os
 import sys
 
@@ -22,10 +22,11 @@ def main():
     cc.load_library(_build.PROBE_LIB if os.environ.get("CAPSCONV_PROBE_LIB") else None)
     dev = "cuda:0"
     L = capsinputs.stack_layers(capsinputs.STACK_BATCH, pkg.output_dims)[li]
+    dt = torch.float32 if os.environ.get("DTYPE") == "fp32" else torch.bfloat16
     Ho, Wo = pkg.output_dims(L.H, L.W, L.KH, L.KW, L.stride)
-    I = capsinputs.make_input(L, dtype=torch.bfloat16, layer_idx=li).to(dev).permute(0, 1, 2, 4, 3, 5).contiguous()
-    K = capsinputs.make_kernel(L, dtype=torch.bfloat16, layer_idx=li).to(dev)
-    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), dtype=torch.bfloat16, layer_idx=li).to(dev)
+    I = capsinputs.make_input(L, dtype=dt, layer_idx=li).to(dev).permute(0, 1, 2, 4, 3, 5).contiguous()
+    K = capsinputs.make_kernel(L, dtype=dt, layer_idx=li).to(dev)
+    dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), dtype=dt, layer_idx=li).to(dev)
     dO = dO.permute(0, 1, 2, 4, 3, 5).contiguous()
     if op == "fwd":
         f = lambda: pkg.fwd(I, K, L.stride, layout="rows")  # noqa: E731
