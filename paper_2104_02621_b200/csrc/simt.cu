@@ -359,9 +359,15 @@ __global__ void __launch_bounds__(128) bwd_data_d4s(DimsT<int> d, const T *__res
         Ks[e] = c0 + j < d.C ? ldf<T>(K + (((size_t)t * d.C + c0 + j) * d.Cout + co) * 16 + k16) : 0.f;
     }
     __syncthreads();
-    const int n = blockIdx.y * blockDim.x + threadIdx.x;
-    if (n >= d.B * d.H * d.W) return;
-    const int w = n % d.W, h = (n / d.W) % d.H, b = n / (d.W * d.H);
+    // stride > 1: threads walk the input pixels phase by phase ((h mod s, w mod s)
+    // outermost per image) so that a warp's lanes take the same taps
+    const int Hq = (d.H + d.s - 1) / d.s, Wq = (d.W + d.s - 1) / d.s, s2 = d.s * d.s;
+    const int v = blockIdx.y * blockDim.x + threadIdx.x;
+    if (v >= d.B * s2 * Hq * Wq) return;
+    const int ww = v % Wq, hh = (v / Wq) % Hq, ph = (v / (Wq * Hq)) % s2, b = v / (Wq * Hq * s2);
+    const int h = hh * d.s + ph / d.s, w = ww * d.s + ph % d.s;
+    if (h >= d.H || w >= d.W) return;
+    const int n = (b * d.H + h) * d.W + w;
     float acc[CG][16];
 #pragma unroll
     for (int j = 0; j < CG; ++j)
@@ -455,6 +461,62 @@ __global__ void __launch_bounds__(128) bwd_kernel_d4g(DimsT<int> d, const T *__r
     for (int j = 0; j < CG; ++j) {
         if (co0 + j >= d.Cout) continue;
         float *out = part + ((size_t)split * ncaps + ((size_t)t * d.C + c) * d.Cout + co0 + j) * 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            reinterpret_cast<float4 *>(out)[i] =
+                make_float4(acc[j][4 * i], acc[j][4 * i + 1], acc[j][4 * i + 2], acc[j][4 * i + 3]);
+    }
+}
+
+// Weight gradient, four input channels per thread: thread = (tap, group of 4 c,
+// c') x one split; lanes run over c' so the four input capsules of a pixel are
+// warp-wide broadcasts and the dO capsule loads are contiguous (20 loads per
+// 256 FMAs; for many output channels, where bwd_kernel_d4g's wider threads lose).
+template <typename T>
+__global__ void __launch_bounds__(128) bwd_kernel_d4c(DimsT<int> d, const T *__restrict__ I, const T *__restrict__ dO,
+                                                      float *__restrict__ part, int nsplit) {
+    constexpr int CC = 4;
+    const int ngc = d.C / CC;
+    const int nthr = d.KH * d.KW * ngc * d.Cout;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nthr) return;
+    const int split = blockIdx.y;
+    const int co = idx % d.Cout, rest = idx / d.Cout;
+    const int c0 = (rest % ngc) * CC, t = rest / ngc;
+    const int q = t % d.KW, p = t / d.KW;
+    const int npix = d.B * d.Ho * d.Wo;
+    const int n0 = (int)((int64_t)npix * split / nsplit), n1 = (int)((int64_t)npix * (split + 1) / nsplit);
+    float acc[CC][16];
+#pragma unroll
+    for (int j = 0; j < CC; ++j)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[j][e] = 0.f;
+    int y = n0 % d.Wo, x = (n0 / d.Wo) % d.Ho, b = n0 / (d.Wo * d.Ho);
+    for (int n = n0; n < n1; ++n) {
+        const int h = x * d.s + p - d.pad, w = y * d.s + q - d.pad;
+        if (h >= 0 && h < d.H && w >= 0 && w < d.W) {
+            float g[16];
+            load_caps16<T>(dO + ((size_t)n * d.Cout + co) * 16, g);
+            const T *ip = I + (((size_t)(b * d.H + h) * d.W + w) * d.C + c0) * 16;
+#pragma unroll
+            for (int j = 0; j < CC; ++j) {
+                float a[16];
+                load_caps16<T>(ip + j * 16, a);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+                            acc[j][tt * 4 + m] = fmaf(a[i * 4 + tt], g[i * 4 + m], acc[j][tt * 4 + m]);
+            }
+        }
+        if (++y == d.Wo) { y = 0; if (++x == d.Ho) { x = 0; ++b; } }
+    }
+    const int ncaps = d.KH * d.KW * d.C * d.Cout;
+#pragma unroll
+    for (int j = 0; j < CC; ++j) {
+        float *out = part + ((size_t)split * ncaps + ((size_t)t * d.C + c0 + j) * d.Cout + co) * 16;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             reinterpret_cast<float4 *>(out)[i] =
@@ -577,8 +639,10 @@ bool fits32(const Problem &p, int64_t fwd_split, int64_t dk_split) {
 // Number of splits of the (b, x', y') reduction for dK: enough threads to
 // fill the machine a few times over, never more than the pixel count.
 int64_t dk_splits(const Problem &p) {
-    const int64_t units = is_d4(p) ? p.KH * p.KW * p.C * (p.Cout >= 4 && p.Cout <= 8 ? (p.Cout + 3) / 4 : p.Cout)
-                                   : p.n_k();
+    const int64_t units = !is_d4(p) ? p.n_k()
+                          : p.C % 4 == 0 ? p.KH * p.KW * (p.C / 4) * p.Cout                       // bwd_kernel_d4c
+                          : p.Cout >= 4 && p.Cout <= 8 ? p.KH * p.KW * p.C * ((p.Cout + 3) / 4)   // bwd_kernel_d4g
+                                         : p.KH * p.KW * p.C * p.Cout;
     const int64_t target = (int64_t)device_info().num_sms * 2048;
     int64_t s = (target + units - 1) / units;
     const int64_t npix = p.n_pix_out();
@@ -648,8 +712,8 @@ cudaError_t bwd_data_impl(const Problem &p, const void *dO, const void *K, void 
     if (vec) {
         const bool i32 = fits32(p, 1, 1);
         const size_t ks_bytes = (size_t)p.KH * p.KW * 4 * p.Cout * 16 * sizeof(float);
-        const int64_t npix = p.B * p.H * p.W;
-        if (i32 && p.C >= 4 && ks_bytes <= (size_t)kSimtSmemMax && (npix + 127) / 128 <= 65535) {
+        const int64_t npix = p.B * (p.s * p.s) * ((p.H + p.s - 1) / p.s) * ((p.W + p.s - 1) / p.s);   // phase grid
+        if (i32 && p.C >= 4 && ks_bytes <= (size_t)kSimtSmemMax && (npix + 127) / 128 <= 65535 && npix < (1 << 30)) {
             cudaError_t e = smem_optin(reinterpret_cast<const void *>(bwd_data_d4s<T>), (int)ks_bytes);
             if (e != cudaSuccess) return e;
             bwd_data_d4s<T><<<dim3((unsigned)((p.C + 3) / 4), blocks_for(npix, 128)), 128, ks_bytes, st>>>(
@@ -688,9 +752,13 @@ cudaError_t bwd_kernel_impl(const Problem &p, const void *I, const void *dO, flo
         // four channels per thread pays for few output channels (stack L1, Cout = 8:
         // 2.71 -> 2.46 ms fp32); with many (L3, Cout = 32) the one-channel
         // threads' broadcast input loads and lower register count win (2.79 vs 4.88)
-        if (fits32(p, 1, nsplit) && p.Cout >= 4 && p.Cout <= 8) {
+        if (fits32(p, 1, nsplit) && p.Cout >= 4 && p.Cout <= 8 && p.C % 4 != 0) {
             const int64_t nthr = p.KH * p.KW * p.C * ((p.Cout + 3) / 4);
             bwd_kernel_d4g<T><<<dim3(blocks_for(nthr, 128), (unsigned)nsplit), 128, 0, st>>>(
+                dims_as<int>(d), (const T *)I, (const T *)dO, part, (int)nsplit);
+        } else if (fits32(p, 1, nsplit) && p.C % 4 == 0) {
+            const int64_t nthr = p.KH * p.KW * (p.C / 4) * p.Cout;
+            bwd_kernel_d4c<T><<<dim3(blocks_for(nthr, 128), (unsigned)nsplit), 128, 0, st>>>(
                 dims_as<int>(d), (const T *)I, (const T *)dO, part, (int)nsplit);
         } else if (fits32(p, 1, nsplit))
             bwd_kernel_d4<T, int><<<grid, 128, 0, st>>>(dims_as<int>(d), (const T *)I, (const T *)dO, part, (int)nsplit);
