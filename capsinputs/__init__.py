@@ -87,6 +87,23 @@ STACK_SAME_LAYERS = [
 ]
 
 
+# 7. the routing-free P-CapsNet training step (PAPER.md:278 /
+#    Fig 7): a primary layer from a one-channel 28x28 image (MNIST-shaped) to
+#    the stack's 24x24 map of 8 capsules of 4x4 -- a plain 5x5 convolution to
+#    128 channels, written as the capsule convolution with C = Cout = 1,
+#    D1 = D2 = 1, D3 = 128 (reading R25) -- then the stack, then one SGD step
+#    on every weight (fp32 master copies).
+PRIMARY = dict(H=28, W=28, KH=5, KW=5, D3=128)
+PRIMARY_SEED_LAYER = 9          # seeds of the image / primary kernel (layer_idx)
+TRAIN_LR = 0.01
+
+
+def primary_layer(batch: int) -> Layer:
+    """The primary layer as a capsule-convolution Layer (reading R25)."""
+    return Layer(B=batch, H=PRIMARY["H"], W=PRIMARY["W"], C=1, Cout=1, KH=PRIMARY["KH"], KW=PRIMARY["KW"],
+                 D1=1, D2=1, D3=PRIMARY["D3"], stride=1)
+
+
 def stack_layers(batch: int, out_hw) -> List[Layer]:
     """Materialise the stack for ``batch`` images.  ``out_hw(H, W, KH, KW, s)``
     is the caller's shape law (oracle or product), so this module stays free

@@ -284,6 +284,21 @@ CAPSCONV_API capsconv_status_t capsconv_bwd_kernel_ex(capsconv_dtype_t dt, capsc
         const void *I, const void *dO, float *dK,
         void *workspace, size_t workspace_bytes, capsconv_stream_t stream);
 
+/* ---- Training-step helper (the routing-free P-CapsNet
+ * training step of PAPER.md:278 / Fig 7): one plain SGD step on a weight
+ * tensor kept in fp32 ("master" copy), with its working copy re-rounded:
+ *   w_master[i] -= lr * grad[i];   w_out[i] = round_wdt(w_master[i])
+ * for i < n, elementwise, in fp32 (RNE to bf16 when wdt = CAPSCONV_BF16;
+ * w_out may be w_master itself when wdt = CAPSCONV_F32).  grad is a dK of
+ * this library (fp32, the layout of K).  w_master and grad are device fp32
+ * arrays of n elements, w_out a device array of n `wdt` elements; caller-
+ * owned, 16-byte aligned; w_out must not overlap grad.  n = 0 is a no-op.
+ * Asynchronous on `stream` like every call; errors as above (NULL pointer
+ * with n > 0 -> CAPSCONV_ERR_NULL, n < 0 or a non-finite lr ->
+ * CAPSCONV_ERR_SHAPE, unknown wdt -> CAPSCONV_ERR_DTYPE). */
+CAPSCONV_API capsconv_status_t capsconv_sgd_update(capsconv_dtype_t wdt, int64_t n, float lr, float *w_master,
+        const float *grad, void *w_out, capsconv_stream_t stream);
+
 /* Static description of a status code. */
 CAPSCONV_API const char *capsconv_status_string(capsconv_status_t status);
 

@@ -18,6 +18,11 @@ Parity status of every function (see DESIGN.md §3 "Oracle pins"):
   stack_fwd_bwd                           -- composition of pinned layers;
                                              pinned by the depth-1 reduction and
                                              finite differences on a tiny stack
+  sgd_update                              -- pinned: hand-computed step
+  primary_to_caps / caps_to_primary       -- pinned: inverse pair, channel order
+                                             on a one-hot map (reading R25)
+  train_step                              -- composition of pinned pieces; its
+                                             primary layer pinned to torch conv2d
 """
 from .oracle import (  # noqa: F401
     build,
@@ -33,5 +38,9 @@ from .oracle import (  # noqa: F401
     num_threads,
     set_num_threads,
     stack_fwd_bwd,
+    sgd_update,
+    primary_to_caps,
+    caps_to_primary,
+    train_step,
     OracleError,
 )

@@ -257,3 +257,43 @@ def stack_fwd_bwd(X, Ks, strides, dY, bf16_boundaries: bool, pads=None):
         dIabs[li] = dIa
         g = dI
     return acts, g, dKs, {"fwd": fabs_, "dK": dKabs, "dI": dIabs}
+
+
+def sgd_update(w, g, lr):
+    """One SGD step (plain gradient descent, no momentum):
+    w - lr * g, exact in float64 (the device computes it with one fp32 fma)."""
+    return _f64(w) - float(lr) * _f64(g)
+
+
+def primary_to_caps(prim, C, D):
+    """Primary-layer output (B, H, W, 1, 1, C*D*D), channel o = (d1*C + c)*D + d2
+    (the rows order, reading R25) -> the natural capsule map (B, H, W, C, D, D)."""
+    p = _f64(prim)
+    B, H, W = p.shape[:3]
+    return np.ascontiguousarray(p.reshape(B, H, W, D, C, D).transpose(0, 1, 2, 4, 3, 5))
+
+
+def caps_to_primary(x):
+    """Inverse of primary_to_caps: (B, H, W, C, D, D) -> (B, H, W, 1, 1, C*D*D)."""
+    x = _f64(x)
+    B, H, W, C, D1, D2 = x.shape
+    return np.ascontiguousarray(x.transpose(0, 1, 2, 4, 3, 5).reshape(B, H, W, 1, 1, C * D1 * D2))
+
+
+def train_step(img, Kp, Ks, strides, dY, lr, bf16_boundaries: bool):
+    """The routing-free P-CapsNet training step:
+    primary layer (the capsule convolution with C = Cout = D1 = D2 = 1, reading
+    R25) -> the stack (stack_fwd_bwd) -> primary dK from the stack's dX -> one
+    SGD step on every weight.  dY is the stack output gradient in the natural
+    layout.  Returns (new weights [Kp, K_0, ...] in float64, dKs [dKp, dK_0, ...],
+    abs-sums [of dKp, dK_0, ...])."""
+    C0, D = Ks[0].shape[2], Ks[0].shape[4]
+    prim, _ = fwd(img, Kp, 1)
+    if bf16_boundaries:
+        prim = round_bf16(prim)
+    X = primary_to_caps(prim, C0, D)
+    acts, dX, dKs, absd = stack_fwd_bwd(X, Ks, strides, dY, bf16_boundaries)
+    dprim = caps_to_primary(dX)
+    dKp, dKp_abs = bwd_kernel(img, dprim, 1, Kp.shape[0], Kp.shape[1])
+    new = [sgd_update(Kp, dKp, lr)] + [sgd_update(K, g, lr) for K, g in zip(Ks, dKs)]
+    return new, [dKp] + list(dKs), [dKp_abs] + list(absd["dK"])

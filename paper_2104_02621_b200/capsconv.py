@@ -73,6 +73,8 @@ def load_library(path: Optional[str] = None):
         for name in ("capsconv_workspace_bytes_ex", "capsconv_select_path_ex", "capsconv_fwd_ex",
                      "capsconv_bwd_data_ex", "capsconv_bwd_kernel_ex"):
             getattr(lib, name).restype = ci
+        lib.capsconv_sgd_update.argtypes = [ctypes.c_int, i64, ctypes.c_float, vp, vp, vp, vp]
+        lib.capsconv_sgd_update.restype = ctypes.c_int
         lib.capsconv_workspace_bytes_slices.argtypes = [ctypes.c_int, ctypes.c_int] + [i64] * 12 + [ctypes.POINTER(sz)]
         for name in ("capsconv_fwd_slices", "capsconv_bwd_data_slices", "capsconv_bwd_kernel_slices"):
             getattr(lib, name).argtypes = [ctypes.c_int] + [i64] * 12 + [vp, vp, vp, vp, sz, vp]
@@ -292,6 +294,30 @@ def bwd_kernel(I: torch.Tensor, dO: torch.Tensor, stride: int, KH: int, KW: int,
         raise ValueError("out must be float32 of the kernel's shape")
     ext = (B, H, W, C, Cout, KH, KW, D1, D2, D3, stride, pad)
     return _call("capsconv_bwd_kernel", OP_BWD_KERNEL, I.dtype, ext, I, dO, out, stream, layout)
+
+
+def sgd_update(w_master: torch.Tensor, grad: torch.Tensor, lr: float, w_out: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """One SGD step (capsconv_sgd_update): w_master -= lr * grad in fp32, then
+    w_out = w_master rounded to w_out's dtype (bf16 or fp32; default: w_master
+    itself).  Returns w_out."""
+    dev = _need_cuda(w_master, grad)
+    if w_out is None:
+        w_out = w_master
+    _need_cuda(w_out)
+    if w_master.dtype != torch.float32 or grad.dtype != torch.float32:
+        raise ValueError("w_master and grad must be float32")
+    n = w_master.numel()
+    if grad.numel() != n or w_out.numel() != n:
+        raise ValueError("w_master, grad and w_out must have the same number of elements")
+    lib = load_library()
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        st = lib.capsconv_sgd_update(_dt(w_out.dtype), n, ctypes.c_float(lr), ctypes.c_void_p(w_master.data_ptr()),
+                                     ctypes.c_void_p(grad.data_ptr()), ctypes.c_void_p(w_out.data_ptr()),
+                                     ctypes.c_void_p(s.cuda_stream))
+    _check(st, "sgd_update")
+    return w_out
 
 
 # ------------------------------------------------------------ S-slice capsules (R22)

@@ -4,6 +4,7 @@
 // Every argument is validated before anything is enqueued, so a non-OK
 // status other than CAPSCONV_ERR_CUDA leaves all buffers untouched.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -560,6 +561,23 @@ capsconv_status_t capsconv_bwd_kernel_slices(capsconv_dtype_t dt, int64_t B, int
     if (e == cudaSuccess) e = slices_extract_dk(dKx, dK, KH * KW, C, Cout, S, D2 * D3, cs);
     pack_guard_end(cs, dK, (size_t)pe.n_k() * 4);   // bound: the expanded dK
     return finish(e, "capsconv_bwd_kernel_slices");
+}
+
+capsconv_status_t capsconv_sgd_update(capsconv_dtype_t wdt, int64_t n, float lr, float *w_master,
+                                      const float *grad, void *w_out, capsconv_stream_t stream) {
+    if (wdt != CAPSCONV_BF16 && wdt != CAPSCONV_F32) return fail(CAPSCONV_ERR_DTYPE, "unknown weight dtype %d", (int)wdt);
+    if (n < 0) return fail(CAPSCONV_ERR_SHAPE, "n = %lld < 0", (long long)n);
+    if (!std::isfinite(lr)) return fail(CAPSCONV_ERR_SHAPE, "learning rate is not finite");
+    if (n == 0) return CAPSCONV_OK;
+    if (!w_master || !grad || !w_out) return fail(CAPSCONV_ERR_NULL, "a tensor pointer is NULL");
+    if (!aligned16(w_master) || !aligned16(grad) || !aligned16(w_out))
+        return fail(CAPSCONV_ERR_SHAPE, "sgd_update pointers must be 16-byte aligned");
+    const capsconv_status_t st = check_device();
+    if (st) return st;
+    const cudaStream_t cs = (cudaStream_t)stream;
+    const cudaError_t e = sgd_update(wdt, n, lr, w_master, grad, w_out, cs);
+    pack_guard_end(cs, w_out, (size_t)n * (wdt == CAPSCONV_BF16 ? 2 : 4));   // w_out is the next call's K
+    return finish(e, "capsconv_sgd_update");
 }
 
 const char *capsconv_status_string(capsconv_status_t s) {

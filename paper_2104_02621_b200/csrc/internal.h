@@ -116,6 +116,10 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 #endif
 
+// ---------------------------------------------------------------- optimizer step (optim.cu)
+cudaError_t sgd_update(capsconv_dtype_t wdt, int64_t n, float lr, float *w, const float *g, void *out,
+                       cudaStream_t st);
+
 // ---------------------------------------------------------------- SIMT path
 size_t simt_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t simt_fwd(const Problem &p, const void *I, const void *K, void *O, void *ws, size_t ws_bytes,
