@@ -49,7 +49,8 @@ def parse():
                     help="ours; reference = the CPU oracle; paper-alg34 = the paper's Algorithms 3/4 literally "
                          "(materialised im2col / extends + cuBLAS strided-batched matmuls via torch) on the GPU, "
                          "a context row (SURVEY NEXT-3 (ii))")
-    ap.add_argument("--config", default="stack", choices=["stack", "stack_same", "layer_s1", "layer_s2", "fc"])
+    ap.add_argument("--config", default="stack",
+                    choices=["stack", "stack_same", "layer_s1", "layer_s2", "fc", "pcapsnet_train"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce on the compute stream")
     ap.add_argument("--no-dk-stream", action="store_true", help="dK passes on the compute stream (no second chain)")
@@ -92,6 +93,10 @@ def workload(cfg: str, world: int):
         specs = [LayerSpec(*l) for l in capsinputs.STACK_LAYERS]
         si = capsinputs.STACK_INPUT
         return specs, si["H"], si["W"], si["D"], capsinputs.STACK_BATCH, "capsnet_stack_3conv_fc_b1024"
+    if cfg == "pcapsnet_train":   # primary layer + the stack + SGD on every weight
+        specs = [LayerSpec(*l) for l in capsinputs.STACK_LAYERS]
+        si = capsinputs.STACK_INPUT
+        return specs, si["H"], si["W"], si["D"], capsinputs.STACK_BATCH, "pcapsnet_train_step_b1024"
     if cfg == "stack_same":   # zero-padded ("same") 3x3 layers, SURVEY NEXT-2
         specs = [LayerSpec(*l) for l in capsinputs.STACK_SAME_LAYERS]
         si = capsinputs.STACK_INPUT
@@ -219,9 +224,19 @@ class GraphCallTimer:
             out.setdefault(key, []).append(a.elapsed_time(b))
 
 
+def pass_name(li, kind):
+    return ("L%d_%s" % (li + 1, kind)) if li >= 0 else ("SGD" if kind == "opt" else "P_%s" % kind)
+
+
+def pass_flops(st, li, kind):
+    return st.layer_flops(li) if li >= 0 else st.aux_flops(kind)
+
+
 def pass_bytes(st, li, kind, elem):
     """Algorithmic HBM bytes of one pass: every operand moved once
     (SURVEY §8(d)): fwd |I|+|K|+|O|; dI |dO|+|K|+|dI|; dK |I|+|dO|+4|dK|."""
+    if li < 0:
+        return st.aux_bytes(kind, elem)
     sp = st.specs[li]
     h, w = st.hw[li]
     ho, wo = st.hw[li + 1]
@@ -238,6 +253,8 @@ def pass_bytes(st, li, kind, elem):
 
 def pass_write_bytes(st, li, kind, elem):
     """The part of pass_bytes the pass writes: |O| (fwd), |dI| (dI), 4|dK| (dK)."""
+    if li < 0:
+        return st.aux_write_bytes(kind, elem)
     sp = st.specs[li]
     h, w = st.hw[li]
     ho, wo = st.hw[li + 1]
@@ -261,10 +278,20 @@ def run_reference(args, rank, world):
     flops_per_image, Ks, strides, layers = stack_oracle_setup(specs, H, W, D, dtype)
 
     Xa, dYa = stack_oracle_inputs(layers, specs, H, W, D, gbatch, dtype, gbatch)
+    train = args.config == "pcapsnet_train"
+    if train:   # oracle.train_step (primary layer + stack + SGD)
+        P = capsinputs.primary_layer(gbatch)
+        Kp64 = capsinputs.make_kernel(P, dtype=dtype, layer_idx=capsinputs.PRIMARY_SEED_LAYER).to(torch.float64).numpy()
+        imga = capsinputs.make_input(P, dtype=dtype, layer_idx=capsinputs.PRIMARY_SEED_LAYER).to(torch.float64).numpy()
+        prim = 2 * 1 * H * W * specs[0].C * D * D * capsinputs.PRIMARY["KH"] * capsinputs.PRIMARY["KW"]
+        flops_per_image += 2 * prim
 
     def one(b):
         t0 = time.perf_counter()
-        oracle.stack_fwd_bwd(Xa[:b], Ks, strides[0], dYa[:b], dtype == torch.bfloat16, pads=strides[1])
+        if train:
+            oracle.train_step(imga[:b], Kp64, Ks, strides[0], dYa[:b], capsinputs.TRAIN_LR, True)
+        else:
+            oracle.stack_fwd_bwd(Xa[:b], Ks, strides[0], dYa[:b], dtype == torch.bfloat16, pads=strides[1])
         return time.perf_counter() - t0
 
     t1 = one(1)
@@ -463,6 +490,83 @@ def run_paper_alg34(args, rank, world):
 
 
 # ---------------------------------------------------------------- our arm
+class TrainBench:
+    """bench.py's view of a CapsTrainer (config pcapsnet_train):
+    the stack's attributes, plus the primary layer (pass layer -1: fwd, dK) and
+    the SGD step (layer -1, "opt") for the per-pass table."""
+
+    def __init__(self, trainer):
+        self.tr = trainer
+        self.stack = trainer.stack
+
+    def __getattr__(self, name):          # specs, hw, D, batch, acts, out, dk_stream, layer_flops ...
+        return getattr(self.stack, name)
+
+    @property
+    def dK(self):                         # what a step returns (read back by the e2e leg)
+        return [self.tr.masterP] + self.tr.masters
+
+    def step(self, x, dy, timer=None):
+        return self.tr.step(x, dy, timer)
+
+    def step_flops(self, batch=None):
+        return self.tr.step_flops()
+
+    def _prim_elems(self):
+        b, (h, w) = self.stack.batch, self.stack.hw[0]
+        img = b * self.tr.Himg * self.tr.Wimg
+        return img, b * h * w * self.tr.KP.shape[5], self.tr.KP.numel()
+
+    def aux_flops(self, kind):
+        nimg, nprim, nk = self._prim_elems()
+        if kind == "opt":
+            return 2 * sum(m.numel() for m in self.dK)
+        return 2 * nprim * self.tr.KPH * self.tr.KPW
+
+    def aux_bytes(self, kind, elem):
+        nimg, nprim, nk = self._prim_elems()
+        if kind == "fwd":
+            return (nimg + nk + nprim) * elem
+        if kind == "dK":
+            return (nimg + nprim) * elem + 4 * nk
+        n = sum(m.numel() for m in self.dK)       # master read+write, dK read, working copy write
+        return n * (4 + 4 + 4 + elem)
+
+    def aux_write_bytes(self, kind, elem):
+        nimg, nprim, nk = self._prim_elems()
+        if kind == "fwd":
+            return nprim * elem
+        if kind == "dK":
+            return 4 * nk
+        return sum(m.numel() for m in self.dK) * (4 + elem)
+
+
+def train_parity(pkg, specs, H, W, D, PB, Kp, weights, img_nat, dY_nat, dev):
+    """The training step on the first PB images (same trainer code, eager)
+    against oracle.train_step: max normalised error of every dK and of every
+    updated master weight (as lr * dK error)."""
+    import oracle
+    from paper_2104_02621_b200.train import CapsTrainer
+    lr = capsinputs.TRAIN_LR
+    tr = CapsTrainer(specs, H, W, D, PB, Kp, weights, dev, lr)
+    tr.step(img_nat.to(dev), dY_nat.permute(0, 1, 2, 4, 3, 5).contiguous().to(dev))
+    torch.cuda.synchronize()
+    f64 = lambda t: t.detach().to("cpu", torch.float64).numpy()  # noqa: E731
+    new, rdK, den = oracle.train_step(f64(img_nat), f64(Kp), [f64(k) for k in weights], [s.stride for s in specs],
+                                      f64(dY_nat), lr, True)
+    names = ["dKp"] + ["dK%d" % (i + 1) for i in range(len(specs))]
+    errs = {}
+    for name, got, ref, a in zip(names, [tr.dKP] + list(tr.stack.dK), rdK, den):
+        errs[name] = float((abs(f64(got) - ref) / (a + 1e-30)).max())
+    for i, (m, ref, a) in enumerate(zip([tr.masterP] + tr.masters, new, den)):
+        errs["W%d" % i] = float((abs(f64(m) - ref) / (lr * a + 1e-6)).max())
+    worst = max(errs.values())
+    tol = 2e-2
+    return {"images": PB, "max_norm_err": {k: float("%.3g" % v) for k, v in errs.items()},
+            "worst": float("%.3g" % worst), "tol": tol, "pass": bool(worst <= tol),
+            "note": "W_i: |w_gpu - w_oracle| / (lr * sum|dK terms| + 1e-6) after the SGD step"}
+
+
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -521,9 +625,25 @@ def main():
     X = X_host.to(dev)
     dY = dY_host.to(dev)
 
-    st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap, layout=args.layout,
-                   dk_stream=not args.no_dk_stream)
-    gflops = st.step_flops(batch=gbatch)          # whole-job algorithmic flops per step
+    train = args.config == "pcapsnet_train"
+    if train:   # the input is the image; the stack's input is the primary layer's output
+        if dtype != torch.bfloat16 or args.layout != "rows":
+            raise SystemExit("bench: --config pcapsnet_train runs bf16 in the rows layout")
+        from paper_2104_02621_b200.train import CapsTrainer
+        P = capsinputs.primary_layer(gbatch)
+        Kp = capsinputs.make_kernel(P, dtype=dtype, layer_idx=capsinputs.PRIMARY_SEED_LAYER)
+        img_host = capsinputs.make_input(P, dtype=dtype, layer_idx=capsinputs.PRIMARY_SEED_LAYER,
+                                         batch_offset=lo, batch=batch)
+        img_nat = img_host[:PB].clone()
+        X_host = img_host.pin_memory()
+        X = X_host.to(dev)
+        st = TrainBench(CapsTrainer(specs, H, W, D, batch, Kp, weights, dev, capsinputs.TRAIN_LR,
+                                    overlap=not args.no_overlap, dk_stream=not args.no_dk_stream))
+        gflops = st.step_flops() * world
+    else:
+        st = CapsStack(specs, H, W, D, batch, weights, dev, overlap=not args.no_overlap, layout=args.layout,
+                       dk_stream=not args.no_dk_stream)
+        gflops = st.step_flops(batch=gbatch)          # whole-job algorithmic flops per step
     peaks = load_peaks()
 
     # L2 flush buffer: 2x the L2 size, rewritten between timed steps
@@ -645,12 +765,12 @@ def main():
     for (li, kind), v in sorted(calls.items()):
         avg = sum(v) / len(v)
         byts = pass_bytes(st, li, kind, elem)
-        fl = st.layer_flops(li)
+        fl = pass_flops(st, li, kind)
         gbs = byts / (avg * 1e-3) / 1e9
         tr = max(byts / (peaks["hbm_gbs"] * 1e9), fl / (cpeak * 1e12)) * 1e3
         tw = max(tr, pass_write_bytes(st, li, kind, elem) / (write_gbs * 1e9) * 1e3)
         t_roof_sum += tr
-        per_pass["L%d_%s" % (li + 1, kind)] = {"ms": round(avg, 5), "GB_s": round(gbs, 1),
+        per_pass[pass_name(li, kind)] = {"ms": round(avg, 5), "GB_s": round(gbs, 1),
                                                 "TFLOP_s": round(fl / (avg * 1e-3) / 1e12, 1),
                                                 "roof_frac": round(tr / avg, 3),
                                                 "wfloor_frac": round(tw / avg, 3)}
@@ -661,12 +781,12 @@ def main():
     try:   # the committed captures are of the bf16 rows kernels of the stack
         if dtype == torch.bfloat16 and args.layout == "rows" and args.config == "stack":
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get("L%d_%s" % (bli + 1, bkind))
+                traffic = json.load(f).get(pass_name(bli, bkind))
     except Exception:
         pass
     # the binding roof of the dominant pass: HBM time of its algorithmic bytes
     # vs tensor time of its algorithmic flops, whichever is longer
-    bflops = st.layer_flops(bli)
+    bflops = pass_flops(st, bli, bkind)
     t_hbm = bbytes / (peaks["hbm_gbs"] * 1e9)
     # kernels are timed inside a long step: the sustained tensor figure applies
     t_tc = bflops / (cpeak * 1e12)
@@ -678,7 +798,7 @@ def main():
         achieved = bbytes / (bavg * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4)}
-    roofline.update({"traffic": traffic, "kernel": "L%d_%s" % (bli + 1, bkind), "bytes_per_launch": bbytes,
+    roofline.update({"traffic": traffic, "kernel": pass_name(bli, bkind), "bytes_per_launch": bbytes,
                      "flops_per_launch": bflops,
                      "peak_src": peaks["src"] if dtype == torch.bfloat16 or t_tc <= t_hbm or "FFMA" in peaks["src"]
                      else "derived: SMs x 128 FFMA lanes x 2 x max SM clock",
@@ -742,9 +862,19 @@ def main():
             import oracle
             oracle.build()
             fl1, Ks, strides, layers = stack_oracle_setup(specs, H, W, D, dtype)
+            if train:
+                fl1 = st.step_flops() / batch
+                Kp64 = Kp.to(torch.float64).numpy()
 
             def timed(b):
                 Xs, dYs = stack_oracle_inputs(layers, specs, H, W, D, b, dtype, gbatch)
+                if train:
+                    imgs = capsinputs.make_input(capsinputs.primary_layer(gbatch), dtype=dtype,
+                                                 layer_idx=capsinputs.PRIMARY_SEED_LAYER, batch=b)
+                    imgs = imgs.to(torch.float64).numpy()
+                    t0 = time.perf_counter()
+                    oracle.train_step(imgs, Kp64, Ks, strides[0], dYs, capsinputs.TRAIN_LR, True)
+                    return time.perf_counter() - t0
                 t0 = time.perf_counter()
                 oracle.stack_fwd_bwd(Xs, Ks, strides[0], dYs, dtype == torch.bfloat16, pads=strides[1])
                 return time.perf_counter() - t0
@@ -781,7 +911,10 @@ def main():
     parity = None
     if rank == 0 and not args.no_parity:
         try:
-            parity = parity_check(pkg, specs, H, W, D, PB, weights, X_nat, dY_nat, dtype, dev, args.layout)
+            if train:
+                parity = train_parity(pkg, specs, H, W, D, PB, Kp, weights, img_nat, dY_nat, dev)
+            else:
+                parity = parity_check(pkg, specs, H, W, D, PB, weights, X_nat, dY_nat, dtype, dev, args.layout)
         except Exception as e:
             parity = {"pass": False, "error": str(e)[:200]}
 
@@ -794,7 +927,10 @@ def main():
             "config": {"workload": name, "global_batch": gbatch, "per_rank_batch": batch,
                        "layers": ["%dx%d s%d%s %d->%d" % (s.KH, s.KW, s.stride, " p%d" % s.pad if s.pad else "", s.C,
                                                           s.Cout) for s in specs],
-                       "input": "%dx%dx%d capsules %dx%d" % (H, W, specs[0].C, D, D),
+                       "input": ("%dx%dx1 image -> %dx%d primary layer -> %dx%dx%d capsules %dx%d, SGD lr %g" % (
+                           capsinputs.PRIMARY["H"], capsinputs.PRIMARY["W"], capsinputs.PRIMARY["KH"],
+                           capsinputs.PRIMARY["KW"], H, W, specs[0].C, D, D, capsinputs.TRAIN_LR) if train
+                           else "%dx%dx%d capsules %dx%d" % (H, W, specs[0].C, D, D)),
                        "layout": args.layout,
                        "parallelism": "dp%d" % world, "l2": "flushed between timed steps (%d MiB write)" % (flush.numel() >> 20),
                        "allreduce": "per-layer dK fp32 SUM on a side stream" if world > 1 else None,

@@ -212,6 +212,7 @@ static size_t workspace_for(capsconv_op_t op, const Problem &p) {
         size_t a = mma_workspace_bytes(op, p), b = simt_workspace_bytes(op, p);
         return a > b ? a : b;
     }
+    if (primary_supported(p)) return std::max(primary_workspace_bytes(op, p), simt_workspace_bytes(op, p));
     return simt_workspace_bytes(op, p);
 }
 
@@ -279,6 +280,10 @@ static cudaError_t dispatch(capsconv_op_t op, const Problem &p, const void *a, c
                             size_t ws_bytes, cudaStream_t cs) {
     if (p.layout == CAPSCONV_LAYOUT_ROWS) return dispatch_rows(op, p, a, b, out, ws, ws_bytes, cs);
     const size_t need = workspace_for(op, p);
+    if (op != CAPSCONV_OP_BWD_DATA && primary_supported(p) && aligned16(a) && aligned16(b) && aligned16(out) &&
+        aligned16(ws) && ws_bytes >= primary_workspace_bytes(op, p))   // one-channel plain convolution (primary.cu)
+        return op == CAPSCONV_OP_FWD ? primary_fwd(p, a, b, out, cs)
+                                     : primary_bwd_kernel(p, a, b, static_cast<float *>(out), ws, cs);
     const bool mma = choose_path(op, p) == CAPSCONV_PATH_MMA && aligned16(a) && aligned16(b) && aligned16(out) &&
                      (need == 0 || aligned16(ws));
     switch (op) {

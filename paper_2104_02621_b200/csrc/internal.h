@@ -116,6 +116,15 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 #endif
 
+// ---------------------------------------------------------------- primary layer (primary.cu)
+// The one-channel plain convolution of the training step's primary layer
+// (C = D1 = D2 = 1, stride 1, no padding, N = Cout*D3 in {32, 64, 128, 256},
+// 3x3 / 5x5 / 7x7): fwd and dK (dI has no consumer; the general path takes it).
+bool primary_supported(const Problem &p);
+size_t primary_workspace_bytes(capsconv_op_t op, const Problem &p);
+cudaError_t primary_fwd(const Problem &p, const void *img, const void *K, void *O, cudaStream_t st);
+cudaError_t primary_bwd_kernel(const Problem &p, const void *img, const void *dO, float *dK, void *ws, cudaStream_t st);
+
 // ---------------------------------------------------------------- optimizer step (optim.cu)
 cudaError_t sgd_update(capsconv_dtype_t wdt, int64_t n, float lr, float *w, const float *g, void *out,
                        cudaStream_t st);

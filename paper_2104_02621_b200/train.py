@@ -71,18 +71,28 @@ class CapsTrainer:
         prim = 2 * b * h * w * self.KP.shape[5] * self.KPH * self.KPW
         return self.stack.step_flops() + 2 * prim
 
-    def step(self, img: torch.Tensor, dy: torch.Tensor) -> List[torch.Tensor]:
+    def step(self, img: torch.Tensor, dy: torch.Tensor, timer=None) -> List[torch.Tensor]:
         """One training step on `img` (B, Himg, Wimg, 1, 1, 1) with the upstream
         gradient `dy` of the stack output (rows layout); returns the fp32
-        master weights [primary, layer 0, ...] after the update."""
+        master weights [primary, layer 0, ...] after the update.  `timer`
+        (bench.py) brackets every pass; the primary layer's passes are layer -1."""
         ops = self.ops
+        if timer: timer.begin(-1, "fwd")
         ops.fwd(img, self.KP, 1, out=self.prim)                       # primary layer
-        self.stack.forward(self.rows_view(self.prim))
-        self.stack.backward(dy)                                       # dK of every layer, dX = stack.grads[0]
+        if timer: timer.end(-1, "fwd")
+        if timer is None:
+            self.stack.forward(self.rows_view(self.prim))
+            self.stack.backward(dy)                                   # dK of every layer, dX = stack.grads[0]
+        else:
+            self.stack.step(self.rows_view(self.prim), dy, timer)
         g0 = self.stack.grads[0]
         dprim = g0.view(g0.shape[0], g0.shape[1], g0.shape[2], 1, 1, -1)
+        if timer: timer.begin(-1, "dK")
         ops.bwd_kernel(img, dprim, 1, self.KPH, self.KPW, out=self.dKP)
+        if timer: timer.end(-1, "dK")
+        if timer: timer.begin(-1, "opt")
         ops.sgd_update(self.masterP, self.dKP, self.lr, self.KP)
         for m, g, k in zip(self.masters, self.stack.dK, self.stack.K):
             ops.sgd_update(m, g, self.lr, k)
+        if timer: timer.end(-1, "opt")
         return [self.masterP] + self.masters

@@ -114,3 +114,39 @@ def test_sgd_update_exact(cc):
         cc.sgd_update(w2, g, 0.125)               # fp32 working copy = the master itself
         torch.cuda.synchronize()
         assert torch.equal(w2, w)
+
+
+PRIMARY_CASES = [
+    # B, H, W, K, N (= Cout * D3), Cout
+    (3, 28, 28, 5, 128, 1),
+    (2, 11, 9, 3, 32, 1),
+    (2, 13, 17, 7, 64, 2),
+    (1, 9, 12, 5, 256, 4),
+]
+
+
+@pytest.mark.parametrize("case", PRIMARY_CASES, ids=lambda c: "x".join(map(str, c)))
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+def test_primary_layer_kernels(cc, oracle_mod, case, dtype):
+    """The one-channel plain-convolution kernels (csrc/primary.cu: C = D1 = D2
+    = 1) against the oracle, fwd and dK, random data; also exact-integer data
+    bitwise (sums of at most 49 products of small integers)."""
+    B, H, W, K, N, Cout = case
+    L = capsinputs.Layer(B=B, H=H, W=W, C=1, Cout=Cout, KH=K, KW=K, D1=1, D2=1, D3=N // Cout, stride=1)
+    Ho, Wo = H - K + 1, W - K + 1
+    for kind in ("uniform", "int"):
+        img = capsinputs.make_input(L, kind, dtype)
+        Kp = capsinputs.make_kernel(L, kind, dtype)
+        dO = capsinputs.make_grad_output(L.o_shape(Ho, Wo), kind, dtype)
+        O = cc.fwd(img.to(DEV), Kp.to(DEV), 1)
+        dK = cc.bwd_kernel(img.to(DEV), dO.to(DEV), 1, K, K)
+        torch.cuda.synchronize()
+        rO, aO = oracle_mod.fwd(to_np(img), to_np(Kp), 1)
+        rdK, adK = oracle_mod.bwd_kernel(to_np(img), to_np(dO), 1, K, K)
+        if kind == "int":
+            want = oracle_mod.round_bf16(rO) if dtype == torch.bfloat16 else rO
+            np.testing.assert_array_equal(to_np(O), want)
+            np.testing.assert_array_equal(to_np(dK), rdK)
+        else:
+            assert_close(to_np(O), rO, aO, dtype, "primary fwd")
+            assert_close(to_np(dK), rdK, adK, torch.float32, "primary dK")
