@@ -11,7 +11,11 @@
 // they write (fwd) or read (dK).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "internal.h"
+#include "rows.cuh"
+#include "umma.cuh"
 
 namespace capsconv {
 namespace {
@@ -92,6 +96,169 @@ __global__ void __launch_bounds__(128) primary_fwd_kernel(const T *__restrict__ 
         pr_store32<T>(O + (size_t)pix0 * N + g * 32, a0);
         if (v1) pr_store32<T>(O + (size_t)pix1 * N + g * 32, a1);
     }
+}
+
+// Forward on the tensor cores (bf16, N = 128, KH*KW <= 32): a tile of 128
+// output pixels is one MMA row block; its A operand (128 pixels x 32 taps,
+// the 5x5 patch padded with zeros) is gathered by the four producer warps
+// straight into the no-swizzle K-major core-matrix layout (element (m, k) at
+// (k/8)*2048 + m*16 + (k%8)*2: each thread writes its own pixel's four
+// 16-byte chunks, conflict-free), B = the 128 x 32 weight image staged once;
+// two 128x128x16 MMAs per tile into one of two TMEM accumulators; the same
+// warps drain the previous tile (each thread its pixel's 128 channels =
+// 256 contiguous bytes).  Persistent: one CTA per SM walks tiles blockIdx.x,
+// + gridDim.x, ...
+constexpr int kPtN = 128, kPtK = 32;
+constexpr uint32_t kPtStage = 128u * kPtK * 2u;   // 8 KB A stage
+constexpr uint32_t kPtB = kPtN * kPtK * 2u;       // 8 KB weights
+constexpr uint32_t kPtSmem = 2 * kPtStage + kPtB + 4 * 8192u;
+
+template <int KH, int KW>
+__global__ void __launch_bounds__(160, 1) primary_tc_fwd_kernel(const __nv_bfloat16 *__restrict__ img,
+                                                                const __nv_bfloat16 *__restrict__ K,
+                                                                __nv_bfloat16 *__restrict__ O, int B, int H, int W) {
+    using namespace umma;
+    // A stages | weights | per-warp output staging (32 pixels x 256 B, 16-byte chunks swizzled by row)
+    extern __shared__ __align__(1024) uint8_t sm[];   // kPtSmem bytes
+    __shared__ uint64_t afull[2], aempty[2], accf[2], acce[2];
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const uint32_t a0 = smem_u32(sm), bs = a0 + 2 * kPtStage, ob = bs + kPtB + (uint32_t)(warp & 3) * 8192u;
+    constexpr int ntap = KH * KW;
+    const int Ho = H - KH + 1, Wo = W - KW + 1, npix = B * Ho * Wo;
+    const int ntiles = (npix + 127) / 128;
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(afull + i, 128);
+            mbar_init(aempty + i, 1);
+            mbar_init(accf + i, 1);
+            mbar_init(acce + i, 128);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 4) tmem_alloc_dyn(&tslot, 256);
+    pdl_wait();
+    if (tid < 128) {   // weights: row n = tid, k = tap (zero past ntap)
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int k0 = 2 * j, k1 = 2 * j + 1;
+            __nv_bfloat162 h;
+            h.x = k0 < ntap ? K[(size_t)k0 * kPtN + tid] : __float2bfloat16_rn(0.f);
+            h.y = k1 < ntap ? K[(size_t)k1 * kPtN + tid] : __float2bfloat16_rn(0.f);
+            w[j] = *reinterpret_cast<uint32_t *>(&h);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(bs + (uint32_t)c * 2048u + (uint32_t)tid * 16u),
+                         "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3])
+                         : "memory");
+        fence_proxy_async_smem();
+    }
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = tslot;
+    const int nk = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (warp == 4) {
+        // ------------------------------------------------------------ MMA
+        const uint32_t idesc = idesc_bf16(128, kPtN, 0, 0);
+        for (int k = 0; k < nk; ++k) {
+            const int s = k & 1;
+            const uint32_t ph = (uint32_t)(k >> 1) & 1u;
+            mbar_wait(afull + s, ph);
+            mbar_wait(acce + s, ph ^ 1u);
+            fence_after_sync();
+            const uint32_t as = a0 + (uint32_t)s * kPtStage;
+#pragma unroll
+            for (int ks = 0; ks < kPtK / 16; ++ks) {
+                const uint64_t ad = smem_desc(as + (uint32_t)ks * 4096u, 2048u, 128u);
+                const uint64_t bd = smem_desc(bs + (uint32_t)ks * 4096u, 2048u, 128u);
+                rows::mma_ss_elect(tmem + (uint32_t)s * kPtN, ad, bd, idesc, ks > 0 ? 1u : 0u);
+            }
+            if (elect_one()) {
+                mma_commit(aempty + s);
+                mma_commit(accf + s);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------------------ im2col producer + epilogue
+        for (int k = 0; k <= nk; ++k) {
+            if (k < nk) {
+                const int s = k & 1;
+                mbar_wait(aempty + s, ((uint32_t)(k >> 1) & 1u) ^ 1u);
+                const int pix = ((int)blockIdx.x + k * (int)gridDim.x) * 128 + tid;
+                uint32_t w[16];
+                if (pix < npix) {
+                    const int y = pix % Wo, x = (pix / Wo) % Ho, b = pix / (Wo * Ho);
+                    const __nv_bfloat16 *ip = img + ((size_t)b * H + x) * W + y;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int t0 = 2 * j, t1 = 2 * j + 1;
+                        __nv_bfloat162 h;
+                        h.x = t0 < ntap ? ip[(size_t)(t0 / KW) * W + t0 % KW] : __float2bfloat16_rn(0.f);
+                        h.y = t1 < ntap ? ip[(size_t)(t1 / KW) * W + t1 % KW] : __float2bfloat16_rn(0.f);
+                        w[j] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) w[j] = 0u;
+                }
+                const uint32_t as = a0 + (uint32_t)s * kPtStage + (uint32_t)tid * 16u;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(as + (uint32_t)c * 2048u),
+                                 "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3])
+                                 : "memory");
+                fence_proxy_async_smem();
+                mbar_arrive(afull + s);
+            }
+            if (k >= 1) {
+                const int kk = k - 1, s = kk & 1;
+                mbar_wait(accf + s, (uint32_t)(kk >> 1) & 1u);
+                fence_after_sync();
+                const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)s * kPtN;
+                // row `lane` of the warp's staging: 16 chunks of 16 B, chunk j at (j ^ (lane & 15))
+#pragma unroll
+                for (int c = 0; c < kPtN / 32; ++c) {
+                    float v[32];
+                    rows::tmem_ld32(tb + (uint32_t)c * 32u, v);
+                    tmem_wait_ld();
+                    if (c == kPtN / 32 - 1) {   // accumulator drained: hand the slot back
+                        fence_before_sync();
+                        mbar_arrive(acce + s);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t u[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+                            u[e] = *reinterpret_cast<uint32_t *>(&h);
+                        }
+                        const uint32_t ch = (uint32_t)((c * 4 + j) ^ (lane & 15));
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(ob + (uint32_t)lane * 256u + ch * 16u),
+                                     "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3])
+                                     : "memory");
+                    }
+                }
+                __syncwarp();
+                // the warp's 32 consecutive pixels are 8 KB contiguous in O: 512 B per store instruction
+                const int wpix0 = ((int)blockIdx.x + kk * (int)gridDim.x) * 128 + warp * 32;
+                uint4 *wo = reinterpret_cast<uint4 *>(O + (size_t)wpix0 * kPtN);
+#pragma unroll 4
+                for (int i = 0; i < 16; ++i) {
+                    const int u = i * 32 + lane, r = u >> 4, j = u & 15;   // row r, chunk j of the warp's block
+                    if (wpix0 + r < npix) wo[u] = ld_shared_v4(ob + (uint32_t)r * 256u + (uint32_t)((j ^ (r & 15)) * 16));
+                }
+                __syncwarp();
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 4) tmem_dealloc_dyn(tmem, 256);
 }
 
 // Weight gradient: thread = channel n (blockDim = N), block = a range of
@@ -175,6 +342,20 @@ size_t primary_workspace_bytes(capsconv_op_t op, const Problem &p) {
 
 cudaError_t primary_fwd(const Problem &p, const void *img, const void *K, void *O, cudaStream_t st) {
     const int N = (int)(p.Cout * p.D3), ngrp = N / 32, wpb = ngrp < 4 ? ngrp : 4;
+    if (p.dt == CAPSCONV_BF16 && N == kPtN && (p.KH == 5 || p.KH == 3) &&
+        !(kProbes && probe_env("CAPSCONV_PRIMARY_SIMT"))) {
+        const int64_t npix = p.B * p.Ho * p.Wo;
+        const int grid = (int)std::min<int64_t>((npix + 127) / 128, device_info().num_sms);
+        const auto *ip = static_cast<const __nv_bfloat16 *>(img);
+        const auto *kp = static_cast<const __nv_bfloat16 *>(K);
+        auto *op = static_cast<__nv_bfloat16 *>(O);
+        auto kern = p.KH == 5 ? primary_tc_fwd_kernel<5, 5> : primary_tc_fwd_kernel<3, 3>;
+        cudaError_t e = smem_optin(reinterpret_cast<const void *>(kern), (int)kPtSmem);
+        if (e != cudaSuccess) return e;
+        e = launch_k(kern, dim3(grid), dim3(160), kPtSmem, st, ip, kp, op, (int)p.B, (int)p.H, (int)p.W);
+        note_launches(1);
+        return e;
+    }
     const int ppb = 64 * (4 / wpb);
     const int64_t npix = p.B * p.Ho * p.Wo;
     const size_t smem = (size_t)p.KH * p.KW * N * sizeof(float);
