@@ -261,6 +261,137 @@ __global__ void __launch_bounds__(160, 1) primary_tc_fwd_kernel(const __nv_bfloa
     if (warp == 4) tmem_dealloc_dyn(tmem, 256);
 }
 
+// Weight gradient on the tensor cores (bf16, N = 128, KH*KW <= 64): the
+// transposed product dK^T[n][t] = sum_pix dO[pix][n] * A[pix][t] with the
+// pixels as the reduction.  A = dO^T is MN-major straight from two TMA boxes
+// (64 channels x 128 pixels, SWIZZLE_128B) per 128-pixel tile; B = the
+// im2col tile (128 pixels x 64 taps, zero past KH*KW), MN-major in the same
+// swizzled layout, gathered by four producer warps (row = pixel, 16-byte
+// chunk c at c ^ (row & 7)); eight 128x64x16 MMAs per tile accumulate into
+// one TMEM accumulator for the CTA's whole pixel range; the producers then
+// write the CTA's partial (fixed-order sum in primary_dk_reduce).
+constexpr int kPdStg = 3;
+constexpr uint32_t kPdA = 2u * 16384u, kPdB = 16384u, kPdStage = kPdA + kPdB;
+constexpr uint32_t kPdSmem = 1024u + kPdStg * kPdStage;
+
+template <int KH, int KW>
+__global__ void __launch_bounds__(192, 1) primary_tc_dk_kernel(const __grid_constant__ CUtensorMap tmD,
+                                                               const __nv_bfloat16 *__restrict__ img,
+                                                               float *__restrict__ part, int B, int H, int W) {
+    using namespace umma;
+    extern __shared__ __align__(1024) uint8_t smd[];
+    __shared__ uint64_t full[kPdStg], empty[kPdStg], accf;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t s0 = (smem_u32(smd) + 1023u) & ~1023u;
+    constexpr int ntap = KH * KW;
+    const int Ho = H - KH + 1, Wo = W - KW + 1, npix = B * Ho * Wo;
+    const int ntiles = (npix + 127) / 128;
+    const int nk = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPdStg; ++i) {
+            mbar_init(full + i, 1 + 128);
+            mbar_init(empty + i, 1);
+        }
+        mbar_init(&accf, 1);
+        mbar_fence_init();
+    }
+    if (warp == 5) tmem_alloc_dyn(&tslot, 64);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = tslot;
+    pdl_wait();
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA: dO^T boxes
+        if (lane == 0) {
+            for (int k = 0; k < nk; ++k) {
+                const int s = k % kPdStg;
+                mbar_wait(empty + s, ((uint32_t)(k / kPdStg) & 1u) ^ 1u);
+                const uint32_t stg = s0 + (uint32_t)s * kPdStage, mb = smem_u32(full + s);
+                mbar_arrive_expect_tx(full + s, kPdA);
+                const int r0 = ((int)blockIdx.x + k * (int)gridDim.x) * 128;
+                rows::tma_load2d(stg, &tmD, 0, r0, mb);
+                rows::tma_load2d(stg + 16384u, &tmD, 64, r0, mb);
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------------------ MMA
+        const uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+        for (int k = 0; k < nk; ++k) {
+            const int s = k % kPdStg;
+            mbar_wait(full + s, (uint32_t)(k / kPdStg) & 1u);
+            fence_after_sync();
+            const uint32_t stg = s0 + (uint32_t)s * kPdStage;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint64_t ad = rows::sdesc(stg + (uint32_t)kk * 2048u, 16384u, 1024u, 128);
+                const uint64_t bd = rows::sdesc(stg + kPdA + (uint32_t)kk * 2048u, 16384u, 1024u, 128);
+                rows::mma_ss_elect(tmem, ad, bd, idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            }
+            if (elect_one()) mma_commit(empty + s);
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(&accf);
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ im2col producers (warps 1-4), then the partial
+        const int row = threadIdx.x - 32;   // pixel row of the tile
+        for (int k = 0; k < nk; ++k) {
+            const int s = k % kPdStg;
+            mbar_wait(empty + s, ((uint32_t)(k / kPdStg) & 1u) ^ 1u);
+            const int pix = ((int)blockIdx.x + k * (int)gridDim.x) * 128 + row;
+            uint32_t w[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w[j] = 0u;
+            if (pix < npix) {
+                const int y = pix % Wo, x = (pix / Wo) % Ho, b = pix / (Wo * Ho);
+                const __nv_bfloat16 *ip = img + ((size_t)b * H + x) * W + y;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int t0 = 2 * j, t1 = 2 * j + 1;
+                    if (t0 < ntap) {
+                        __nv_bfloat162 h;
+                        h.x = ip[(size_t)(t0 / KW) * W + t0 % KW];
+                        h.y = t1 < ntap ? ip[(size_t)(t1 / KW) * W + t1 % KW] : __float2bfloat16_rn(0.f);
+                        w[j] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                }
+            }
+            const uint32_t rb = s0 + (uint32_t)s * kPdStage + kPdA + (uint32_t)row * 128u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(rb + (uint32_t)((c ^ (row & 7)) * 16)),
+                             "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3])
+                             : "memory");
+            fence_proxy_async_smem();
+            mbar_arrive(full + s);
+        }
+        if (nk > 0) {
+            mbar_wait(&accf, 0u);
+            fence_after_sync();
+            const int q = warp & 3, n = q * 32 + lane;   // TMEM lane quarter of this warp = channels n
+            float v[32];
+            rows::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16), v);
+            tmem_wait_ld();
+            float *pp = part + (size_t)blockIdx.x * ntap * kPtN + n;
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+                if (t < ntap) pp[(size_t)t * kPtN] = v[t];
+            if (ntap > 32) {
+                rows::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32u, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int t = 0; t < 32; ++t)
+                    if (32 + t < ntap) pp[(size_t)(32 + t) * kPtN] = v[t];
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 5) tmem_dealloc_dyn(tmem, 64);
+}
+
 // Weight gradient: thread = channel n (blockDim = N), block = a range of
 // image rows (b, x); the KH x KW window of the image slides along y in
 // registers (KH new values per output pixel, warp-wide broadcasts) and meets
@@ -374,6 +505,24 @@ cudaError_t primary_fwd(const Problem &p, const void *img, const void *K, void *
 
 cudaError_t primary_bwd_kernel(const Problem &p, const void *img, const void *dO, float *dK, void *ws, cudaStream_t st) {
     const int N = (int)(p.Cout * p.D3);
+    if (p.dt == CAPSCONV_BF16 && N == kPtN && (p.KH == 5 || p.KH == 3 || p.KH == 7) &&
+        !(kProbes && probe_env("CAPSCONV_PRIMARY_SIMT"))) {
+        const int64_t npix = p.B * p.Ho * p.Wo;
+        const int grid = (int)std::min<int64_t>((npix + 127) / 128, device_info().num_sms);
+        CUtensorMap tm;
+        if (!rows::make_rows_map2(&tm, dO, npix, kPtN, 64, 128, 128)) return cudaErrorInvalidValue;
+        auto kern = p.KH == 5 ? primary_tc_dk_kernel<5, 5>
+                    : p.KH == 3 ? primary_tc_dk_kernel<3, 3> : primary_tc_dk_kernel<7, 7>;
+        cudaError_t e = smem_optin(reinterpret_cast<const void *>(kern), (int)kPdSmem);
+        if (e != cudaSuccess) return e;
+        e = launch_k(kern, dim3(grid), dim3(192), kPdSmem, st, tm, static_cast<const __nv_bfloat16 *>(img),
+                     static_cast<float *>(ws), (int)p.B, (int)p.H, (int)p.W);
+        if (e != cudaSuccess) return e;
+        const int n_out = (int)(p.KH * p.KW) * N;
+        primary_dk_reduce<<<(n_out + 255) / 256, 256, 0, st>>>(static_cast<const float *>(ws), dK, grid, n_out);
+        note_launches(2);
+        return cudaGetLastError();
+    }
     const int nblk = primary_dk_blocks(p);
     const int rows = (int)(p.B * p.Ho), rpb = (rows + nblk - 1) / nblk;
     float *part = static_cast<float *>(ws);

@@ -122,6 +122,8 @@ PRIMARY_CASES = [
     (2, 11, 9, 3, 32, 1),
     (2, 13, 17, 7, 64, 2),
     (1, 9, 12, 5, 256, 4),
+    (2, 15, 14, 7, 128, 1),      # tensor-core dK with 49 taps; CUDA-core forward (49 > 32 taps)
+    (3, 10, 12, 3, 128, 2),      # tensor-core fwd and dK with 9 taps, Cout = 2
 ]
 
 
@@ -129,8 +131,9 @@ PRIMARY_CASES = [
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
 def test_primary_layer_kernels(cc, oracle_mod, case, dtype):
     """The one-channel plain-convolution kernels (csrc/primary.cu: C = D1 = D2
-    = 1) against the oracle, fwd and dK, random data; also exact-integer data
-    bitwise (sums of at most 49 products of small integers)."""
+    = 1; tcgen05 for bf16 with 128 channels, CUDA cores otherwise) against the
+    oracle, fwd and dK, random data; also exact-integer data bitwise (sums of
+    at most 49 products of small integers; ragged last 128-pixel tiles)."""
     B, H, W, K, N, Cout = case
     L = capsinputs.Layer(B=B, H=H, W=W, C=1, Cout=Cout, KH=K, KW=K, D1=1, D2=1, D3=N // Cout, stride=1)
     Ho, Wo = H - K + 1, W - K + 1
