@@ -779,7 +779,7 @@ def main():
     (bli, bkind), bavg, bbytes = best
     traffic = None
     try:   # the committed captures are of the bf16 rows kernels of the stack
-        if dtype == torch.bfloat16 and args.layout == "rows" and args.config == "stack":
+        if dtype == torch.bfloat16 and args.layout == "rows" and args.config in ("stack", "pcapsnet_train"):
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
                 traffic = json.load(f).get(pass_name(bli, bkind))
     except Exception:

@@ -12,9 +12,10 @@ o = (d1 * C + c) * D2 + d2, so the primary output buffer is the stack input
 and the stack's dX is the primary layer's dO, without a copy.  The image
 gradient is not formed (nothing consumes it).
 
-Optimizer: plain SGD on fp32 master copies of every weight,
-capsconv_sgd_update (which also rewrites the working bf16 copy the
-convolution calls read).  The whole step is capturable in one CUDA graph.
+Optimizer: plain SGD on fp32 master copies of every weight, one
+capsconv_sgd_update over flat buffers holding all weights, masters and dKs
+(it also rewrites the working bf16 copies the convolution calls read).  The
+whole step is capturable in one CUDA graph.
 """
 from __future__ import annotations
 
@@ -47,13 +48,33 @@ class CapsTrainer:
         self.stack = CapsStack(specs, H, W, D, batch, weights, device, ops=ops, group=group, overlap=overlap,
                                layout="rows", dk_stream=dk_stream)
         self.dtype = self.stack.dtype
-        self.KP = KP.to(self.device, self.dtype).contiguous()
-        # fp32 master copies (the optimizer's state) of every weight
-        self.masterP = self.KP.float().clone()
-        self.masters = [k.float().clone() for k in self.stack.K]
+        # every weight, its fp32 master and its dK live in three flat buffers
+        # (primary first, then the stack's layers), so the optimizer step is one
+        # capsconv_sgd_update over all of them; every piece starts 16-byte aligned
+        shapes = [tuple(KP.shape)] + [tuple(k.shape) for k in self.stack.K]
+        sizes = [int(torch.Size(sh).numel()) for sh in shapes]
+        if any(n % 8 for n in sizes):
+            raise ValueError("weight sizes must be multiples of 8 elements (16-byte aligned pieces)")
+        total = sum(sizes)
+        self.kflat = torch.empty(total, dtype=self.dtype, device=self.device)
+        self.mflat = torch.empty(total, dtype=torch.float32, device=self.device)
+        self.gflat = torch.zeros(total, dtype=torch.float32, device=self.device)
+        views = []
+        off = 0
+        for sh, n in zip(shapes, sizes):
+            views.append((self.kflat[off:off + n].view(sh), self.mflat[off:off + n].view(sh),
+                          self.gflat[off:off + n].view(sh)))
+            off += n
+        src = [KP.to(self.device, self.dtype)] + list(self.stack.K)
+        for (kv, mv, gv), w in zip(views, src):
+            kv.copy_(w)
+            mv.copy_(kv.float())
+        self.KP, self.masterP, self.dKP = views[0]
+        self.stack.K = [v[0] for v in views[1:]]
+        self.masters = [v[1] for v in views[1:]]
+        self.stack.dK = [v[2] for v in views[1:]]
         # the primary output = the stack's first capsule map (rows layout)
         self.prim = torch.empty((batch, H, W, 1, 1, C0 * D * D), dtype=self.dtype, device=self.device)
-        self.dKP = torch.empty(self.KP.shape, dtype=torch.float32, device=self.device)
 
     @property
     def specs(self):
@@ -91,8 +112,6 @@ class CapsTrainer:
         ops.bwd_kernel(img, dprim, 1, self.KPH, self.KPW, out=self.dKP)
         if timer: timer.end(-1, "dK")
         if timer: timer.begin(-1, "opt")
-        ops.sgd_update(self.masterP, self.dKP, self.lr, self.KP)
-        for m, g, k in zip(self.masters, self.stack.dK, self.stack.K):
-            ops.sgd_update(m, g, self.lr, k)
+        ops.sgd_update(self.mflat, self.gflat, self.lr, self.kflat)   # every weight in one pass
         if timer: timer.end(-1, "opt")
         return [self.masterP] + self.masters
