@@ -441,13 +441,18 @@ __global__ void __launch_bounds__(256) primary_dk_kernel(const T *__restrict__ i
         for (int q = 0; q < KW; ++q) pp[(size_t)(p * KW + q) * N] = acc[p][q];
 }
 
+// One warp per output element: lane l adds partials l, l+32, ... in order,
+// then a fixed butterfly over the lanes -- a fixed summation order for every
+// element (deterministic), with nblk/32 loads per lane instead of nblk.
 __global__ void __launch_bounds__(256) primary_dk_reduce(const float *__restrict__ part, float *__restrict__ dK,
                                                          int nblk, int n_out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (i >= n_out) return;
     float s = 0.f;
-    for (int k = 0; k < nblk; ++k) s += part[(size_t)k * n_out + i];   // fixed order: deterministic
-    dK[i] = s;
+    for (int k = lane; k < nblk; k += 32) s += part[(size_t)k * n_out + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dK[i] = s;
 }
 
 int primary_dk_blocks(const Problem &p) {
@@ -519,7 +524,7 @@ cudaError_t primary_bwd_kernel(const Problem &p, const void *img, const void *dO
                      static_cast<float *>(ws), (int)p.B, (int)p.H, (int)p.W);
         if (e != cudaSuccess) return e;
         const int n_out = (int)(p.KH * p.KW) * N;
-        primary_dk_reduce<<<(n_out + 255) / 256, 256, 0, st>>>(static_cast<const float *>(ws), dK, grid, n_out);
+        primary_dk_reduce<<<(n_out + 7) / 8, 256, 0, st>>>(static_cast<const float *>(ws), dK, grid, n_out);
         note_launches(2);
         return cudaGetLastError();
     }
@@ -540,7 +545,7 @@ cudaError_t primary_bwd_kernel(const Problem &p, const void *img, const void *dO
     else { CAPSCONV_PRIMARY_DK(7) }
 #undef CAPSCONV_PRIMARY_DK
     const int n_out = (int)(p.KH * p.KW) * N;
-    primary_dk_reduce<<<(n_out + 255) / 256, 256, 0, st>>>(part, dK, nblk, n_out);
+    primary_dk_reduce<<<(n_out + 7) / 8, 256, 0, st>>>(part, dK, nblk, n_out);
     note_launches(2);
     return cudaGetLastError();
 }

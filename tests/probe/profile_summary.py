@@ -66,6 +66,11 @@ CAPS_R2C = [("L%d_%s" % (l, o), "r2c_L%d_%s.ncu-rep" % (l, o), 0, desc) for (l, 
     (4, "dK", "rows_fc_kernel mode 2")]]
 
 
+# Round 2, the training step's tensor-core primary kernels (tests/probe/prof_r2_train.sh)
+CAPS_R2T = [("P_fwd", "r2_P_fwd.ncu-rep", 0, "primary_tc_fwd_kernel<5,5>: im2col tile -> 2 MMAs 128x128x16, staged 512-B stores"),
+            ("P_dK", "r2_P_dK.ncu-rep", 0, "primary_tc_dk_kernel<5,5>: dO^T MN-major TMA boxes x im2col, 8 MMAs 128x64x16 per tile")]
+
+
 def full_summaries(caps, rnd, traffic, tag=None, src=None):
     tag = tag or "r%d" % rnd
     src = src or (PROF if rnd == 1 else PROF)
@@ -94,7 +99,7 @@ def full_summaries(caps, rnd, traffic, tag=None, src=None):
                 d[k] = (float(v[i].replace(",", "")), u[i])
         tb = int(d["dram__bytes_read.sum"][0] * SCALE[d["dram__bytes_read.sum"][1]] +
                  d["dram__bytes_write.sum"][0] * SCALE[d["dram__bytes_write.sum"][1]])
-        traffic[name if tag == "r2c" else tag + "_" + name] = tb
+        traffic[name if tag in ("r2c", "r2t") else tag + "_" + name] = tb
         out.append("  %-80s %d" % ("dram read+write bytes per launch", tb))
         out.append("")
     open(os.path.join(PROF, "%s_ncu_full_summary.txt" % tag), "w").write("\n".join(out) + "\n")
@@ -129,6 +134,7 @@ if __name__ == "__main__":
     full_summaries(CAPS_R2, 2, traffic, tag="r2a")
     full_summaries(CAPS_R2B, 2, traffic, tag="r2b")
     full_summaries(CAPS_R2C, 2, traffic, tag="r2c")
+    full_summaries(CAPS_R2T, 2, traffic, tag="r2t")
     traffic["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the ncu --set full "
                         "captures in profiles/ (tests/probe/profile_summary.py); unprefixed keys: round-2 final build "
                         "(r2c captures of the kernels bench.py times); r2b_*: before dynamic strips / PDL packs; r2a_*: earlier round-2 rows kernels; r1_*: "
@@ -138,3 +144,4 @@ if __name__ == "__main__":
     launches(2, "--steps 2 --warmup 1", tag="r2")
     launches(2, "--steps 2 --warmup 1 --no-parity", tag="r2b")
     launches(2, "--steps 2 --warmup 1 --no-parity", tag="r2c")
+    launches(2, "--config pcapsnet_train --steps 2 --warmup 1 --no-parity", tag="r2t")
