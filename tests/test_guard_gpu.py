@@ -24,6 +24,8 @@ CASES = [
     (37, 4, 4, 32, 10, 4, 4, 4, 4, 4, 1),    # rows FC GEMMs, ragged batch tile
     (2, 34, 17, 8, 8, 3, 3, 4, 4, 4, 1),     # several x tiles / ring wraps
     (2, 6, 5, 2, 3, 2, 3, 2, 3, 5, 1),       # generic shapes: natural path between permutations
+    (3, 28, 28, 1, 1, 5, 5, 1, 1, 128, 1),   # training-step primary layer: tcgen05 fwd / dK (bf16)
+    (2, 13, 17, 1, 2, 7, 7, 1, 1, 32, 1),    # primary layer on CUDA cores (N = 64, 7x7)
 ]
 
 
@@ -101,3 +103,19 @@ def test_guards(cc, case, dtype, layout, monkeypatch):
             assert torch.equal(b[:GUARD], r[:GUARD]), name + ": write before the workspace"
             assert torch.equal(b[-GUARD:], r[-GUARD:]), name + ": write past the workspace"
         assert torch.equal(view, plain), name + ": result differs from the unguarded call"
+
+
+def test_guard_sgd_update(cc):
+    """capsconv_sgd_update writes exactly n masters and n working copies."""
+    gen = torch.Generator().manual_seed(11)
+    for n in (5, 4096 + 6):   # ragged tails of the 4-wide vectors
+        wb, wr, w = guarded((n,), torch.float32, gen)
+        w.copy_(torch.rand(n, generator=gen).to(DEV))
+        wr = wb.clone()
+        g = torch.rand(n, generator=gen).to(DEV)
+        ob, orf, o = guarded((n,), torch.bfloat16, gen)
+        cc.sgd_update(w, g, 0.5, o)
+        torch.cuda.synchronize()
+        assert torch.equal(wb[:GUARD], wr[:GUARD]) and torch.equal(wb[-GUARD:], wr[-GUARD:]), "master guards"
+        assert torch.equal(ob[:GUARD], orf[:GUARD]) and torch.equal(ob[-GUARD:], orf[-GUARD:]), "copy guards"
+        assert torch.equal(o, w.to(torch.bfloat16))
