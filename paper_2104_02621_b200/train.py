@@ -22,6 +22,7 @@ from __future__ import annotations
 from typing import List, Optional, Sequence
 
 import torch
+import torch.distributed as dist
 
 from .stack import CapsStack, LayerSpec
 
@@ -110,6 +111,8 @@ class CapsTrainer:
         dprim = g0.view(g0.shape[0], g0.shape[1], g0.shape[2], 1, 1, -1)
         if timer: timer.begin(-1, "dK")
         ops.bwd_kernel(img, dprim, 1, self.KPH, self.KPW, out=self.dKP)
+        if self.stack.world > 1:   # data parallel: the primary layer's dK is summed like the stack's
+            dist.all_reduce(self.dKP, op=dist.ReduceOp.SUM, group=self.stack.group)
         if timer: timer.end(-1, "dK")
         if timer: timer.begin(-1, "opt")
         ops.sgd_update(self.mflat, self.gflat, self.lr, self.kflat)   # every weight in one pass

@@ -149,3 +149,99 @@ def test_single_process_padded_stack_matches_oracle():
     np.testing.assert_allclose(st.out.numpy(), acts[-1], rtol=1e-12, atol=1e-12)
     for li in range(len(specs)):
         np.testing.assert_allclose(dKs[li].numpy(), rdKs[li], rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- training step
+class OracleTrainOps(OracleOps):
+    """OracleOps plus the rows layout (permuted around the oracle) and SGD,
+    for the product CapsTrainer on CPU (test only)."""
+
+    @staticmethod
+    def _nat(t, layout):
+        return t.permute(0, 1, 2, 4, 3, 5).contiguous() if layout == "rows" else t
+
+    @staticmethod
+    def fwd(I, K, stride, out=None, pad=0, layout="natural"):
+        O, _ = oracle.fwd(OracleTrainOps._nat(I, layout).numpy(), K.numpy(), stride, pad)
+        out.copy_(OracleTrainOps._nat(torch.from_numpy(O), layout))
+        return out
+
+    @staticmethod
+    def bwd_data(dO, K, stride, H, W, out=None, pad=0, layout="natural"):
+        dI, _ = oracle.bwd_data(OracleTrainOps._nat(dO, layout).numpy(), K.numpy(), stride, H, W, pad)
+        out.copy_(OracleTrainOps._nat(torch.from_numpy(dI), layout))
+        return out
+
+    @staticmethod
+    def bwd_kernel(I, dO, stride, KH, KW, out=None, pad=0, layout="natural"):
+        dK, _ = oracle.bwd_kernel(OracleTrainOps._nat(I, layout).numpy(), OracleTrainOps._nat(dO, layout).numpy(),
+                                  stride, KH, KW, pad)
+        out.copy_(torch.from_numpy(dK))
+        return out
+
+    @staticmethod
+    def sgd_update(w, g, lr, out=None):
+        w.copy_(torch.from_numpy(oracle.sgd_update(w.numpy(), g.numpy(), lr)))
+        if out is not None:
+            out.copy_(w)
+        return out
+
+
+TSPECS = [LayerSpec(2, 2, 3, 3, 1), LayerSpec(2, 2, 2, 2, 1)]
+TLR = 0.05
+
+
+def make_train_data():
+    g = torch.Generator().manual_seed(9)
+    weights = [torch.rand((s.KH, s.KW, s.C, s.Cout, D, D), generator=g, dtype=torch.float64) - 0.5 for s in TSPECS]
+    Kp = torch.rand((3, 3, 1, 1, 1, TSPECS[0].C * D * D), generator=g, dtype=torch.float64) - 0.5
+    img = torch.rand((GB, H + 2, W + 2, 1, 1, 1), generator=g, dtype=torch.float64) - 0.5
+    h, w = H, W
+    for s in TSPECS:
+        h, w = oracle.output_dims(h, w, s.KH, s.KW, s.stride)
+    dY = torch.rand((GB, h, w, D, TSPECS[-1].Cout, D), generator=g, dtype=torch.float64) - 0.5   # rows layout
+    return weights, Kp, img, dY
+
+
+def _train_worker(rank, world, port, out_q):
+    from paper_2104_02621_b200.train import CapsTrainer
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        weights, Kp, img, dY = make_train_data()
+        lo, hi = shard_range(GB, rank, world)
+        tr = CapsTrainer(TSPECS, H, W, D, hi - lo, Kp, weights, "cpu", TLR, ops=OracleTrainOps)
+        new = tr.step(img[lo:hi], dY[lo:hi])
+        out_q.put((rank, [m.numpy().copy() for m in new]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_training_step_equals_full_batch():
+    """Data-parallel training step: every rank ends with the same updated
+    weights -- the primary layer's included -- and they equal the full-batch
+    step (dK is a sum over the batch, so the SUM all-reduce of the shard dKs
+    is the full-batch dK)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict()
+    for _ in range(2):
+        r, ws = q.get(timeout=300)
+        res[r] = ws
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2104_02621_b200.train import CapsTrainer
+    weights, Kp, img, dY = make_train_data()
+    full = CapsTrainer(TSPECS, H, W, D, GB, Kp, weights, "cpu", TLR, ops=OracleTrainOps)
+    ref = [m.numpy().copy() for m in full.step(img, dY)]
+    assert len(ref) == len(TSPECS) + 1
+    for i in range(len(ref)):
+        np.testing.assert_array_equal(res[0][i], res[1][i])
+        np.testing.assert_allclose(res[0][i], ref[i], rtol=1e-6, atol=1e-6)
+        assert not np.array_equal(ref[i], ([Kp] + weights)[i].numpy().astype(np.float32))   # the step moved it
