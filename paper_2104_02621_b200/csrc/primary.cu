@@ -5,10 +5,11 @@
 //   O[b,x,y,n]  = sum_{p,q} img[b, x+p, y+q] * K[p, q, n]
 //   dK[p,q,n]   = sum_{b,x,y} img[b, x+p, y+q] * dO[b, x, y, n]
 // (the general kernels of simt.cu take it too, one output element per thread
-// with two loads per multiply-add, ~100x slower).  CUDA cores: K = KH*KW <= 32
-// multiply-adds per output is far too short a reduction for the tensor cores'
-// 16-deep k-steps to pay, and both passes are bounded by the N-channel map
-// they write (fwd) or read (dK).
+// with two loads per multiply-add, ~100x slower).  Both passes are bounded by
+// the N-channel map they write (fwd) or read (dK).  bf16 with N = 128 runs on
+// tcgen05 (an im2col tile gathered by producer warps is one MMA operand:
+// primary_tc_fwd_kernel, primary_tc_dk_kernel); fp32 and other widths run the
+// CUDA-core kernels (primary_fwd_kernel, primary_dk_kernel).
 #include <cuda_bf16.h>
 
 #include <algorithm>
