@@ -195,7 +195,7 @@ static capsconv_path_t choose_path(capsconv_op_t op, const Problem &p) {
         if (rows_mma(op, p)) return CAPSCONV_PATH_MMA;
         return choose_path(op, natural_of(p));
     }
-    if (mma_supported(op, p)) return CAPSCONV_PATH_MMA;
+    if (mma_supported(op, p) || primary_tc(op, p)) return CAPSCONV_PATH_MMA;
     return CAPSCONV_PATH_SIMT;
 }
 
@@ -206,14 +206,12 @@ static size_t workspace_for(capsconv_op_t op, const Problem &p) {
         // misaligned pointers take the fallback: cover both
         return std::max(rows_mma_ws(op, p), fb);
     }
-    if (choose_path(op, p) == CAPSCONV_PATH_MMA) {
-        // The MMA path falls back to SIMT for misaligned pointers, so the
-        // workspace covers both.
-        size_t a = mma_workspace_bytes(op, p), b = simt_workspace_bytes(op, p);
-        return a > b ? a : b;
-    }
-    if (primary_supported(p)) return std::max(primary_workspace_bytes(op, p), simt_workspace_bytes(op, p));
-    return simt_workspace_bytes(op, p);
+    // every kernel family that may take the call (misaligned pointers fall back
+    // to the SIMT kernels), so the workspace covers all of them
+    size_t need = simt_workspace_bytes(op, p);
+    if (mma_supported(op, p)) need = std::max(need, mma_workspace_bytes(op, p));
+    if (primary_supported(p)) need = std::max(need, primary_workspace_bytes(op, p));
+    return need;
 }
 
 static capsconv_status_t check_device() {
@@ -280,8 +278,9 @@ static cudaError_t dispatch(capsconv_op_t op, const Problem &p, const void *a, c
                             size_t ws_bytes, cudaStream_t cs) {
     if (p.layout == CAPSCONV_LAYOUT_ROWS) return dispatch_rows(op, p, a, b, out, ws, ws_bytes, cs);
     const size_t need = workspace_for(op, p);
-    if (op != CAPSCONV_OP_BWD_DATA && primary_supported(p) && aligned16(a) && aligned16(b) && aligned16(out) &&
-        aligned16(ws) && ws_bytes >= primary_workspace_bytes(op, p))   // one-channel plain convolution (primary.cu)
+    if (op != CAPSCONV_OP_BWD_DATA && primary_supported(p) && g_path_override.load() != CAPSCONV_PATH_SIMT &&
+        aligned16(a) && aligned16(b) && aligned16(out) && aligned16(ws) &&
+        ws_bytes >= primary_workspace_bytes(op, p))   // one-channel plain convolution (primary.cu)
         return op == CAPSCONV_OP_FWD ? primary_fwd(p, a, b, out, cs)
                                      : primary_bwd_kernel(p, a, b, static_cast<float *>(out), ws, cs);
     const bool mma = choose_path(op, p) == CAPSCONV_PATH_MMA && aligned16(a) && aligned16(b) && aligned16(out) &&

@@ -121,6 +121,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 // (C = D1 = D2 = 1, stride 1, no padding, N = Cout*D3 in {32, 64, 128, 256},
 // 3x3 / 5x5 / 7x7): fwd and dK (dI has no consumer; the general path takes it).
 bool primary_supported(const Problem &p);
+bool primary_tc(capsconv_op_t op, const Problem &p);   // ... and runs on tcgen05 (bf16, 128 channels)
 size_t primary_workspace_bytes(capsconv_op_t op, const Problem &p);
 cudaError_t primary_fwd(const Problem &p, const void *img, const void *K, void *O, cudaStream_t st);
 cudaError_t primary_bwd_kernel(const Problem &p, const void *img, const void *dO, float *dK, void *ws, cudaStream_t st);

@@ -472,6 +472,13 @@ bool primary_supported(const Problem &p) {
            p.B * p.Ho * p.Wo * N < ((int64_t)1 << 31);
 }
 
+bool primary_tc(capsconv_op_t op, const Problem &p) {
+    if (!primary_supported(p) || p.dt != CAPSCONV_BF16 || p.Cout * p.D3 != kPtN) return false;
+    if (op == CAPSCONV_OP_FWD) return p.KH == 3 || p.KH == 5;                 // <= 32 taps per im2col row
+    if (op == CAPSCONV_OP_BWD_KERNEL) return p.KH == 3 || p.KH == 5 || p.KH == 7;   // <= 64 taps
+    return false;
+}
+
 size_t primary_workspace_bytes(capsconv_op_t op, const Problem &p) {
     if (op != CAPSCONV_OP_BWD_KERNEL) return 0;
     return (size_t)primary_dk_blocks(p) * (size_t)(p.KH * p.KW) * (size_t)(p.Cout * p.D3) * sizeof(float);
@@ -479,8 +486,7 @@ size_t primary_workspace_bytes(capsconv_op_t op, const Problem &p) {
 
 cudaError_t primary_fwd(const Problem &p, const void *img, const void *K, void *O, cudaStream_t st) {
     const int N = (int)(p.Cout * p.D3), ngrp = N / 32, wpb = ngrp < 4 ? ngrp : 4;
-    if (p.dt == CAPSCONV_BF16 && N == kPtN && (p.KH == 5 || p.KH == 3) &&
-        !(kProbes && probe_env("CAPSCONV_PRIMARY_SIMT"))) {
+    if (primary_tc(CAPSCONV_OP_FWD, p) && !(kProbes && probe_env("CAPSCONV_PRIMARY_SIMT"))) {
         const int64_t npix = p.B * p.Ho * p.Wo;
         const int grid = (int)std::min<int64_t>((npix + 127) / 128, device_info().num_sms);
         const auto *ip = static_cast<const __nv_bfloat16 *>(img);
@@ -511,8 +517,7 @@ cudaError_t primary_fwd(const Problem &p, const void *img, const void *K, void *
 
 cudaError_t primary_bwd_kernel(const Problem &p, const void *img, const void *dO, float *dK, void *ws, cudaStream_t st) {
     const int N = (int)(p.Cout * p.D3);
-    if (p.dt == CAPSCONV_BF16 && N == kPtN && (p.KH == 5 || p.KH == 3 || p.KH == 7) &&
-        !(kProbes && probe_env("CAPSCONV_PRIMARY_SIMT"))) {
+    if (primary_tc(CAPSCONV_OP_BWD_KERNEL, p) && !(kProbes && probe_env("CAPSCONV_PRIMARY_SIMT"))) {
         const int64_t npix = p.B * p.Ho * p.Wo;
         const int grid = (int)std::min<int64_t>((npix + 127) / 128, device_info().num_sms);
         CUtensorMap tm;
