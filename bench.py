@@ -58,7 +58,8 @@ def parse():
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--layout", default=None, choices=["rows", "natural"],
                     help="capsule-tensor layout of the stack's activations (include/capsconv.h); default rows for "
-                         "bf16 (its tensor-core kernels), natural for fp32 (the SIMT kernels' own layout)")
+                         "bf16 (its tensor-core kernels), natural for fp32 (the SIMT kernels' own layout) and for "
+                         "the padded stack_same (the natural tensor-core kernels take padding)")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-bench oracle parity check")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = 1024 images per rank (default), strong = 1024 images shared by the ranks")
@@ -66,8 +67,8 @@ def parse():
                     help="override the global batch (e.g. 128/256/512: one rank's share of the batch-1024 stack "
                          "at 8/4/2 GPUs -- the compute side of strong scaling on one GPU)")
     args = ap.parse_args()
-    if args.layout is None:
-        args.layout = "natural" if args.dtype == "fp32" else "rows"
+    if args.layout is None:   # the rows kernels take bf16 unpadded layers; the natural ones pad (NEXT-2) and fp32
+        args.layout = "natural" if (args.dtype == "fp32" or args.config == "stack_same") else "rows"
     return args
 
 
