@@ -377,7 +377,8 @@ def parity_check(pkg, specs, H, W, D, PB, weights, X_nat, dY_nat, dtype, dev, la
     import numpy as np
     import oracle
     from paper_2104_02621_b200.stack import CapsStack
-    st = CapsStack(specs, H, W, D, PB, weights, dev, overlap=False, layout=layout)
+    st = CapsStack(specs, H, W, D, PB, weights, dev, overlap=False, layout=layout,
+                   distributed=False)   # rank 0 alone runs the check: no collectives
     perm = (lambda t: t.permute(0, 1, 2, 4, 3, 5).contiguous()) if layout == "rows" else (lambda t: t)
     st.step(perm(X_nat.to(dev)), perm(dY_nat.to(dev)))
     torch.cuda.synchronize()
@@ -549,7 +550,7 @@ def train_parity(pkg, specs, H, W, D, PB, Kp, weights, img_nat, dY_nat, dev):
     import oracle
     from paper_2104_02621_b200.train import CapsTrainer
     lr = capsinputs.TRAIN_LR
-    tr = CapsTrainer(specs, H, W, D, PB, Kp, weights, dev, lr)
+    tr = CapsTrainer(specs, H, W, D, PB, Kp, weights, dev, lr, distributed=False)   # rank 0 alone: no collectives
     tr.step(img_nat.to(dev), dY_nat.permute(0, 1, 2, 4, 3, 5).contiguous().to(dev))
     torch.cuda.synchronize()
     f64 = lambda t: t.detach().to("cpu", torch.float64).numpy()  # noqa: E731

@@ -46,7 +46,7 @@ def shard_range(global_batch: int, rank: int, world: int):
 class CapsStack:
     def __init__(self, specs: Sequence[LayerSpec], H: int, W: int, D: int, batch: int, weights: List[torch.Tensor],
                  device, ops=None, group=None, overlap: bool = True, layout: str = "natural",
-                 dk_stream: bool = True):
+                 dk_stream: bool = True, distributed: bool = True):
         if ops is None:
             from . import capsconv as ops
         self.ops = ops
@@ -60,7 +60,10 @@ class CapsStack:
         self.batch = batch
         self.D = D
         self.group = group
-        self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+        # distributed=False: a rank-local stack (no collectives) even inside a
+        # process group, e.g. a check one rank runs on its own
+        self.world = (dist.get_world_size(group) if (distributed and dist.is_available() and dist.is_initialized())
+                      else 1)
         self.overlap = overlap and self.device.type == "cuda"
         self.K = [w.to(self.device).contiguous() for w in weights]
         # spatial extents per layer

@@ -30,7 +30,7 @@ from .stack import CapsStack, LayerSpec
 class CapsTrainer:
     def __init__(self, specs: Sequence[LayerSpec], H: int, W: int, D: int, batch: int,
                  primary_kernel: torch.Tensor, weights: List[torch.Tensor], device, lr: float,
-                 ops=None, group=None, overlap: bool = True, dk_stream: bool = True):
+                 ops=None, group=None, overlap: bool = True, dk_stream: bool = True, distributed: bool = True):
         if ops is None:
             from . import capsconv as ops
         self.ops = ops
@@ -47,7 +47,7 @@ class CapsTrainer:
         self.KPH, self.KPW = int(KP.shape[0]), int(KP.shape[1])
         self.Himg, self.Wimg = H + self.KPH - 1, W + self.KPW - 1     # valid convolution onto H x W
         self.stack = CapsStack(specs, H, W, D, batch, weights, device, ops=ops, group=group, overlap=overlap,
-                               layout="rows", dk_stream=dk_stream)
+                               layout="rows", dk_stream=dk_stream, distributed=distributed)
         self.dtype = self.stack.dtype
         # every weight, its fp32 master and its dK live in three flat buffers
         # (primary first, then the stack's layers), so the optimizer step is one
