@@ -165,3 +165,19 @@ def test_layout_argument(cc):
     assert rows >= nat + n_in + n_out
     with pytest.raises(ValueError):
         cc.workspace_bytes(cc.OP_FWD, torch.float32, ext, "columns")
+
+
+def test_sgd_update_validation(cc):
+    """capsconv_sgd_update validates before any launch (no device needed):
+    unknown dtype (4), n < 0 or a non-finite lr (2), NULL pointers (1); n = 0
+    is a no-op that returns OK even with NULL pointers."""
+    lib = cc.load_library()
+    f = lib.capsconv_sgd_update
+    buf = (ctypes.c_float * 8)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    lr = ctypes.c_float(0.1)
+    assert f(7, 4, lr, p, p, p, None) == 4 and b"dtype" in lib.capsconv_last_error()
+    assert f(0, -1, lr, p, p, p, None) == 2
+    assert f(0, 4, ctypes.c_float(float("nan")), p, p, p, None) == 2 and b"learning rate" in lib.capsconv_last_error()
+    assert f(0, 4, lr, None, p, p, None) == 1 and b"NULL" in lib.capsconv_last_error()
+    assert f(1, 0, lr, None, None, None, None) == 0
